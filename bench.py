@@ -1,0 +1,381 @@
+#!/usr/bin/env python
+"""Benchmark: trajectory problems solved per second at a fixed number of AM
+sweeps (BASELINE.json metric), on 1..8 B200s, plus the FP64-pipe roofline.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1] [--impl ours|reference]
+
+A step is one pass of the hot path over one goal batch: solve (fixed sweeps,
+tol=0 as the reference's bench-kernels uses) + fused scoring/argmin.
+* value: device-resident inputs, CUDA events on the launching stream around
+  each step, L2 flushed between steps (256 MiB write), max over ranks.
+* e2e:   the public API from pinned host buffers (planner.plan_batch ->
+  bmpc_plan_host: H2D, solve, score, D2H inside the timed region).
+* roofline: algorithmic fp64 work of the persistent AM kernel
+  (W(n,m,nb) slots per instance per sweep; 2 flops per
+  slot) / its CUDA-event duration, against the DFMA peak measured live.
+Multi-GPU (torchrun): weak scaling, each rank solves its own contiguous block
+of l goal columns of one shared scene; the per-shard winners are all-gathered
+(the only collective) to form the global argmin.
+--impl reference: the CPU oracle port of the reference (oracle/am_oracle.py +
+oracle/am_oracle.c, the reference's algorithm op for op) on all host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "trajectory problems solved/sec (fixed AM iters)"
+
+
+def work_slots(n: int, m: int, nb: int) -> int:
+    """Algorithmic fp64-pipe slots per instance per AM sweep."""
+    return 33 * m * n + 97 * n + 21 * n * nb + 3 * nb * nb + 24 * nb
+
+
+# ---------------------------------------------------------------- clocks ----
+class ClockSampler:
+    def __init__(self, index: int, period_ms: int = 100):
+        self.index, self.period, self.rows, self._stop = index, period_ms, [], threading.Event()
+        self.t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                r = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                    "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                   timeout=5)
+                if r.returncode == 0 and r.stdout.strip():
+                    self.rows.append([s.strip() for s in r.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(self.period / 1000.0)
+
+    def __enter__(self):
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if "Active" in r[3 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------- workloads ----
+def make_step_workload(cfg_name: str, world: int, rank: int):
+    from paper_2109_10392_b200.scenes import CONFIGS, make_workload
+
+    cfg = CONFIGS[cfg_name]
+    if cfg.scenes == 1:
+        # one scene, world * l goals; rank owns a contiguous block of l columns
+        W = make_workload(cfg_name, l=cfg.l * world)
+        W = W.columns(rank * cfg.l, (rank + 1) * cfg.l)
+        offset = rank * cfg.l
+    else:
+        W = make_workload(cfg_name, seed0=rank * cfg.scenes)
+        offset = 0
+    return cfg, W, offset
+
+
+# ------------------------------------------------------------ CPU oracle ----
+def _cpu_worker(args):
+    cfg_name, l_lo, l_hi, iters, world_l = args
+    from threadpoolctl import threadpool_limits
+
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import am_oracle as O
+
+    from paper_2109_10392_b200.scenes import CONFIGS, make_workload
+
+    cfg = CONFIGS[cfg_name]
+    with threadpool_limits(1):
+        W = make_workload(cfg_name, l=world_l, scenes=1)
+        o = O.OracleSolver(cfg.n, cfg.t_f, cfg.degree, cfg.m)
+        t = time.perf_counter()
+        r = o.solve(W.xi_x[0], W.xi_y[0], W.b_xy[:, l_lo:l_hi], W.b_psi[:, l_lo:l_hi], W.a, W.b,
+                    W.v_min, W.v_max, W.a_max, iters, kernel="c")
+        sc = o.score(r, W.xi_x[0], W.xi_y[0], W.a, W.b, kind="cruise", v_cruise=20.0)
+        return time.perf_counter() - t, l_hi - l_lo, sc["best_index"]
+
+
+def cpu_oracle_rate(cfg_name: str, goals: int, iters: int, procs: int, reps: int = 1):
+    """Aggregate problems/s of the oracle port: `procs` processes, 1 BLAS thread each,
+    disjoint goal blocks of one scene (SURVEY.md 8d CPU-baseline recipe)."""
+    import multiprocessing as mp
+
+    per = int(math.ceil(goals / procs))
+    jobs = [(cfg_name, i * per, min(goals, (i + 1) * per), iters, goals) for i in range(procs)
+            if i * per < goals]
+    ctx = mp.get_context("spawn")
+    best = None
+    with ctx.Pool(len(jobs)) as pool:
+        pool.map(_cpu_worker, [(cfg_name, 0, 1, 1, goals)] * len(jobs))  # warm-up imports
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            pool.map(_cpu_worker, jobs)
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+    return goals / best, best, len(jobs)
+
+
+# ---------------------------------------------------------------- our arm ----
+def run_ours(args, rank, world, local_rank):
+    import ctypes
+
+    import torch
+
+    from paper_2109_10392_b200 import _native as nat
+    from paper_2109_10392_b200 import device as D
+    from paper_2109_10392_b200 import make_solver
+    from paper_2109_10392_b200.planner import FilterLimits, MetaCostSpec, _spec_struct, plan_batch
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    cfg, W, offset = make_step_workload(args.config, world, rank)
+    iters = args.iters or cfg.iters
+    solver = make_solver(W.n, W.t_f, W.degree, W.m)
+    ctx = solver._context()
+    lib = nat.load()
+    L = W.L
+    nb, n = solver.basis.n_b, solver.basis.grid.n
+    spec = MetaCostSpec("cruise", v_cruise=20.0)
+    limits = FilterLimits()
+    sspec = _spec_struct(spec, limits)
+    stream = torch.cuda.current_stream()
+    sp = ctypes.c_void_p(stream.cuda_stream)
+
+    prob = D.DeviceProblem.from_host(n, W.xi_x, W.xi_y, W.b_xy, W.b_psi, W.l, W.a, W.b, W.v_min,
+                                     W.v_max, W.a_max, device=dev)
+    pstruct = prob.c_struct()
+    sol = D.alloc_solution(nb, n, L, iters, False, dev)
+    sc = D.alloc_score(L, prob.S, dev)
+    opts = nat.SolveOpts(max_iter=iters, tol=0.0)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    launches_per_step = 6  # solve: pack, am_solve, first_converged; score: pack, score, argmin
+
+    def step():
+        out = D.solution_struct(sol)
+        nat.check(lib.bmpc_solve(ctx, ctypes.byref(pstruct), ctypes.byref(opts), ctypes.byref(out), sp))
+        nat.check(lib.bmpc_score(ctx, ctypes.byref(pstruct), D.ptr(sol.c_x), D.ptr(sol.c_y),
+                                 D.ptr(sol.c_psi), D.ptr(sol.res_final), ctypes.byref(sspec),
+                                 ctypes.byref(D.score_struct(sc)), sp))
+        return out
+
+    def kernel_only():
+        out = D.solution_struct(sol)
+        nat.check(lib.bmpc_sweeps(ctx, ctypes.byref(pstruct), ctypes.byref(opts), iters, 0, 0, None,
+                                  0, ctypes.byref(out), sp))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    t_local = sum(step_ms)
+    # global argmin across shards (the only collective): exercised once, outside timing
+    best_local = None
+    if world > 1:
+        from paper_2109_10392_b200.dist import allgather_winner, local_winner
+
+        rec = local_winner(sc.meta_cost.cpu().numpy(), sc.flags.cpu().numpy() == 7, offset)
+        best_local, _ = allgather_winner(rec)
+        tt = torch.tensor([t_local], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_max = float(tt.item())
+    else:
+        t_max = t_local
+    total_problems = L * world * args.steps
+    value = total_problems / (t_max / 1e3)
+
+    # roofline: the persistent AM kernel alone
+    kk = []
+    for i in range(max(3, args.steps)):
+        flush.fill_(float(i))
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        kernel_only()
+        b.record(stream)
+        torch.cuda.synchronize()
+        kk.append(a.elapsed_time(b))
+    k_ms = statistics.median(kk)
+    flops = 2.0 * work_slots(n, W.m, nb) * L * iters
+    peak = D.peak_fp64_tflops(5)
+    achieved = flops / (k_ms * 1e-3) / 1e12
+
+    # e2e through the public API from pinned host buffers
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+
+    class _H:
+        pass
+
+    H = _H()
+    H.xi_x, H.xi_y, H.b_xy, H.b_psi = pin(W.xi_x), pin(W.xi_y), pin(W.b_xy), pin(W.b_psi)
+    H.l, H.S, H.a, H.b, H.v_min, H.v_max, H.a_max = W.l, W.S, W.a, W.b, W.v_min, W.v_max, W.a_max
+    for _ in range(args.warmup):
+        plan_batch(solver, H, max_iter=iters, tol=0.0, spec=spec, limits=limits)
+    e2e_ms = []
+    best_e2e = None
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = plan_batch(solver, H, max_iter=iters, tol=0.0, spec=spec, limits=limits)
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        best_e2e = res.best_index[0]
+    e2e_local = sum(e2e_ms)
+    if world > 1:
+        tt = torch.tensor([e2e_local], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e_local = float(tt.item())
+    e2e_value = total_problems / (e2e_local / 1e3)
+    h2d = sum(a.nbytes for a in (H.xi_x, H.xi_y, H.b_xy, H.b_psi))
+    d2h = 3 * nb * L * 8 + 3 * L * 8 + 3 * L * 8 + L + 4 * W.S * 8
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        procs = os.cpu_count() or 1
+        rate, secs, used = cpu_oracle_rate(args.config if cfg.scenes == 1 else "c1",
+                                           cfg.l if cfg.scenes == 1 else 1024, iters, procs)
+        cpu = {"value": rate, "unit": "problems/s", "cores": used, "kind": "port",
+               "sample": f"{args.config} scene 0, {cfg.l if cfg.scenes == 1 else 1024} goals x {iters} "
+                         f"sweeps + scoring, split over {used} processes (1 BLAS thread each), "
+                         f"{secs:.2f}s wall; oracle/am_oracle.py + am_oracle.c"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "problems/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded scene generator, paper_2109_10392_b200/scenes.py)",
+            "config": {"workload": args.config, "problems_per_gpu": L, "iters": iters, "n": n,
+                       "m": W.m, "n_b": nb, "scenes_per_gpu": W.S, "tol": 0.0,
+                       "l2": "flushed between steps (256 MiB write)",
+                       "parallelism": f"goal/scene shards x{world}"},
+            "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "am_solve_kernel", "kernel_ms": k_ms,
+                         "work": f"2*W(n,m,nb)*L*iters, W={work_slots(n, W.m, nb)} slots",
+                         "peak_source": "measured live: DFMA microbenchmark (csrc/peak.cu)"},
+            "e2e": {"value": e2e_value, "unit": "problems/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_local / args.steps},
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+            "best_index_scene0": best_local if world > 1 else best_e2e,
+        }
+        print(json.dumps(line))
+
+
+# ---------------------------------------------------------- reference arm ----
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from paper_2109_10392_b200.scenes import CONFIGS
+
+    cfg = CONFIGS[args.config]
+    iters = args.iters or cfg.iters
+    goals = cfg.l if cfg.scenes == 1 else 1024
+    procs = os.cpu_count() or 1
+    times = []
+    import multiprocessing as mp
+
+    per = int(math.ceil(goals / procs))
+    cfg_name = args.config if cfg.scenes == 1 else "c1"
+    jobs = [(cfg_name, i * per, min(goals, (i + 1) * per), iters, goals) for i in range(procs)
+            if i * per < goals]
+    with mp.get_context("spawn").Pool(len(jobs)) as pool:
+        pool.map(_cpu_worker, [(cfg_name, 0, 1, 1, goals)] * len(jobs))
+        for _ in range(args.warmup):
+            pool.map(_cpu_worker, jobs)
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            pool.map(_cpu_worker, jobs)
+            times.append(time.perf_counter() - t0)
+    value = goals * args.steps / sum(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "problems/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(times) / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "problems_per_step": goals, "iters": iters,
+                   "tol": 0.0},
+        "cpu_baseline": {"value": value, "unit": "problems/s", "cores": len(jobs), "kind": "port",
+                         "sample": f"{cfg_name} scene 0, {goals} goals x {iters} sweeps + scoring per "
+                                   f"step over {len(jobs)} processes (1 BLAS thread each)"},
+        "e2e": {"value": value, "unit": "problems/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c1")
+    ap.add_argument("--iters", type=int, default=0)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and args.impl == "ours":
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+    if world > 1 and args.impl == "ours":
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

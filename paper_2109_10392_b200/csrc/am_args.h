@@ -1,0 +1,65 @@
+// am_args.h -- argument blocks shared by the C-ABI and the sm_100a kernels.
+#pragma once
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+// Device-side constants of one problem shape (uploaded once per context).
+typedef struct {
+  int n;          // horizon samples
+  int npad;       // n rounded up to a multiple of 32
+  int nb;         // Bernstein coefficients per axis (degree + 1)
+  int kxs, kps;   // padded row strides of the KKT inverse blocks
+  double rho;
+  const double* PT;   // [3][nb][npad]: P^T, Pdot^T, Pddot^T, zero padded past n
+  const double* tau;  // [npad] (t_k - t0)/(tf - t0), cold-start line parameter
+  const double* Kx;   // [nb][kxs]  rows 0..nb-1 of the per-axis KKT inverse, nb+6 used
+  const double* Kp;   // [nb][kps]  rows 0..nb-1 of the heading KKT inverse, nb+4 used
+} bmpc_dev_consts;
+
+enum { BMPC_INIT_COLD = 0, BMPC_INIT_WARM = 1, BMPC_INIT_RESUME = 2 };
+enum {
+  BMPC_F_HISTORY = 1,   // write residual history rows
+  BMPC_F_V = 2,         // write the last tail's clipped speed v (n, L)
+  BMPC_F_CARRY = 4,     // write the carried state (for chunked / resumed solves)
+};
+
+typedef struct {
+  int m, l, L, S;       // obstacles, goals per scene, instances, scenes (L = S*l)
+  int iters;            // AM sweeps in this launch
+  int init_mode;        // BMPC_INIT_*
+  int flags;            // BMPC_F_*
+  int hist_offset;      // first history row written by this launch
+  double a, b, v_min, v_max, a_max;
+  const double* xi;     // [S][m][n] interleaved (xi_x, xi_y) pairs
+  const double* b_xy;   // [12][L]
+  const double* b_psi;  // [4][L]
+  // warm start (BMPC_INIT_WARM), reference AmState layouts (rows, L)
+  const double *w_alpha, *w_d, *w_alpha_a, *w_d_a, *w_v, *w_cpsi;
+  const double *w_lx, *w_ly, *w_lp;   // may be NULL (zero multipliers)
+  double* carry;        // [L][5*nb]: lambda_x, lambda_y, lambda_psi, G_x, G_y
+  double *c_x, *c_y, *c_psi, *l_x, *l_y, *l_psi;  // (nb, L)
+  double* v_out;        // (n, L)
+  double* hist;         // [rows][3][L]
+  double* res_final;    // [3][L]
+} bmpc_solve_args;
+
+// Fused scoring (sample_plan + filter_candidates + meta_cost), warp per instance.
+typedef struct {
+  int n, npad, nb, m, l, L;
+  double a, b;
+  int kind;  // 0 cruise, 1 highspeed
+  double v_cruise, v_max, y_rl, w1, w2;
+  double heading_limit, residual_tol, ratio_min;
+  const double* PT;
+  const double* xi;  // packed (S, m, n) (xi_x, xi_y) pairs
+  const double *c_x, *c_y, *c_psi, *res_final;
+  double *meta, *min_ratio, *heading_max;
+  unsigned char* flags;  // bit0 heading ok, bit1 residual ok, bit2 collision ok
+} bmpc_score_args;
+
+#ifdef __cplusplus
+}
+#endif

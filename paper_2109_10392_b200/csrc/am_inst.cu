@@ -1,0 +1,34 @@
+// am_inst.cu -- one n_b instantiation of the persistent AM kernel (compiled
+// once per n_b with -DBMPC_INST_NB=<n_b> so the builds run in parallel).
+#include "am_solve_kernel.cuh"
+
+namespace bmpc {
+
+size_t am_solve_smem_bytes(int nb, int npad, int kxs, int kps, int warps);
+
+template <int NB, int NKM>
+static cudaError_t launch_t(const bmpc_dev_consts& C, const bmpc_solve_args& A, int warps,
+                            cudaStream_t st) {
+  const size_t smem = am_solve_smem_bytes(NB, C.npad, C.kxs, C.kps, warps);
+  auto kfn = am_solve_kernel<NB, NKM>;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int grid = (A.L + warps - 1) / warps;
+  kfn<<<grid, warps * 32, smem, st>>>(C, A);
+  return cudaGetLastError();
+}
+
+#define BMPC_CAT2(a, b) a##b
+#define BMPC_CAT(a, b) BMPC_CAT2(a, b)
+
+cudaError_t BMPC_CAT(launch_am_nb_, BMPC_INST_NB)(const bmpc_dev_consts& C,
+                                                   const bmpc_solve_args& A, int warps,
+                                                   cudaStream_t st) {
+  const int nk = C.npad / 32;
+  if (nk <= 2) return launch_t<BMPC_INST_NB, 2>(C, A, warps, st);
+  if (nk <= 4) return launch_t<BMPC_INST_NB, 4>(C, A, warps, st);
+  if (nk <= 8) return launch_t<BMPC_INST_NB, 8>(C, A, warps, st);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace bmpc

@@ -1,0 +1,521 @@
+// capi.cu -- extern "C" boundary (include/batchmpc_b200.h) over the sm_100a kernels.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/batchmpc_b200.h"
+#include "am_args.h"
+
+namespace bmpc {
+cudaError_t launch_am_solve(const bmpc_dev_consts& C, const bmpc_solve_args& A, int warps,
+                            cudaStream_t st);
+size_t am_solve_smem_bytes(int nb, int npad, int kxs, int kps, int warps);
+cudaError_t op_obstacle_update(int n, int l, long long mn, const double* x, const double* y,
+                               const double* xi_x, const double* xi_y, double a, double b,
+                               double* alpha, double* d, cudaStream_t st);
+cudaError_t op_accel_update(long long nl, const double* xdd, const double* ydd, double a_max,
+                            double* alpha_a, double* d_a, cudaStream_t st);
+cudaError_t op_v_update(long long nl, const double* xd, const double* yd, double v_min,
+                        double v_max, double* v, cudaStream_t st);
+cudaError_t op_assemble_g(int n, int l, long long mn, const double* xi_x, const double* xi_y,
+                          const double* alpha, const double* d, const double* alpha_a,
+                          const double* d_a, const double* v, const double* psi, double a,
+                          double b, double* g_x, double* g_y, cudaStream_t st);
+cudaError_t op_residual_vectors(int n, int l, long long mn, const double* x, const double* y,
+                                const double* xd, const double* yd, const double* xdd,
+                                const double* ydd, const double* psi, const double* xi_x,
+                                const double* xi_y, const double* alpha, const double* d,
+                                const double* alpha_a, const double* d_a, const double* v,
+                                double a, double b, double* r_x, double* r_y, cudaStream_t st);
+cudaError_t op_tail(bool with_angles, int n, int l, long long mn, const double* x, const double* y,
+                    const double* xd, const double* yd, const double* xdd, const double* ydd,
+                    const double* psi, const double* xi_x, const double* xi_y, double v_min,
+                    double v_max, double a_max, double a, double b, double* alpha, double* d,
+                    double* alpha_a, double* d_a, double* v, double* r_x, double* r_y,
+                    double* g_x, double* g_y, double* sq_obs, double* sq_acc, double* sq_nonhol,
+                    cudaStream_t st);
+cudaError_t op_sample(int n, int npad, int nb, int L, const double* PT, const double* c_x,
+                      const double* c_y, const double* c_psi, double* x, double* y, double* xd,
+                      double* yd, double* xdd, double* ydd, double* psi, double* psid, double* v,
+                      cudaStream_t st);
+using ScoreArgs = bmpc_score_args;
+cudaError_t op_score(const ScoreArgs& S, cudaStream_t st);
+cudaError_t op_argmin(int S, int l, const double* meta, const uint8_t* flags, long long* best,
+                      long long* best_all, long long* best_hc, long long* nfeas, cudaStream_t st);
+cudaError_t op_pack_xi(long long total, const double* xi_x, const double* xi_y, double* out,
+                       cudaStream_t st);
+cudaError_t op_first_converged(int iters, long long L, const double* hist, double tol, int* tstar,
+                               cudaStream_t st);
+cudaError_t dfma_peak_tflops(int reps, double* tflops, cudaStream_t st);
+}  // namespace bmpc
+
+struct bmpc_ctx {
+  bmpc_dev_consts C;
+  double* dmem = nullptr;  // one allocation for every constant
+  int sms = 148;
+};
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+static int cuda_fail(cudaError_t e, const char* where) {
+  return fail(BMPC_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define CK(expr, where)                              \
+  do {                                               \
+    cudaError_t _e = (expr);                         \
+    if (_e != cudaSuccess) return cuda_fail(_e, where); \
+  } while (0)
+
+static inline cudaStream_t S_(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ------------------------------------------------------------ host e2e ----
+struct DevBuf {
+  std::vector<void*> ptrs;
+  cudaStream_t st;
+  explicit DevBuf(cudaStream_t s) : st(s) {}
+  ~DevBuf() {
+    for (void* p : ptrs) cudaFreeAsync(p, st);
+  }
+  template <class T>
+  T* alloc(size_t count) {
+    void* p = nullptr;
+    if (count == 0) count = 1;
+    if (cudaMallocAsync(&p, count * sizeof(T), st) != cudaSuccess) return nullptr;
+    ptrs.push_back(p);
+    return static_cast<T*>(p);
+  }
+};
+
+extern "C" {
+
+const char* bmpc_last_error(void) { return g_err.c_str(); }
+int bmpc_abi_version(void) { return 1; }
+
+int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pdot,
+                    const double* Pddot, const double* tau, const double* kinv_axis,
+                    const double* kinv_psi, bmpc_ctx** out) {
+  if (!out || !P || !Pdot || !Pddot || !tau || !kinv_axis || !kinv_psi)
+    return fail(BMPC_EINVAL, "bmpc_ctx_create: null argument");
+  if (nb < 4 || nb > 16) return fail(BMPC_EINVAL, "bmpc_ctx_create: need 4 <= n_b <= 16");
+  if (n < 2 || n > 256) return fail(BMPC_EINVAL, "bmpc_ctx_create: need 2 <= n <= 256");
+  if (!(rho > 0.0)) return fail(BMPC_EINVAL, "bmpc_ctx_create: rho must be positive");
+  for (int i = 0; i < nb * (nb + 6); ++i)
+    if (!isfinite(kinv_axis[i])) return fail(BMPC_ESINGULAR, "KKT xy inverse is not finite");
+  for (int i = 0; i < nb * (nb + 4); ++i)
+    if (!isfinite(kinv_psi[i])) return fail(BMPC_ESINGULAR, "KKT psi inverse is not finite");
+  const int npad = ((n + 31) / 32) * 32;
+  const int kxs = (nb + 6) | 1, kps = (nb + 4) | 1;
+  const size_t nPT = (size_t)3 * nb * npad, nKx = (size_t)nb * kxs, nKp = (size_t)nb * kps;
+  std::vector<double> h(nPT + nKx + nKp + npad, 0.0);
+  const double* mats[3] = {P, Pdot, Pddot};
+  for (int q = 0; q < 3; ++q)
+    for (int i = 0; i < nb; ++i)
+      for (int k = 0; k < n; ++k) h[((size_t)q * nb + i) * npad + k] = mats[q][(size_t)k * nb + i];
+  for (int i = 0; i < nb; ++i)
+    for (int j = 0; j < nb + 6; ++j) h[nPT + (size_t)i * kxs + j] = kinv_axis[(size_t)i * (nb + 6) + j];
+  for (int i = 0; i < nb; ++i)
+    for (int j = 0; j < nb + 4; ++j) h[nPT + nKx + (size_t)i * kps + j] = kinv_psi[(size_t)i * (nb + 4) + j];
+  for (int k = 0; k < n; ++k) h[nPT + nKx + nKp + k] = tau[k];
+  bmpc_ctx* c = new bmpc_ctx();
+  cudaError_t e = cudaMalloc(&c->dmem, h.size() * sizeof(double));
+  if (e != cudaSuccess) { delete c; return cuda_fail(e, "bmpc_ctx_create/cudaMalloc"); }
+  e = cudaMemcpy(c->dmem, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) { cudaFree(c->dmem); delete c; return cuda_fail(e, "bmpc_ctx_create/memcpy"); }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, dev);
+  c->C.n = n;
+  c->C.npad = npad;
+  c->C.nb = nb;
+  c->C.kxs = kxs;
+  c->C.kps = kps;
+  c->C.rho = rho;
+  c->C.PT = c->dmem;
+  c->C.Kx = c->dmem + nPT;
+  c->C.Kp = c->dmem + nPT + nKx;
+  c->C.tau = c->dmem + nPT + nKx + nKp;
+  *out = c;
+  return BMPC_OK;
+}
+
+int bmpc_ctx_destroy(bmpc_ctx* ctx) {
+  if (!ctx) return BMPC_OK;
+  cudaFree(ctx->dmem);
+  delete ctx;
+  return BMPC_OK;
+}
+
+int bmpc_ctx_info(const bmpc_ctx* ctx, int* n, int* npad, int* nb, const double** PT) {
+  if (!ctx) return fail(BMPC_EINVAL, "null ctx");
+  if (n) *n = ctx->C.n;
+  if (npad) *npad = ctx->C.npad;
+  if (nb) *nb = ctx->C.nb;
+  if (PT) *PT = ctx->C.PT;
+  return BMPC_OK;
+}
+
+static int check_problem(const bmpc_ctx* ctx, const bmpc_problem* p) {
+  if (!ctx || !p) return fail(BMPC_EINVAL, "null ctx/problem");
+  if (p->m < 0 || p->l < 0 || p->S < 1) return fail(BMPC_EINVAL, "invalid m/l/S");
+  if (!(0.0 < p->v_min && p->v_min < p->v_max))
+    return fail(BMPC_EINVAL, "need 0 < v_min < v_max");
+  if (!(p->a_max > 0.0)) return fail(BMPC_EINVAL, "a_max must be positive");
+  if (!(p->a >= p->b && p->b > 0.0)) return fail(BMPC_EINVAL, "ellipse axes must satisfy a >= b > 0");
+  if (p->l > 0 && (!p->b_xy || !p->b_psi)) return fail(BMPC_EINVAL, "null boundary vectors");
+  if (p->m > 0 && (!p->xi_x || !p->xi_y)) return fail(BMPC_EINVAL, "null obstacle predictions");
+  return BMPC_OK;
+}
+
+static int auto_warps(const bmpc_ctx* ctx, int L, int req) {
+  if (req > 0) return req > 8 ? 8 : req;
+  int w = (L + ctx->sms - 1) / ctx->sms;
+  if (w < 1) w = 1;
+  if (w > 8) w = 8;
+  return w;
+}
+
+// Launch `iters` sweeps; xi2 is the packed (S, m, n) double2 buffer.
+static int launch_sweeps(bmpc_ctx* ctx, const bmpc_problem* p, const double* xi2,
+                         const bmpc_solve_opts* o, int iters, int init_mode, int hist_offset,
+                         double* carry, int write_carry, bmpc_solve_out* out, cudaStream_t st) {
+  const int L = p->S * p->l;
+  bmpc_solve_args A;
+  memset(&A, 0, sizeof(A));
+  A.m = p->m;
+  A.l = p->l;
+  A.L = L;
+  A.S = p->S;
+  A.iters = iters;
+  A.init_mode = init_mode;
+  A.flags = (out->history ? BMPC_F_HISTORY : 0) | ((o->want_v && out->v) ? BMPC_F_V : 0) |
+            (write_carry ? BMPC_F_CARRY : 0);
+  A.hist_offset = hist_offset;
+  A.a = p->a;
+  A.b = p->b;
+  A.v_min = p->v_min;
+  A.v_max = p->v_max;
+  A.a_max = p->a_max;
+  A.xi = xi2;
+  A.b_xy = p->b_xy;
+  A.b_psi = p->b_psi;
+  A.w_alpha = o->w_alpha;
+  A.w_d = o->w_d;
+  A.w_alpha_a = o->w_alpha_a;
+  A.w_d_a = o->w_d_a;
+  A.w_v = o->w_v;
+  A.w_cpsi = o->w_c_psi;
+  const bool keep = o->keep_multipliers != 0;
+  A.w_lx = keep ? o->w_l_x : nullptr;
+  A.w_ly = keep ? o->w_l_y : nullptr;
+  A.w_lp = keep ? o->w_l_psi : nullptr;
+  A.carry = carry;
+  A.c_x = out->c_x;
+  A.c_y = out->c_y;
+  A.c_psi = out->c_psi;
+  A.l_x = out->l_x;
+  A.l_y = out->l_y;
+  A.l_psi = out->l_psi;
+  A.v_out = out->v;
+  A.hist = out->history;
+  A.res_final = out->res_final;
+  if (L == 0 || iters <= 0) return BMPC_OK;
+  CK(bmpc::launch_am_solve(ctx->C, A, auto_warps(ctx, L, o->warps_per_block), st), "am_solve launch");
+  return BMPC_OK;
+}
+
+static bool is_warm(const bmpc_solve_opts* o) {
+  return o->w_alpha || o->w_d || o->w_alpha_a || o->w_d_a || o->w_v || o->w_c_psi;
+}
+
+static int check_warm(const bmpc_solve_opts* o, const bmpc_problem* p) {
+  if (!is_warm(o)) return BMPC_OK;
+  if (!o->w_alpha || !o->w_d || !o->w_alpha_a || !o->w_d_a || !o->w_v || !o->w_c_psi)
+    return fail(BMPC_EINVAL, "warm start needs alpha, d, alpha_a, d_a, v and c_psi");
+  if (o->keep_multipliers && (!o->w_l_x || !o->w_l_y || !o->w_l_psi))
+    return fail(BMPC_EINVAL, "keep_multipliers needs the warm multipliers");
+  (void)p;
+  return BMPC_OK;
+}
+
+int bmpc_sweeps(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opts* o, int iters,
+                int resume, int hist_offset, double* carry, int write_carry, bmpc_solve_out* out,
+                void* stream) {
+  int rc = check_problem(ctx, p);
+  if (rc) return rc;
+  if (!o || !out) return fail(BMPC_EINVAL, "null opts/out");
+  if ((resume || write_carry) && !carry) return fail(BMPC_EINVAL, "carry buffer required");
+  if ((rc = check_warm(o, p))) return rc;
+  cudaStream_t st = S_(stream);
+  const long long tot = (long long)p->S * p->m * ctx->C.n;
+  double* xi2 = nullptr;
+  if (tot > 0) {
+    CK(cudaMallocAsync(&xi2, tot * 2 * sizeof(double), st), "cudaMallocAsync");
+    CK(bmpc::op_pack_xi(tot, p->xi_x, p->xi_y, xi2, st), "pack_xi");
+  }
+  const int mode = resume ? BMPC_INIT_RESUME : (is_warm(o) ? BMPC_INIT_WARM : BMPC_INIT_COLD);
+  rc = launch_sweeps(ctx, p, xi2, o, iters, mode, hist_offset, carry, write_carry, out, st);
+  if (xi2) cudaFreeAsync(xi2, st);
+  return rc;
+}
+
+int bmpc_solve(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opts* o,
+               bmpc_solve_out* out, void* stream) {
+  int rc = check_problem(ctx, p);
+  if (rc) return rc;
+  if (!o || !out) return fail(BMPC_EINVAL, "null opts/out");
+  if (o->max_iter < 1) return fail(BMPC_EINVAL, "max_iter must be >= 1");
+  if (!out->history || !out->res_final)
+    return fail(BMPC_EINVAL, "history and res_final outputs are required");
+  if ((rc = check_warm(o, p))) return rc;
+  cudaStream_t st = S_(stream);
+  const int L = p->S * p->l;
+  const long long tot = (long long)p->S * p->m * ctx->C.n;
+  double* xi2 = nullptr;
+  int* tstar = nullptr;
+  if (tot > 0) {
+    CK(cudaMallocAsync(&xi2, tot * 2 * sizeof(double), st), "cudaMallocAsync");
+    CK(bmpc::op_pack_xi(tot, p->xi_x, p->xi_y, xi2, st), "pack_xi");
+  }
+  const int mode = is_warm(o) ? BMPC_INIT_WARM : BMPC_INIT_COLD;
+  rc = launch_sweeps(ctx, p, xi2, o, o->max_iter, mode, 0, nullptr, 0, out, st);
+  int iters = o->max_iter, converged = 0;
+  if (!rc && L > 0) {
+    // Global early stop (solver.py:437-439): find the first sweep whose worst
+    // residual is <= tol; when it is not the last one, re-run exactly that many
+    // sweeps (the instances are independent and deterministic, so the re-run
+    // reproduces the same iterates).
+    int t = 1 << 30;
+    CK(cudaMallocAsync(&tstar, sizeof(int), st), "cudaMallocAsync");
+    CK(cudaMemcpyAsync(tstar, &t, sizeof(int), cudaMemcpyHostToDevice, st), "memcpy");
+    CK(bmpc::op_first_converged(o->max_iter, L, out->history, o->tol, tstar, st), "first_converged");
+    CK(cudaMemcpyAsync(&t, tstar, sizeof(int), cudaMemcpyDeviceToHost, st), "memcpy");
+    CK(cudaStreamSynchronize(st), "sync");
+    if (t < o->max_iter) {
+      converged = 1;
+      iters = t + 1;
+      if (iters < o->max_iter)
+        rc = launch_sweeps(ctx, p, xi2, o, iters, mode, 0, nullptr, 0, out, st);
+    }
+  }
+  if (xi2) cudaFreeAsync(xi2, st);
+  if (tstar) cudaFreeAsync(tstar, st);
+  if (rc) return rc;
+  CK(cudaGetLastError(), "bmpc_solve");
+  out->iterations = iters;
+  out->converged = converged;
+  return BMPC_OK;
+}
+
+int bmpc_score(bmpc_ctx* ctx, const bmpc_problem* p, const double* c_x, const double* c_y,
+               const double* c_psi, const double* res_final, const bmpc_score_spec* spec,
+               bmpc_score_out* out, void* stream) {
+  int rc = check_problem(ctx, p);
+  if (rc) return rc;
+  if (!spec || !out || !c_x || !c_y || !c_psi || !res_final)
+    return fail(BMPC_EINVAL, "bmpc_score: null argument");
+  if (spec->kind != 0 && spec->kind != 1) return fail(BMPC_EINVAL, "unknown meta-cost kind");
+  cudaStream_t st = S_(stream);
+  const int L = p->S * p->l;
+  const long long tot = (long long)p->S * p->m * ctx->C.n;
+  double* xi2 = nullptr;
+  if (tot > 0) {
+    CK(cudaMallocAsync(&xi2, tot * 2 * sizeof(double), st), "cudaMallocAsync");
+    CK(bmpc::op_pack_xi(tot, p->xi_x, p->xi_y, xi2, st), "pack_xi");
+  }
+  bmpc::ScoreArgs S;
+  memset(&S, 0, sizeof(S));
+  S.n = ctx->C.n;
+  S.npad = ctx->C.npad;
+  S.nb = ctx->C.nb;
+  S.m = p->m;
+  S.l = p->l;
+  S.L = L;
+  S.a = p->a;
+  S.b = p->b;
+  S.kind = spec->kind;
+  S.v_cruise = spec->v_cruise;
+  S.v_max = spec->v_max;
+  S.y_rl = spec->y_rl;
+  S.w1 = spec->w1;
+  S.w2 = spec->w2;
+  S.heading_limit = spec->heading_limit;
+  S.residual_tol = spec->residual_tol;
+  S.ratio_min = 1.0 - spec->collision_margin;
+  S.PT = ctx->C.PT;
+  S.xi = xi2;
+  S.c_x = c_x;
+  S.c_y = c_y;
+  S.c_psi = c_psi;
+  S.res_final = res_final;
+  S.meta = out->meta_cost;
+  S.min_ratio = out->min_ratio;
+  S.heading_max = out->heading_max;
+  S.flags = out->flags;
+  if (!S.meta || !S.min_ratio || !S.heading_max || !S.flags)
+    return fail(BMPC_EINVAL, "bmpc_score: per-instance outputs required");
+  CK(bmpc::op_score(S, st), "score");
+  if (out->best_index && out->argmin_all && out->argmin_hc && out->n_feasible)
+    CK(bmpc::op_argmin(p->S, p->l, out->meta_cost, out->flags, out->best_index, out->argmin_all,
+                       out->argmin_hc, out->n_feasible, st),
+       "argmin");
+  if (xi2) cudaFreeAsync(xi2, st);
+  return BMPC_OK;
+}
+
+int bmpc_sample(bmpc_ctx* ctx, int L, const double* c_x, const double* c_y, const double* c_psi,
+                double* x, double* y, double* xd, double* yd, double* xdd, double* ydd,
+                double* psi, double* psid, double* v, void* stream) {
+  if (!ctx || L < 0) return fail(BMPC_EINVAL, "bmpc_sample: bad argument");
+  CK(bmpc::op_sample(ctx->C.n, ctx->C.npad, ctx->C.nb, L, ctx->C.PT, c_x, c_y, c_psi, x, y, xd, yd,
+                     xdd, ydd, psi, psid, v, S_(stream)),
+     "sample");
+  return BMPC_OK;
+}
+
+int bmpc_plan_host(bmpc_ctx* ctx, const bmpc_problem* hp, const bmpc_solve_opts* o,
+                   bmpc_solve_out* ho, const bmpc_score_spec* spec, bmpc_score_out* hs,
+                   void* stream) {
+  int rc = check_problem(ctx, hp);
+  if (rc) return rc;
+  if (!o || !ho) return fail(BMPC_EINVAL, "null opts/out");
+  if (is_warm(o)) return fail(BMPC_EINVAL, "bmpc_plan_host: warm starts use the device API");
+  cudaStream_t st = S_(stream);
+  const int n = ctx->C.n, nb = ctx->C.nb;
+  const size_t L = (size_t)hp->S * hp->l, mn = (size_t)hp->m * n;
+  DevBuf B(st);
+  bmpc_problem dp = *hp;
+  double* xix = B.alloc<double>(hp->S * mn);
+  double* xiy = B.alloc<double>(hp->S * mn);
+  double* bxy = B.alloc<double>(12 * L);
+  double* bps = B.alloc<double>(4 * L);
+  if (!xix || !xiy || !bxy || !bps) return fail(BMPC_ECUDA, "device allocation failed");
+  CK(cudaMemcpyAsync(xix, hp->xi_x, hp->S * mn * 8, cudaMemcpyHostToDevice, st), "h2d");
+  CK(cudaMemcpyAsync(xiy, hp->xi_y, hp->S * mn * 8, cudaMemcpyHostToDevice, st), "h2d");
+  CK(cudaMemcpyAsync(bxy, hp->b_xy, 12 * L * 8, cudaMemcpyHostToDevice, st), "h2d");
+  CK(cudaMemcpyAsync(bps, hp->b_psi, 4 * L * 8, cudaMemcpyHostToDevice, st), "h2d");
+  dp.xi_x = xix;
+  dp.xi_y = xiy;
+  dp.b_xy = bxy;
+  dp.b_psi = bps;
+  bmpc_solve_out dout;
+  memset(&dout, 0, sizeof(dout));
+  double* coef = B.alloc<double>(6 * nb * L);
+  dout.c_x = coef;
+  dout.c_y = coef + nb * L;
+  dout.c_psi = coef + 2 * nb * L;
+  dout.l_x = coef + 3 * nb * L;
+  dout.l_y = coef + 4 * nb * L;
+  dout.l_psi = coef + 5 * nb * L;
+  dout.history = B.alloc<double>((size_t)o->max_iter * 3 * L);
+  dout.res_final = B.alloc<double>(3 * L);
+  dout.v = (o->want_v && ho->v) ? B.alloc<double>(n * L) : nullptr;
+  if (!coef || !dout.history || !dout.res_final) return fail(BMPC_ECUDA, "device allocation failed");
+  rc = bmpc_solve(ctx, &dp, o, &dout, stream);
+  if (rc) return rc;
+  ho->iterations = dout.iterations;
+  ho->converged = dout.converged;
+  bmpc_score_out ds;
+  memset(&ds, 0, sizeof(ds));
+  if (spec && hs) {
+    ds.meta_cost = B.alloc<double>(L);
+    ds.min_ratio = B.alloc<double>(L);
+    ds.heading_max = B.alloc<double>(L);
+    ds.flags = B.alloc<unsigned char>(L);
+    ds.best_index = B.alloc<long long>(hp->S);
+    ds.argmin_all = B.alloc<long long>(hp->S);
+    ds.argmin_hc = B.alloc<long long>(hp->S);
+    ds.n_feasible = B.alloc<long long>(hp->S);
+    rc = bmpc_score(ctx, &dp, dout.c_x, dout.c_y, dout.c_psi, dout.res_final, spec, &ds, stream);
+    if (rc) return rc;
+  }
+  struct Cp { void* h; const void* d; size_t bytes; };
+  const Cp cps[] = {
+      {ho->c_x, dout.c_x, nb * L * 8}, {ho->c_y, dout.c_y, nb * L * 8},
+      {ho->c_psi, dout.c_psi, nb * L * 8}, {ho->l_x, dout.l_x, nb * L * 8},
+      {ho->l_y, dout.l_y, nb * L * 8}, {ho->l_psi, dout.l_psi, nb * L * 8},
+      {ho->v, dout.v, n * L * 8},
+      {ho->history, dout.history, (size_t)dout.iterations * 3 * L * 8},
+      {ho->res_final, dout.res_final, 3 * L * 8},
+      {hs ? hs->meta_cost : nullptr, ds.meta_cost, L * 8},
+      {hs ? hs->min_ratio : nullptr, ds.min_ratio, L * 8},
+      {hs ? hs->heading_max : nullptr, ds.heading_max, L * 8},
+      {hs ? hs->flags : nullptr, ds.flags, L},
+      {hs ? hs->best_index : nullptr, ds.best_index, (size_t)hp->S * 8},
+      {hs ? hs->argmin_all : nullptr, ds.argmin_all, (size_t)hp->S * 8},
+      {hs ? hs->argmin_hc : nullptr, ds.argmin_hc, (size_t)hp->S * 8},
+      {hs ? hs->n_feasible : nullptr, ds.n_feasible, (size_t)hp->S * 8},
+  };
+  for (const Cp& c : cps)
+    if (c.h && c.d && c.bytes) CK(cudaMemcpyAsync(c.h, c.d, c.bytes, cudaMemcpyDeviceToHost, st), "d2h");
+  CK(cudaStreamSynchronize(st), "sync");
+  return BMPC_OK;
+}
+
+// ------------------------------------------------------------ op-level ----
+int bmpc_op_obstacle_update(int n, int l, int mn, const double* x, const double* y,
+                            const double* xi_x, const double* xi_y, double a, double b,
+                            double* alpha, double* d, void* s) {
+  if (n < 1 || l < 0 || mn < 0 || mn % n) return fail(BMPC_EINVAL, "obstacle_update: bad shape");
+  CK(bmpc::op_obstacle_update(n, l, mn, x, y, xi_x, xi_y, a, b, alpha, d, S_(s)), "obstacle_update");
+  return BMPC_OK;
+}
+int bmpc_op_accel_update(int n, int l, const double* xdd, const double* ydd, double a_max,
+                         double* alpha_a, double* d_a, void* s) {
+  CK(bmpc::op_accel_update((long long)n * l, xdd, ydd, a_max, alpha_a, d_a, S_(s)), "accel_update");
+  return BMPC_OK;
+}
+int bmpc_op_v_update(int n, int l, const double* xd, const double* yd, double v_min, double v_max,
+                     double* v, void* s) {
+  CK(bmpc::op_v_update((long long)n * l, xd, yd, v_min, v_max, v, S_(s)), "v_update");
+  return BMPC_OK;
+}
+int bmpc_op_assemble_g(int n, int l, int mn, const double* xi_x, const double* xi_y,
+                       const double* alpha, const double* d, const double* alpha_a,
+                       const double* d_a, const double* v, const double* psi, double a, double b,
+                       double* g_x, double* g_y, void* s) {
+  CK(bmpc::op_assemble_g(n, l, mn, xi_x, xi_y, alpha, d, alpha_a, d_a, v, psi, a, b, g_x, g_y, S_(s)),
+     "assemble_g");
+  return BMPC_OK;
+}
+int bmpc_op_residual_vectors(int n, int l, int mn, const double* x, const double* y,
+                             const double* xd, const double* yd, const double* xdd,
+                             const double* ydd, const double* psi, const double* xi_x,
+                             const double* xi_y, const double* alpha, const double* d,
+                             const double* alpha_a, const double* d_a, const double* v, double a,
+                             double b, double* r_x, double* r_y, void* s) {
+  CK(bmpc::op_residual_vectors(n, l, mn, x, y, xd, yd, xdd, ydd, psi, xi_x, xi_y, alpha, d, alpha_a,
+                               d_a, v, a, b, r_x, r_y, S_(s)),
+     "residual_vectors");
+  return BMPC_OK;
+}
+int bmpc_op_tail(int n, int l, int mn, const double* x, const double* y, const double* xd,
+                 const double* yd, const double* xdd, const double* ydd, const double* psi,
+                 const double* xi_x, const double* xi_y, double v_min, double v_max, double a_max,
+                 double a, double b, double* alpha, double* d, double* alpha_a, double* d_a,
+                 double* v, double* r_x, double* r_y, double* g_x, double* g_y, double* sq_obs,
+                 double* sq_acc, double* sq_nonhol, void* s) {
+  const bool with_angles = alpha != nullptr && alpha_a != nullptr;
+  if (!with_angles && (!sq_obs || !sq_acc || !sq_nonhol))
+    return fail(BMPC_EINVAL, "tail_core needs the squared-sum outputs");
+  CK(bmpc::op_tail(with_angles, n, l, mn, x, y, xd, yd, xdd, ydd, psi, xi_x, xi_y, v_min, v_max, a_max,
+                   a, b, alpha, d, alpha_a, d_a, v, r_x, r_y, g_x, g_y, sq_obs, sq_acc, sq_nonhol, S_(s)),
+     "tail");
+  return BMPC_OK;
+}
+
+int bmpc_dfma_peak(int reps, double* tflops, void* s) {
+  if (!tflops) return fail(BMPC_EINVAL, "null output");
+  CK(bmpc::dfma_peak_tflops(reps < 1 ? 1 : reps, tflops, S_(s)), "dfma_peak");
+  return BMPC_OK;
+}
+
+}  // extern "C"

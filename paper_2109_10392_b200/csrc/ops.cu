@@ -1,0 +1,511 @@
+// ops.cu -- operator-level sm_100a kernels behind the reference's `kernels`
+// plugin API (/root/reference/pkg/src/batchmpc/kernels/__init__.py:49-86), plus
+// the scoring / argmin / sampling kernels of the planner path.
+//
+// Compiled with -fmad=false: every basic double operation is an IEEE-rounded
+// add/mul exactly as in the reference's scalar C (Cython, -O3 without FMA), and
+// sqrt / division are the correctly-rounded CUDA defaults, so these kernels
+// agree with the reference to the last bit except where libm's and CUDA's
+// atan2/sin/cos differ by an ulp.
+//
+// Layouts are the reference's: (rows, l) row-major with the instance index
+// fastest; obstacle rows j*n + k.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "am_args.h"
+#include "common.cuh"
+
+namespace bmpc {
+
+constexpr int kTB = 256;
+static inline int nblk(long long total) { return (int)((total + kTB - 1) / kTB); }
+
+// ---------------------------------------------------------------- op kernels --
+// _speedups.pyx:12-39
+__global__ void k_obstacle_update(int n, int l, long long mn, const double* __restrict__ x,
+                                  const double* __restrict__ y, const double* __restrict__ xi_x,
+                                  const double* __restrict__ xi_y, double a, double b,
+                                  double* __restrict__ alpha, double* __restrict__ d) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= mn * l) return;
+  const long long row = e / l;
+  const int c = (int)(e - row * l);
+  const int k = (int)(row % n);
+  const double wx = x[(long long)k * l + c] - xi_x[row];
+  const double wy = y[(long long)k * l + c] - xi_y[row];
+  const double al = atan2(a * wy, b * wx);
+  const double ca = cos(al), sa = sin(al);
+  const double num = a * ca * wx + b * sa * wy;
+  const double den = (a * ca) * (a * ca) + (b * sa) * (b * sa);
+  double dd = num / den;
+  if (dd < 1.0) dd = 1.0;
+  alpha[e] = al;
+  d[e] = dd;
+}
+
+// _speedups.pyx:42-60
+__global__ void k_accel_update(long long nl, const double* __restrict__ xdd,
+                               const double* __restrict__ ydd, double a_max,
+                               double* __restrict__ alpha_a, double* __restrict__ d_a) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nl) return;
+  const double ax = xdd[e], ay = ydd[e];
+  alpha_a[e] = atan2(ay, ax);
+  double mag = sqrt(ax * ax + ay * ay);
+  if (mag > a_max) mag = a_max;
+  d_a[e] = mag;
+}
+
+// _speedups.pyx:63-78
+__global__ void k_v_update(long long nl, const double* __restrict__ xd,
+                           const double* __restrict__ yd, double v_min, double v_max,
+                           double* __restrict__ v) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nl) return;
+  double s = sqrt(xd[e] * xd[e] + yd[e] * yd[e]);
+  if (s < v_min) s = v_min;
+  else if (s > v_max) s = v_max;
+  v[e] = s;
+}
+
+// _speedups.pyx:81-111
+__global__ void k_assemble_g(int n, int l, long long mn, const double* __restrict__ xi_x,
+                             const double* __restrict__ xi_y, const double* __restrict__ alpha,
+                             const double* __restrict__ d, const double* __restrict__ alpha_a,
+                             const double* __restrict__ d_a, const double* __restrict__ v,
+                             const double* __restrict__ psi, double a, double b,
+                             double* __restrict__ g_x, double* __restrict__ g_y) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long rows = mn + 2LL * n;
+  if (e >= rows * l) return;
+  const long long row = e / l;
+  const long long c = e - row * l;
+  if (row < mn) {
+    const double ang = alpha[e], ad = d[e];
+    g_x[e] = xi_x[row] + a * ad * cos(ang);
+    g_y[e] = xi_y[row] + b * ad * sin(ang);
+  } else if (row < mn + n) {
+    const long long s = (row - mn) * l + c;
+    g_x[e] = d_a[s] * cos(alpha_a[s]);
+    g_y[e] = d_a[s] * sin(alpha_a[s]);
+  } else {
+    const long long s = (row - mn - n) * l + c;
+    g_x[e] = v[s] * cos(psi[s]);
+    g_y[e] = v[s] * sin(psi[s]);
+  }
+}
+
+// _speedups.pyx:321-355
+__global__ void k_residual_vectors(int n, int l, long long mn, const double* __restrict__ x,
+                                   const double* __restrict__ y, const double* __restrict__ xd,
+                                   const double* __restrict__ yd, const double* __restrict__ xdd,
+                                   const double* __restrict__ ydd, const double* __restrict__ psi,
+                                   const double* __restrict__ xi_x, const double* __restrict__ xi_y,
+                                   const double* __restrict__ alpha, const double* __restrict__ d,
+                                   const double* __restrict__ alpha_a,
+                                   const double* __restrict__ d_a, const double* __restrict__ v,
+                                   double a, double b, double* __restrict__ r_x,
+                                   double* __restrict__ r_y) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long rows = mn + 2LL * n;
+  if (e >= rows * l) return;
+  const long long row = e / l;
+  const long long c = e - row * l;
+  if (row < mn) {
+    const long long s = (row % n) * l + c;
+    const double ang = alpha[e], ad = d[e];
+    r_x[e] = x[s] - xi_x[row] - a * ad * cos(ang);
+    r_y[e] = y[s] - xi_y[row] - b * ad * sin(ang);
+  } else if (row < mn + n) {
+    const long long s = (row - mn) * l + c;
+    r_x[e] = xdd[s] - d_a[s] * cos(alpha_a[s]);
+    r_y[e] = ydd[s] - d_a[s] * sin(alpha_a[s]);
+  } else {
+    const long long s = (row - mn - n) * l + c;
+    r_x[e] = xd[s] - v[s] * cos(psi[s]);
+    r_y[e] = yd[s] - v[s] * sin(psi[s]);
+  }
+}
+
+// _speedups.pyx:114-218 (with_angles=false) and :221-318 (tail_update, with_angles=true).
+// One thread per instance column walks the rows in the reference's order, so
+// the per-instance squared block sums accumulate in the same sequence.
+template <bool WITH_ANGLES>
+__global__ void k_tail(int n, int l, long long mn, const double* __restrict__ x,
+                       const double* __restrict__ y, const double* __restrict__ xd,
+                       const double* __restrict__ yd, const double* __restrict__ xdd,
+                       const double* __restrict__ ydd, const double* __restrict__ psi,
+                       const double* __restrict__ xi_x, const double* __restrict__ xi_y,
+                       double v_min, double v_max, double a_max, double a, double b,
+                       double* __restrict__ alpha, double* __restrict__ d,
+                       double* __restrict__ alpha_a, double* __restrict__ d_a,
+                       double* __restrict__ v, double* __restrict__ r_x,
+                       double* __restrict__ r_y, double* __restrict__ g_x,
+                       double* __restrict__ g_y, double* __restrict__ sq_obs,
+                       double* __restrict__ sq_acc, double* __restrict__ sq_nonhol) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= l) return;
+  double so = 0.0, sa_ = 0.0, sn = 0.0;
+  for (long long row = 0; row < mn; ++row) {
+    const long long k = row % n;
+    const long long e = row * l + c;
+    const double wx = x[k * l + c] - xi_x[row];
+    const double wy = y[k * l + c] - xi_y[row];
+    const double px = b * wx, py = a * wy;
+    const double r = sqrt(px * px + py * py);
+    if (WITH_ANGLES) alpha[e] = atan2(py, px);
+    double ca, sa;
+    if (r > 0.0) {
+      ca = px / r;
+      sa = py / r;
+    } else {
+      ca = 1.0;
+      sa = 0.0;
+    }
+    double dd = r / (a * b);
+    if (dd < 1.0) dd = 1.0;
+    d[e] = dd;
+    const double adca = a * dd * ca, bdsa = b * dd * sa;
+    const double rx = wx - adca, ry = wy - bdsa;
+    r_x[e] = rx;
+    r_y[e] = ry;
+    so += rx * rx + ry * ry;
+    g_x[e] = xi_x[row] + adca;
+    g_y[e] = xi_y[row] + bdsa;
+  }
+  for (int k = 0; k < n; ++k) {
+    const long long i = (long long)k * l + c;
+    const double ax = xdd[i], ay = ydd[i];
+    const double mag = sqrt(ax * ax + ay * ay);
+    if (WITH_ANGLES) alpha_a[i] = atan2(ay, ax);
+    double caa, saa;
+    if (mag > 0.0) {
+      caa = ax / mag;
+      saa = ay / mag;
+    } else {
+      caa = 1.0;
+      saa = 0.0;
+    }
+    const double dd = mag < a_max ? mag : a_max;
+    d_a[i] = dd;
+    const double daca = dd * caa, dasa = dd * saa;
+    double rx = ax - daca, ry = ay - dasa;
+    const long long ea = (mn + k) * l + c;
+    r_x[ea] = rx;
+    r_y[ea] = ry;
+    sa_ += rx * rx + ry * ry;
+    g_x[ea] = daca;
+    g_y[ea] = dasa;
+    double s = sqrt(xd[i] * xd[i] + yd[i] * yd[i]);
+    if (s < v_min) s = v_min;
+    else if (s > v_max) s = v_max;
+    v[i] = s;
+    const double cp = cos(psi[i]), sp = sin(psi[i]);
+    const double vcp = s * cp, vsp = s * sp;
+    rx = xd[i] - vcp;
+    ry = yd[i] - vsp;
+    const long long en = (mn + n + k) * l + c;
+    r_x[en] = rx;
+    r_y[en] = ry;
+    sn += rx * rx + ry * ry;
+    g_x[en] = vcp;
+    g_y[en] = vsp;
+  }
+  if (!WITH_ANGLES) {
+    sq_obs[c] = so;
+    sq_acc[c] = sa_;
+    sq_nonhol[c] = sn;
+  }
+}
+
+// ------------------------------------------------------------------ sampling --
+// (n, L) samples of P c for the planner (planner.py:412-423) and end-of-solve
+// materialisation (solver.py:442-450).  PT is the [3][nb][npad] transposed basis.
+__global__ void k_sample(int n, int npad, int nb, int L, const double* __restrict__ PT,
+                         const double* __restrict__ c_x, const double* __restrict__ c_y,
+                         const double* __restrict__ c_psi, double* x, double* y, double* xd,
+                         double* yd, double* xdd, double* ydd, double* psi, double* psid,
+                         double* v) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (long long)n * L) return;
+  const int k = (int)(e / L);
+  const long long c = e - (long long)k * L;
+  const double* P = PT;
+  const double* Pd = PT + (long long)nb * npad;
+  const double* Pdd = PT + 2LL * nb * npad;
+  double sx = 0, sy = 0, sxd = 0, syd = 0, sxdd = 0, sydd = 0, sp = 0, spd = 0;
+  for (int i = 0; i < nb; ++i) {
+    const double p = P[i * npad + k], pd = Pd[i * npad + k], pdd = Pdd[i * npad + k];
+    const double cx = c_x ? c_x[(long long)i * L + c] : 0.0;
+    const double cy = c_y ? c_y[(long long)i * L + c] : 0.0;
+    const double cp = c_psi ? c_psi[(long long)i * L + c] : 0.0;
+    sx = __fma_rn(p, cx, sx);
+    sy = __fma_rn(p, cy, sy);
+    sxd = __fma_rn(pd, cx, sxd);
+    syd = __fma_rn(pd, cy, syd);
+    sxdd = __fma_rn(pdd, cx, sxdd);
+    sydd = __fma_rn(pdd, cy, sydd);
+    sp = __fma_rn(p, cp, sp);
+    spd = __fma_rn(pd, cp, spd);
+  }
+  if (x) x[e] = sx;
+  if (y) y[e] = sy;
+  if (xd) xd[e] = sxd;
+  if (yd) yd[e] = syd;
+  if (xdd) xdd[e] = sxdd;
+  if (ydd) ydd[e] = sydd;
+  if (psi) psi[e] = sp;
+  if (psid) psid[e] = spd;
+  if (v) v[e] = sqrt(sxd * sxd + syd * syd);
+}
+
+// ---------------------------------------------------------- fused scoring --
+// Warp per instance: sample_plan + collision_ratios + filter_candidates +
+// meta_cost (planner.py:210-245, :412-423) straight from the coefficients.
+using ScoreArgs = bmpc_score_args;
+
+__global__ void k_score(const ScoreArgs S) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= S.L) return;
+  const int inst = warp;
+  const double2* xi = reinterpret_cast<const double2*>(S.xi) + (size_t)(inst / S.l) * S.m * S.n;
+  const double* P = S.PT;
+  const double* Pd = S.PT + (size_t)S.nb * S.npad;
+  double hmax = 0.0, rmin = INFINITY, cost = 0.0;
+  bool any_nan = false;
+  for (int k = lane; k < S.n; k += 32) {
+    double x = 0, y = 0, xd = 0, yd = 0, ps = 0;
+    for (int i = 0; i < S.nb; ++i) {
+      const double p = P[i * S.npad + k], pd = Pd[i * S.npad + k];
+      const size_t o = (size_t)i * S.L + inst;
+      x = __fma_rn(p, S.c_x[o], x);
+      y = __fma_rn(p, S.c_y[o], y);
+      xd = __fma_rn(pd, S.c_x[o], xd);
+      yd = __fma_rn(pd, S.c_y[o], yd);
+      ps = __fma_rn(p, S.c_psi[o], ps);
+    }
+    const double v = sqrt(xd * xd + yd * yd);
+    const double ah = fabs(ps);
+    if (ah != ah) any_nan = true;
+    hmax = fmax(hmax, ah);
+    for (int j = 0; j < S.m; ++j) {
+      const double2 q = __ldg(xi + j * S.n + k);
+      const double wx = (x - q.x) / S.a, wy = (y - q.y) / S.b;
+      rmin = fmin(rmin, sqrt(wx * wx + wy * wy));
+    }
+    if (S.kind == 0) {
+      const double dv = v - S.v_cruise;
+      cost += dv * dv;
+    } else {
+      const double dv = v - S.v_max, dy = y - S.y_rl;
+      cost += S.w1 * (dv * dv) + S.w2 * (dy * dy);
+    }
+  }
+  hmax = warp_max(hmax);
+  rmin = warp_min(rmin);
+  cost = warp_sum(cost);
+  any_nan = __any_sync(BMPC_FULL, any_nan);
+  if (lane == 0) {
+    if (any_nan) hmax = NAN;
+    const double r0 = S.res_final[inst], r1 = S.res_final[(size_t)S.L + inst],
+                 r2 = S.res_final[2 * (size_t)S.L + inst];
+    const double rmax = fmax(r0, fmax(r1, r2));
+    uint8_t f = 0;
+    if (hmax <= S.heading_limit) f |= 1;
+    if (rmax <= S.residual_tol) f |= 2;
+    if (rmin >= S.ratio_min) f |= 4;
+    S.meta[inst] = cost;
+    S.min_ratio[inst] = rmin;
+    S.heading_max[inst] = hmax;
+    S.flags[inst] = f;
+  }
+}
+
+// ------------------------------------------------------------------ argmin --
+// One block per scene: numpy argmin semantics (first minimum; NaN wins) over
+// where(mask, cost, inf) for three masks; -1 encodes "None".
+__device__ __forceinline__ bool better(double c, long long i, double bc, long long bi) {
+  const bool cn = c != c, bn = bc != bc;
+  if (bi < 0) return true;
+  if (cn || bn) return cn && (!bn || i < bi);
+  return c < bc || (c == bc && i < bi);
+}
+
+__global__ void k_argmin(int l, const double* __restrict__ meta, const uint8_t* __restrict__ flags,
+                         long long* best, long long* best_all, long long* best_hc,
+                         long long* nfeas) {
+  const int s = blockIdx.x;
+  __shared__ double sc[3][256];
+  __shared__ long long si[3][256];
+  __shared__ int scount[256];
+  __shared__ int shc[256];
+  double bc[3] = {INFINITY, INFINITY, INFINITY};
+  long long bi[3] = {-1, -1, -1};
+  int cnt = 0, cnt_hc = 0;
+  for (int i = threadIdx.x; i < l; i += blockDim.x) {
+    const long long g = (long long)s * l + i;
+    const double c = meta[g];
+    const uint8_t f = flags[g];
+    const double cf = (f == 7) ? c : INFINITY;
+    const double chc = ((f & 5) == 5) ? c : INFINITY;
+    cnt += (f == 7);
+    cnt_hc += ((f & 5) == 5);
+    if (better(cf, i, bc[0], bi[0])) { bc[0] = cf; bi[0] = i; }
+    if (better(c, i, bc[1], bi[1])) { bc[1] = c; bi[1] = i; }
+    if (better(chc, i, bc[2], bi[2])) { bc[2] = chc; bi[2] = i; }
+  }
+  for (int q = 0; q < 3; ++q) { sc[q][threadIdx.x] = bc[q]; si[q][threadIdx.x] = bi[q]; }
+  scount[threadIdx.x] = cnt;
+  shc[threadIdx.x] = cnt_hc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0, tot_hc = 0;
+    for (int t = 0; t < (int)blockDim.x; ++t) {
+      tot += scount[t];
+      tot_hc += shc[t];
+      for (int q = 0; q < 3; ++q)
+        if (si[q][t] >= 0 && better(sc[q][t], si[q][t], bc[q], bi[q])) {
+          bc[q] = sc[q][t];
+          bi[q] = si[q][t];
+        }
+    }
+    // mask semantics: the filtered argmin is None when nothing passes
+    const bool any_f = tot > 0;
+    const bool any_hc = tot_hc > 0;
+    best[s] = any_f ? bi[0] : -1;
+    best_all[s] = l > 0 ? bi[1] : -1;
+    best_hc[s] = any_hc ? bi[2] : -1;
+    nfeas[s] = tot;
+  }
+}
+
+// ------------------------------------------------------------------- misc --
+__global__ void k_pack_xi(long long total, const double* __restrict__ xi_x,
+                          const double* __restrict__ xi_y, double2* __restrict__ out) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < total) out[e] = make_double2(xi_x[e], xi_y[e]);
+}
+
+// First iteration t whose worst residual over all instances is <= tol
+// (solver.py:437-439); rows >= iters leave *tstar untouched.
+__global__ void k_first_converged(int iters, long long L, const double* __restrict__ hist,
+                                  double tol, int* tstar) {
+  const int t = blockIdx.x;
+  if (t >= iters) return;
+  double mx = -INFINITY;
+  bool nan = false;
+  const double* row = hist + (size_t)t * 3 * L;
+  for (long long e = threadIdx.x; e < 3 * L; e += blockDim.x) {
+    const double v = row[e];
+    if (v != v) nan = true;
+    mx = fmax(mx, v);
+  }
+  mx = warp_max(mx);
+  nan = __any_sync(BMPC_FULL, nan);
+  __shared__ double sm[32];
+  __shared__ int sn[32];
+  if ((threadIdx.x & 31) == 0) { sm[threadIdx.x >> 5] = mx; sn[threadIdx.x >> 5] = nan; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = -INFINITY;
+    bool anynan = false;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { m = fmax(m, sm[w]); anynan |= sn[w] != 0; }
+    // numpy max propagates NaN, and NaN <= tol is False
+    if (!anynan && m <= tol) atomicMin(tstar, t);
+  }
+}
+
+// ---------------------------------------------------------------- launchers --
+cudaError_t op_obstacle_update(int n, int l, long long mn, const double* x, const double* y,
+                               const double* xi_x, const double* xi_y, double a, double b,
+                               double* alpha, double* d, cudaStream_t st) {
+  if (mn * l > 0) k_obstacle_update<<<nblk(mn * l), kTB, 0, st>>>(n, l, mn, x, y, xi_x, xi_y, a, b, alpha, d);
+  return cudaGetLastError();
+}
+cudaError_t op_accel_update(long long nl, const double* xdd, const double* ydd, double a_max,
+                            double* alpha_a, double* d_a, cudaStream_t st) {
+  if (nl > 0) k_accel_update<<<nblk(nl), kTB, 0, st>>>(nl, xdd, ydd, a_max, alpha_a, d_a);
+  return cudaGetLastError();
+}
+cudaError_t op_v_update(long long nl, const double* xd, const double* yd, double v_min,
+                        double v_max, double* v, cudaStream_t st) {
+  if (nl > 0) k_v_update<<<nblk(nl), kTB, 0, st>>>(nl, xd, yd, v_min, v_max, v);
+  return cudaGetLastError();
+}
+cudaError_t op_assemble_g(int n, int l, long long mn, const double* xi_x, const double* xi_y,
+                          const double* alpha, const double* d, const double* alpha_a,
+                          const double* d_a, const double* v, const double* psi, double a,
+                          double b, double* g_x, double* g_y, cudaStream_t st) {
+  const long long tot = (mn + 2LL * n) * l;
+  if (tot > 0)
+    k_assemble_g<<<nblk(tot), kTB, 0, st>>>(n, l, mn, xi_x, xi_y, alpha, d, alpha_a, d_a, v, psi, a, b, g_x, g_y);
+  return cudaGetLastError();
+}
+cudaError_t op_residual_vectors(int n, int l, long long mn, const double* x, const double* y,
+                                const double* xd, const double* yd, const double* xdd,
+                                const double* ydd, const double* psi, const double* xi_x,
+                                const double* xi_y, const double* alpha, const double* d,
+                                const double* alpha_a, const double* d_a, const double* v,
+                                double a, double b, double* r_x, double* r_y, cudaStream_t st) {
+  const long long tot = (mn + 2LL * n) * l;
+  if (tot > 0)
+    k_residual_vectors<<<nblk(tot), kTB, 0, st>>>(n, l, mn, x, y, xd, yd, xdd, ydd, psi, xi_x, xi_y,
+                                                  alpha, d, alpha_a, d_a, v, a, b, r_x, r_y);
+  return cudaGetLastError();
+}
+cudaError_t op_tail(bool with_angles, int n, int l, long long mn, const double* x, const double* y,
+                    const double* xd, const double* yd, const double* xdd, const double* ydd,
+                    const double* psi, const double* xi_x, const double* xi_y, double v_min,
+                    double v_max, double a_max, double a, double b, double* alpha, double* d,
+                    double* alpha_a, double* d_a, double* v, double* r_x, double* r_y,
+                    double* g_x, double* g_y, double* sq_obs, double* sq_acc, double* sq_nonhol,
+                    cudaStream_t st) {
+  if (l <= 0) return cudaSuccess;
+  const int tb = 64;
+  const int grid = (l + tb - 1) / tb;
+  if (with_angles)
+    k_tail<true><<<grid, tb, 0, st>>>(n, l, mn, x, y, xd, yd, xdd, ydd, psi, xi_x, xi_y, v_min, v_max,
+                                      a_max, a, b, alpha, d, alpha_a, d_a, v, r_x, r_y, g_x, g_y,
+                                      sq_obs, sq_acc, sq_nonhol);
+  else
+    k_tail<false><<<grid, tb, 0, st>>>(n, l, mn, x, y, xd, yd, xdd, ydd, psi, xi_x, xi_y, v_min, v_max,
+                                       a_max, a, b, alpha, d, alpha_a, d_a, v, r_x, r_y, g_x, g_y,
+                                       sq_obs, sq_acc, sq_nonhol);
+  return cudaGetLastError();
+}
+cudaError_t op_sample(int n, int npad, int nb, int L, const double* PT, const double* c_x,
+                      const double* c_y, const double* c_psi, double* x, double* y, double* xd,
+                      double* yd, double* xdd, double* ydd, double* psi, double* psid, double* v,
+                      cudaStream_t st) {
+  const long long tot = (long long)n * L;
+  if (tot > 0)
+    k_sample<<<nblk(tot), kTB, 0, st>>>(n, npad, nb, L, PT, c_x, c_y, c_psi, x, y, xd, yd, xdd, ydd,
+                                        psi, psid, v);
+  return cudaGetLastError();
+}
+cudaError_t op_score(const ScoreArgs& S, cudaStream_t st) {
+  if (S.L <= 0) return cudaSuccess;
+  const int warps = 8;
+  k_score<<<(S.L + warps - 1) / warps, warps * 32, 0, st>>>(S);
+  return cudaGetLastError();
+}
+cudaError_t op_argmin(int S, int l, const double* meta, const uint8_t* flags, long long* best,
+                      long long* best_all, long long* best_hc, long long* nfeas, cudaStream_t st) {
+  if (S > 0) k_argmin<<<S, 256, 0, st>>>(l, meta, flags, best, best_all, best_hc, nfeas);
+  return cudaGetLastError();
+}
+cudaError_t op_pack_xi(long long total, const double* xi_x, const double* xi_y, double* out,
+                       cudaStream_t st) {
+  if (total > 0)
+    k_pack_xi<<<nblk(total), kTB, 0, st>>>(total, xi_x, xi_y, reinterpret_cast<double2*>(out));
+  return cudaGetLastError();
+}
+cudaError_t op_first_converged(int iters, long long L, const double* hist, double tol, int* tstar,
+                               cudaStream_t st) {
+  if (iters > 0) k_first_converged<<<iters, 256, 0, st>>>(iters, L, hist, tol, tstar);
+  return cudaGetLastError();
+}
+
+}  // namespace bmpc

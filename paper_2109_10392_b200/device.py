@@ -1,0 +1,143 @@
+"""Device-resident solve / score on torch-allocated HBM buffers.
+
+torch is plumbing here (allocation, streams, pinned host memory); all compute
+runs in the sm_100a kernels behind the C ABI (include/batchmpc_b200.h).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nat
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2109_10392_b200 needs a CUDA device (sm_100a); no CPU fallback")
+    return torch
+
+
+def stream_ptr(stream=None) -> int:
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+@dataclass
+class DeviceProblem:
+    """Stacked scenes on the device: instance s*l + i is goal i of scene s."""
+
+    m: int
+    l: int
+    S: int
+    xi_x: "object"   # torch (S, m*n) float64
+    xi_y: "object"
+    b_xy: "object"   # (12, L)
+    b_psi: "object"  # (4, L)
+    a: float
+    b: float
+    v_min: float
+    v_max: float
+    a_max: float
+
+    @property
+    def L(self) -> int:
+        return self.S * self.l
+
+    def c_struct(self) -> nat.Problem:
+        return nat.Problem(self.m, self.l, self.S, ptr(self.xi_x), ptr(self.xi_y), ptr(self.b_xy),
+                           ptr(self.b_psi), self.a, self.b, self.v_min, self.v_max, self.a_max)
+
+    @staticmethod
+    def from_host(n, xi_x, xi_y, b_xy, b_psi, l, a, b, v_min, v_max, a_max, device=None,
+                  non_blocking=False) -> "DeviceProblem":
+        torch = _torch()
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        xi_x = np.atleast_2d(np.asarray(xi_x, dtype=np.float64))
+        xi_y = np.atleast_2d(np.asarray(xi_y, dtype=np.float64))
+        S = xi_x.shape[0]
+        mn = xi_x.shape[1]
+
+        def up(a):
+            t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
+            if non_blocking:
+                t = t.pin_memory()
+            return t.to(dev, non_blocking=non_blocking)
+
+        if mn % n:
+            raise ValueError(f"obstacle predictions of length {mn} are not a multiple of n={n}")
+        return DeviceProblem(m=mn // n, l=int(l), S=S, xi_x=up(xi_x), xi_y=up(xi_y),
+                             b_xy=up(b_xy), b_psi=up(b_psi), a=float(a), b=float(b),
+                             v_min=float(v_min), v_max=float(v_max), a_max=float(a_max))
+
+
+@dataclass
+class DeviceSolution:
+    c_x: "object"
+    c_y: "object"
+    c_psi: "object"
+    l_x: "object"
+    l_y: "object"
+    l_psi: "object"
+    history: "object"    # (max_iter, 3, L); rows >= iterations are stale
+    res_final: "object"  # (3, L)
+    v: "object"          # (n, L) or None
+    iterations: int
+    converged: bool
+
+
+@dataclass
+class DeviceScore:
+    meta_cost: "object"
+    min_ratio: "object"
+    heading_max: "object"
+    flags: "object"       # uint8: bit0 heading, bit1 residual, bit2 collision
+    best_index: "object"  # (S,) int64, -1 = None
+    argmin_all: "object"
+    argmin_hc: "object"
+    n_feasible: "object"
+
+
+def alloc_solution(nb: int, n: int, L: int, max_iter: int, want_v: bool, device) -> DeviceSolution:
+    torch = _torch()
+    z = lambda *s: torch.empty(*s, dtype=torch.float64, device=device)  # noqa: E731
+    coef = z(6, nb, L)
+    return DeviceSolution(coef[0], coef[1], coef[2], coef[3], coef[4], coef[5],
+                          z(max_iter, 3, L), z(3, L), z(n, L) if want_v else None, 0, False)
+
+
+def solution_struct(sol: DeviceSolution) -> nat.SolveOut:
+    return nat.SolveOut(ptr(sol.c_x), ptr(sol.c_y), ptr(sol.c_psi), ptr(sol.l_x), ptr(sol.l_y),
+                        ptr(sol.l_psi), ptr(sol.v), ptr(sol.history), ptr(sol.res_final), 0, 0)
+
+
+def alloc_score(L: int, S: int, device) -> DeviceScore:
+    torch = _torch()
+    f = lambda: torch.empty(L, dtype=torch.float64, device=device)  # noqa: E731
+    i = lambda: torch.empty(S, dtype=torch.int64, device=device)  # noqa: E731
+    return DeviceScore(f(), f(), f(), torch.empty(L, dtype=torch.uint8, device=device),
+                       i(), i(), i(), i())
+
+
+def score_struct(sc: DeviceScore) -> nat.ScoreOut:
+    return nat.ScoreOut(ptr(sc.meta_cost), ptr(sc.min_ratio), ptr(sc.heading_max), ptr(sc.flags),
+                        ptr(sc.best_index), ptr(sc.argmin_all), ptr(sc.argmin_hc),
+                        ptr(sc.n_feasible))
+
+
+def peak_fp64_tflops(reps: int = 5) -> float:
+    """Measured DFMA throughput of the current device (the FP64-pipe roofline)."""
+    _torch()
+    out = ctypes.c_double(0.0)
+    nat.check(nat.load().bmpc_dfma_peak(reps, ctypes.byref(out), ctypes.c_void_p(stream_ptr())),
+              "dfma_peak")
+    return out.value

@@ -1,0 +1,366 @@
+"""Planner-level API: goal batch in, ranked trajectories + meta costs out.
+
+Mirrors the scoring half of the reference planner
+(/root/reference/pkg/src/batchmpc/planner.py): ``MetaCostSpec``,
+``FilterLimits``, ``RankedPlan``, ``meta_cost``, ``collision_ratios``,
+``filter_candidates``, ``rank``, ``Planner.build_batch``/``boundary_vectors``/
+``sample_plan``.  Sampling, the collision/heading/residual filters, meta costs
+and the argmin (ties -> lowest index, ``None`` when nothing is feasible) run in
+the fused sm_100a scoring kernel (csrc/ops.cu: k_score, k_argmin).
+
+``plan_batch`` is the one-call hot path used by the benchmark: host arrays in,
+solve + score through the C ABI (``bmpc_plan_host``), host results out.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as nat
+from .basis import BoundarySpec, build_basis, build_constant_matrices, build_time_grid
+from .solver import AmState, BatchSolver, ProblemBatch, Residuals
+from .traffic import VehicleState, predict_constant_velocity, select_nearest
+
+
+@dataclass
+class EgoState:
+    x: float
+    y: float
+    psi: float = 0.0
+    psidot: float = 0.0
+    vx: float = 0.0
+    vy: float = 0.0
+    ax: float = 0.0
+    ay: float = 0.0
+
+    @property
+    def speed(self) -> float:
+        return math.hypot(self.vx, self.vy)
+
+
+@dataclass
+class Goal:
+    x: float
+    y: float
+    vx: float
+    vy: float
+    ax: float
+    ay: float
+    lane: int
+
+
+@dataclass(frozen=True)
+class MetaCostSpec:
+    """Task-level scoring (planner.py:78-93)."""
+
+    kind: str
+    v_cruise: float = 15.0
+    v_max: float = 20.0
+    y_rl: float = 0.0
+    w1: float = 1.0
+    w2: float = 1.0
+
+    def __post_init__(self):
+        if self.kind not in ("cruise", "highspeed"):
+            raise ValueError(f"unknown meta-cost kind {self.kind!r}")
+        if self.w1 < 0 or self.w2 < 0:
+            raise ValueError("meta-cost weights must be nonnegative")
+
+
+@dataclass(frozen=True)
+class FilterLimits:
+    heading_limit: float = math.radians(13.0)
+    residual_tol: float = 1e-3
+    collision_margin: float = 0.01
+
+
+@dataclass
+class Candidate:
+    x: np.ndarray
+    y: np.ndarray
+    psi: np.ndarray
+    psidot: np.ndarray
+    v: np.ndarray
+    xddot: np.ndarray
+    yddot: np.ndarray
+
+
+@dataclass
+class RankedPlan:
+    """Sampled candidates, filter results, costs and the selection (planner.py:162-194)."""
+
+    goals: list
+    x: np.ndarray
+    y: np.ndarray
+    psi: np.ndarray
+    psidot: np.ndarray
+    v: np.ndarray
+    xddot: np.ndarray
+    yddot: np.ndarray
+    residuals: Residuals
+    min_ratio: np.ndarray = field(default=None)
+    heading_max: np.ndarray = field(default=None)
+    feasible: np.ndarray = field(default=None)
+    meta_cost: np.ndarray = field(default=None)
+    best_index: int | None = None
+    _dev: dict = field(default=None, repr=False)  # device coefficients for the fused kernels
+
+    @property
+    def l(self) -> int:
+        return self.x.shape[1]
+
+    def candidate(self, i: int) -> Candidate:
+        return Candidate(x=self.x[:, i], y=self.y[:, i], psi=self.psi[:, i],
+                         psidot=self.psidot[:, i], v=self.v[:, i], xddot=self.xddot[:, i],
+                         yddot=self.yddot[:, i])
+
+    def best(self) -> Candidate:
+        if self.best_index is None:
+            raise ValueError("no feasible candidate was selected")
+        return self.candidate(self.best_index)
+
+
+def _spec_struct(spec: MetaCostSpec | None, limits: FilterLimits) -> nat.ScoreSpec:
+    spec = spec or MetaCostSpec("cruise")
+    return nat.ScoreSpec(0 if spec.kind == "cruise" else 1, spec.v_cruise, spec.v_max, spec.y_rl,
+                         spec.w1, spec.w2, limits.heading_limit, limits.residual_tol,
+                         limits.collision_margin)
+
+
+def meta_cost(traj: Candidate, spec: MetaCostSpec) -> float:
+    """Scalar meta cost of one candidate (planner.py:210-216).  Per-candidate
+    helper only; batched scoring runs in the fused kernel (``rank``)."""
+    if spec.kind == "cruise":
+        return float(np.sum((traj.v - spec.v_cruise) ** 2))
+    return float(np.sum(spec.w1 * (traj.v - spec.v_max) ** 2 + spec.w2 * (traj.y - spec.y_rl) ** 2))
+
+
+def collision_ratios(x, y, xi_x, xi_y, a, b):
+    """(m*n, l) ellipse separation ratios recomputed from positions (planner.py:219-230)."""
+    import torch
+
+    A = [torch.as_tensor(np.asarray(t, dtype=np.float64) if not isinstance(t, torch.Tensor) else t)
+         for t in (x, y, xi_x, xi_y)]
+    host = not A[0].is_cuda
+    dev = torch.device("cuda", torch.cuda.current_device())
+    x, y, xi_x, xi_y = (t.to(dev) for t in A)
+    n = x.shape[0]
+    m = xi_x.shape[0] // n if n else 0
+    wx = (x.repeat(m, 1) - xi_x[:, None]) / a
+    wy = (y.repeat(m, 1) - xi_y[:, None]) / b
+    r = torch.sqrt(wx * wx + wy * wy)
+    return r.cpu().numpy() if host else r
+
+
+def _score_plan(plan: RankedPlan, batch: ProblemBatch, limits: FilterLimits,
+                spec: MetaCostSpec | None):
+    import torch
+
+    from . import device as D
+
+    if plan._dev is None:
+        raise ValueError("RankedPlan was not produced by Planner.sample_plan of this package")
+    dv = plan._dev
+    solver: BatchSolver = dv["solver"]
+    ctx = solver._context()
+    prob = dv.get("prob")
+    if prob is None:
+        prob = solver.device_problem(batch)
+        dv["prob"] = prob
+    L = prob.L
+    sc = D.alloc_score(L, prob.S, prob.b_xy.device)
+    nat.check(nat.load().bmpc_score(ctx, ctypes.byref(prob.c_struct()), D.ptr(dv["c_x"]),
+                                    D.ptr(dv["c_y"]), D.ptr(dv["c_psi"]), D.ptr(dv["res"]),
+                                    ctypes.byref(_spec_struct(spec, limits)), ctypes.byref(D.score_struct(sc)),
+                                    ctypes.c_void_p(D.stream_ptr())), "score")
+    del torch
+    return sc
+
+
+def filter_candidates(plan: RankedPlan, batch: ProblemBatch, limits: FilterLimits) -> np.ndarray:
+    """Heading, residual and recomputed-collision filters (planner.py:233-245)."""
+    sc = _score_plan(plan, batch, limits, None)
+    flags = sc.flags.cpu().numpy()
+    plan.heading_max = sc.heading_max.cpu().numpy()
+    plan.min_ratio = sc.min_ratio.cpu().numpy() if batch.xi_x.size else np.full(plan.l, np.inf)
+    plan.feasible = flags == 7
+    plan._dev["limits"] = limits
+    return plan.feasible
+
+
+def rank(plan: RankedPlan, spec: MetaCostSpec) -> RankedPlan:
+    """Meta cost of every candidate and the cheapest feasible one (planner.py:248-257)."""
+    limits = plan._dev.get("limits", FilterLimits()) if plan._dev else FilterLimits()
+    batch = plan._dev.get("batch") if plan._dev else None
+    sc = _score_plan(plan, batch, limits, spec)
+    plan.meta_cost = sc.meta_cost.cpu().numpy()
+    if plan.feasible is None:
+        plan.best_index = None
+    else:
+        feas = plan.feasible
+        if not feas.any():
+            plan.best_index = None
+        else:
+            # device argmin over the mask the caller's filter produced
+            b = int(sc.best_index.cpu().numpy()[0])
+            plan.best_index = b if b >= 0 else None
+    return plan
+
+
+def sample_goals_uniform(rng: np.random.Generator, ego: EgoState, l: int, t_f: float,
+                         y_range=(-5.25, 5.25), v_range=(10.0, 30.0)) -> list[Goal]:
+    """The BASELINE c1-c4 goal sampler: lateral target and terminal speed uniform."""
+    ys = rng.uniform(*y_range, l)
+    vs = rng.uniform(*v_range, l)
+    return [Goal(x=ego.x + v * t_f, y=float(y), vx=float(v), vy=0.0, ax=0.0, ay=0.0, lane=-1)
+            for y, v in zip(ys, vs)]
+
+
+@dataclass(frozen=True)
+class PlannerConfig:
+    l: int = 11
+    n: int = 100
+    t_f: float = 10.0
+    degree: int = 10
+    rho_xy: float = 1.0
+    max_iter: int = 100
+    tol: float = 1e-3
+    m: int = 10
+    a: float = 5.6
+    b: float = 3.1
+    v_min: float = 0.1
+    v_max: float = 20.0
+    a_max: float = 8.0
+    h: float = 2.5
+    dt_cycle: float = 0.1
+    warm_start: bool = True
+    warm_residual_cap: float = 0.2
+    limits: FilterLimits = FilterLimits()
+
+
+class Planner:
+    """Owns the shared constants; builds goal batches and scores solutions
+    (planner.py:308-423)."""
+
+    def __init__(self, cfg: PlannerConfig, lanes=None, meta: MetaCostSpec | None = None):
+        self.cfg = cfg
+        self.lanes = lanes
+        self.meta = meta or MetaCostSpec("cruise")
+        grid = build_time_grid(0.0, cfg.t_f, cfg.n)
+        self.basis = build_basis(grid, cfg.degree)
+        self.mats = build_constant_matrices(self.basis, cfg.m, BoundarySpec())
+        self.solver = BatchSolver(self.basis, self.mats, cfg.rho_xy)
+
+    def boundary_vectors(self, ego: EgoState, goals: list[Goal]) -> tuple[np.ndarray, np.ndarray]:
+        l = len(goals)
+        b_xy = np.empty((12, l))
+        b_psi = np.empty((4, l))
+        for i, g in enumerate(goals):
+            b_xy[:, i] = [ego.x, ego.vx, ego.ax, g.x, g.vx, g.ax, ego.y, ego.vy, ego.ay, g.y, g.vy, g.ay]
+            b_psi[:, i] = [ego.psi, ego.psidot, 0.0, 0.0]
+        return b_xy, b_psi
+
+    def build_batch(self, ego: EgoState, vehicles: list[VehicleState], goals: list[Goal]
+                    ) -> ProblemBatch:
+        nearest = select_nearest(vehicles, ego.x, ego.y, self.cfg.m)
+        xi_x, xi_y = predict_constant_velocity(nearest, self.basis.grid.times)
+        b_xy, b_psi = self.boundary_vectors(ego, goals)
+        c = self.cfg
+        return ProblemBatch(l=len(goals), xi_x=xi_x, xi_y=xi_y, a=c.a, b=c.b, v_min=c.v_min,
+                            v_max=c.v_max, a_max=c.a_max, b_xy=b_xy, b_psi=b_psi, rho_xy=c.rho_xy)
+
+    def sample_plan(self, state: AmState, goals: list, residuals: Residuals,
+                    batch: ProblemBatch | None = None) -> RankedPlan:
+        """x, y, psi, psidot, v = |(xdot, ydot)| (unclipped), xddot, yddot
+        (planner.py:412-423), sampled on the device."""
+        import torch
+
+        from .device import DeviceSolution
+
+        dev = torch.device("cuda", torch.cuda.current_device())
+        up = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)  # noqa: E731
+        cx, cy, cp = up(state.c_x), up(state.c_y), up(state.c_psi)
+        res = up(np.stack([residuals.r_obs, residuals.r_acc, residuals.r_nonhol]))
+        sol = DeviceSolution(cx, cy, cp, None, None, None, None, res, None, 0, False)
+        smp = self.solver.sample_device(sol, which=("x", "y", "psi", "psidot", "v", "xddot", "yddot"))
+        h = {k: v.cpu().numpy() for k, v in smp.items()}
+        return RankedPlan(goals=goals, x=h["x"], y=h["y"], psi=h["psi"], psidot=h["psidot"], v=h["v"],
+                          xddot=h["xddot"], yddot=h["yddot"], residuals=residuals,
+                          _dev=dict(solver=self.solver, c_x=cx, c_y=cy, c_psi=cp, res=res, batch=batch))
+
+
+@dataclass
+class PlanResult:
+    """Output of plan_batch for S stacked scenes x l goals (host arrays)."""
+
+    c_x: np.ndarray
+    c_y: np.ndarray
+    c_psi: np.ndarray
+    res_final: np.ndarray      # (3, L)
+    meta_cost: np.ndarray      # (L,)
+    min_ratio: np.ndarray
+    heading_max: np.ndarray
+    flags: np.ndarray          # uint8 bit0 heading, bit1 residual, bit2 collision
+    best_index: list           # per scene, None when nothing is feasible
+    argmin_all: np.ndarray
+    argmin_hc: np.ndarray      # -1 = None
+    n_feasible: np.ndarray
+    iterations: int
+    converged: bool
+
+    @property
+    def feasible(self) -> np.ndarray:
+        return self.flags == 7
+
+
+def plan_batch(solver: BatchSolver, scenes, max_iter: int = 100, tol: float = 0.0,
+               spec: MetaCostSpec | None = None, limits: FilterLimits | None = None,
+               stream=None) -> PlanResult:
+    """Solve + score S stacked scenes in one C-ABI call from host buffers
+    (``bmpc_plan_host``): the end-to-end path the benchmark times.
+
+    ``scenes`` is a ProblemBatch (one scene) or any object with the SceneBatch
+    fields (xi_x/xi_y (S, m*n), b_xy (12, S*l), b_psi (4, S*l), l, S, scalars).
+    """
+    from .device import stream_ptr
+
+    limits = limits or FilterLimits()
+    if isinstance(scenes, ProblemBatch):
+        solver._check_batch(scenes)
+        xi_x, xi_y, S = scenes.xi_x[None, :], scenes.xi_y[None, :], 1
+    else:
+        xi_x, xi_y, S = scenes.xi_x, scenes.xi_y, scenes.S
+    l = scenes.l
+    L = S * l
+    nb, n = solver.basis.n_b, solver.basis.grid.n
+    c = lambda a: np.ascontiguousarray(a, dtype=np.float64)  # noqa: E731
+    xi_x, xi_y, b_xy, b_psi = c(xi_x), c(xi_y), c(scenes.b_xy), c(scenes.b_psi)
+    if xi_x.shape[1] % n:
+        raise ValueError("obstacle predictions must have m*n entries per scene")
+    ctx = solver._context()
+    prob = nat.Problem(xi_x.shape[1] // n, l, S, xi_x.ctypes.data, xi_y.ctypes.data,
+                       b_xy.ctypes.data, b_psi.ctypes.data, scenes.a, scenes.b, scenes.v_min,
+                       scenes.v_max, scenes.a_max)
+    opts = nat.SolveOpts(max_iter=int(max_iter), tol=float(tol))
+    coef = np.empty((3, nb, L))
+    res = np.empty((3, L))
+    out = nat.SolveOut(coef[0].ctypes.data, coef[1].ctypes.data, coef[2].ctypes.data, None, None,
+                       None, None, None, res.ctypes.data, 0, 0)
+    meta, mr, hm = np.empty(L), np.empty(L), np.empty(L)
+    flags = np.empty(L, dtype=np.uint8)
+    best, amin, ahc, nf = (np.empty(S, dtype=np.int64) for _ in range(4))
+    so = nat.ScoreOut(meta.ctypes.data, mr.ctypes.data, hm.ctypes.data, flags.ctypes.data,
+                      best.ctypes.data, amin.ctypes.data, ahc.ctypes.data, nf.ctypes.data)
+    nat.check(nat.load().bmpc_plan_host(ctx, ctypes.byref(prob), ctypes.byref(opts), ctypes.byref(out),
+                                        ctypes.byref(_spec_struct(spec, limits)), ctypes.byref(so),
+                                        ctypes.c_void_p(stream_ptr(stream))), "plan")
+    solver.kkt.n_solves += 2 * out.iterations
+    return PlanResult(c_x=coef[0], c_y=coef[1], c_psi=coef[2], res_final=res, meta_cost=meta,
+                      min_ratio=mr, heading_max=hm, flags=flags,
+                      best_index=[int(b) if b >= 0 else None for b in best], argmin_all=amin,
+                      argmin_hc=ahc, n_feasible=nf, iterations=out.iterations,
+                      converged=bool(out.converged))

@@ -1,0 +1,242 @@
+"""Generate the golden fixtures by running the REFERENCE itself.
+
+Runs only in the build container (it imports /root/reference, which does not
+exist on the GPU box); the .npz outputs are committed.  The reference's
+compiled backend is the Cython extension built from the reference's own
+sources by oracle/Makefile (target `ref`), registered into the reference's
+kernel registry for the duration of this script.
+
+    python tests/golden/make_golden.py
+
+Fixtures (float64 unless noted):
+  tail_case.npz   inputs + outputs of every reference kernel (compiled and numpy
+                  back-ends) on the sample data shape of the reference's
+                  tests/test_kernels.py (n=50, m=4, l=7, rng seed 12345)
+  demo.npz        oracles.make_demo_batch(l=11, seed=0) on the canonical solver
+                  (n=100, m=10, degree 10, t_f=10), 80 sweeps, tol=0
+  c0.npz, c1.npz  BASELINE configs 0 and 1 (scenes.make_workload), 100 sweeps,
+                  plus the 1-ulp self-sensitivity screen and planner scoring
+  c3s.npz         4 scenes x 64 goals of the c3 generator (m=20), 100 sweeps
+  c4s.npz         2 scenes x 32 goals of the c4 generator (n=200, n_b=16, m=50), 100 sweeps
+  reverse.npz     goals behind a reversing ego: headings cross +-pi so the
+                  np.unwrap corrections are non-zero (40 sweeps)
+"""
+
+from __future__ import annotations
+
+import math
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+ROOT = HERE.parents[1]
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "oracle"))
+
+from threadpoolctl import threadpool_limits  # noqa: E402
+
+threadpool_limits(1)
+
+import am_oracle  # noqa: E402
+import batchmpc  # noqa: E402
+from batchmpc import build_basis, build_constant_matrices, build_time_grid  # noqa: E402
+from batchmpc import kernels as rk  # noqa: E402
+from batchmpc.kernels import _numpy as rnp  # noqa: E402
+from batchmpc.oracles import demo_solver, make_demo_batch  # noqa: E402
+from batchmpc.planner import (FilterLimits, MetaCostSpec, RankedPlan,  # noqa: E402
+                              filter_candidates, rank)
+from batchmpc.solver import BatchSolver, ProblemBatch  # noqa: E402
+
+from paper_2109_10392_b200.scenes import make_workload  # noqa: E402
+
+REF = am_oracle._load_ref_kernels()
+if REF is None:
+    raise SystemExit("build the reference kernels first: make -C oracle ref")
+rk._BACKENDS["compiled"] = REF
+rk.set_backend("compiled")
+
+
+def ref_solver(n, t_f, degree, m):
+    grid = build_time_grid(0.0, t_f, n)
+    basis = build_basis(grid, degree)
+    return BatchSolver(basis, build_constant_matrices(basis, m), 1.0)
+
+
+def trajectories(solver, st):
+    P = solver.basis.P
+    return [P @ st.c_x, P @ st.c_y, P @ st.c_psi]
+
+
+def rel_div(solver, a, b):
+    out = np.zeros(a.c_x.shape[1])
+    for ta, tb in zip(trajectories(solver, a), trajectories(solver, b)):
+        scale = np.maximum(1.0, np.abs(ta).max(axis=0))
+        out = np.maximum(out, np.abs(ta - tb).max(axis=0) / scale)
+    return out
+
+
+def score(solver, st, info, batch, spec):
+    P, Pd, Pdd = solver.basis.P, solver.basis.Pdot, solver.basis.Pddot
+    xd, yd = Pd @ st.c_x, Pd @ st.c_y
+    plan = RankedPlan(goals=[None] * batch.l, x=P @ st.c_x, y=P @ st.c_y, psi=P @ st.c_psi,
+                      psidot=Pd @ st.c_psi, v=np.sqrt(xd**2 + yd**2), xddot=Pdd @ st.c_x,
+                      yddot=Pdd @ st.c_y, residuals=info.residual_history[-1])
+    limits = FilterLimits()
+    filter_candidates(plan, batch, limits)
+    rank(plan, spec)
+    hc = (plan.heading_max <= limits.heading_limit) & (plan.min_ratio >= 1.0 - limits.collision_margin)
+    best_hc = int(np.argmin(np.where(hc, plan.meta_cost, np.inf))) if hc.any() else -1
+    return dict(meta_cost=plan.meta_cost, feasible=plan.feasible.astype(np.uint8),
+                min_ratio=plan.min_ratio, heading_max=plan.heading_max,
+                best_index=np.int64(-1 if plan.best_index is None else plan.best_index),
+                argmin_all=np.int64(np.argmin(plan.meta_cost)), argmin_hc=np.int64(best_hc))
+
+
+def solve_scene(solver, xi_x, xi_y, b_xy, b_psi, W, iters, screen):
+    batch = ProblemBatch(l=b_xy.shape[1], xi_x=xi_x, xi_y=xi_y, a=W.a, b=W.b, v_min=W.v_min,
+                         v_max=W.v_max, a_max=W.a_max, b_xy=b_xy, b_psi=b_psi)
+    st, info = solver.solve(batch, max_iter=iters, tol=0.0)
+    out = dict(c_x=st.c_x, c_y=st.c_y, c_psi=st.c_psi, lambda_x=st.lambda_x, lambda_y=st.lambda_y,
+               lambda_psi=st.lambda_psi,
+               res_final=np.stack([info.residual_history[-1].r_obs, info.residual_history[-1].r_acc,
+                                   info.residual_history[-1].r_nonhol]))
+    if screen:
+        pb = ProblemBatch(l=batch.l, xi_x=xi_x * (1.0 + 2.2e-16), xi_y=xi_y, a=W.a, b=W.b,
+                          v_min=W.v_min, v_max=W.v_max, a_max=W.a_max, b_xy=b_xy, b_psi=b_psi)
+        st2, _ = solver.solve(pb, max_iter=iters, tol=0.0)
+        out["screen_div"] = rel_div(solver, st, st2)
+    for kind, spec in (("cruise", MetaCostSpec("cruise", v_cruise=20.0)),
+                       ("highspeed", MetaCostSpec("highspeed", v_max=25.0, y_rl=-5.25, w1=1.0, w2=0.1))):
+        for k, v in score(solver, st, info, batch, spec).items():
+            out[f"{kind}_{k}"] = v
+    return st, info, out
+
+
+def workload_fixture(name, W, iters, screen=True, extra=None):
+    solver = ref_solver(W.n, W.t_f, W.degree, W.m)
+    outs = []
+    for s in range(W.S):
+        cols = slice(s * W.l, (s + 1) * W.l)
+        _, info, o = solve_scene(solver, W.xi_x[s], W.xi_y[s], W.b_xy[:, cols], W.b_psi[:, cols], W,
+                                 iters, screen)
+        if extra is not None:
+            extra(o, info)
+        outs.append(o)
+    data = dict(n=W.n, t_f=W.t_f, degree=W.degree, m=W.m, l=W.l, S=W.S, iters=iters,
+                a=W.a, b=W.b, v_min=W.v_min, v_max=W.v_max, a_max=W.a_max,
+                xi_x=W.xi_x, xi_y=W.xi_y, b_xy=W.b_xy, b_psi=W.b_psi)
+    for k in outs[0]:
+        vals = [o[k] for o in outs]
+        if np.ndim(vals[0]) == 0:
+            data[k] = np.array(vals)
+        elif k in ("c_x", "c_y", "c_psi", "lambda_x", "lambda_y", "lambda_psi", "res_final", "history"):
+            data[k] = np.concatenate(vals, axis=-1)
+        else:
+            data[k] = np.concatenate(vals, axis=0)
+    np.savez_compressed(HERE / f"{name}.npz", **data)
+    print(name, {k: np.shape(v) for k, v in data.items() if np.ndim(v)})
+
+
+def tail_case():
+    rng = np.random.default_rng(12345)
+    n, m, l = 50, 4, 7
+    mn = m * n
+    s = dict(
+        x=rng.normal(75, 40, (n, l)), y=rng.normal(6, 3, (n, l)),
+        xdot=rng.normal(15, 2, (n, l)), ydot=rng.normal(0, 1, (n, l)),
+        xddot=rng.normal(0, 2, (n, l)), yddot=rng.normal(0, 2, (n, l)),
+        psi=rng.normal(0, 0.1, (n, l)),
+        xi_x=rng.normal(75, 50, mn), xi_y=rng.normal(6, 4, mn),
+        alpha=rng.uniform(-np.pi, np.pi, (mn, l)), d=1 + rng.uniform(0, 2, (mn, l)),
+        alpha_a=rng.uniform(-np.pi, np.pi, (n, l)), d_a=rng.uniform(0, 8, (n, l)),
+        v=rng.uniform(5, 20, (n, l)),
+    )
+    # exact zero-length cases for the (1, 0) fallbacks
+    s["xddot"][3, 2] = s["yddot"][3, 2] = 0.0
+    s["x"][5, 1] = s["xi_x"][5]
+    s["y"][5, 1] = s["xi_y"][5]
+    out = dict(s)
+    args = (s["x"], s["y"], s["xdot"], s["ydot"], s["xddot"], s["yddot"], s["psi"],
+            s["xi_x"], s["xi_y"], 0.1, 20.0, 8.0, 5.6, 3.1)
+    for tag, mod in (("ref", REF), ("np", rnp)):
+        for name, val in zip(("d", "d_a", "v", "r_x", "r_y", "g_x", "g_y", "sq_obs", "sq_acc", "sq_nonhol"),
+                             mod.tail_core(*args)):
+            out[f"{tag}_core_{name}"] = np.asarray(val)
+        for name, val in zip(("alpha", "d", "alpha_a", "d_a", "v", "r_x", "r_y", "g_x", "g_y"),
+                             mod.tail_update(*args)):
+            out[f"{tag}_upd_{name}"] = np.asarray(val)
+        al, d = mod.obstacle_update(s["x"], s["y"], s["xi_x"], s["xi_y"], 5.6, 3.1)
+        out[f"{tag}_obs_alpha"], out[f"{tag}_obs_d"] = al, d
+        al, da = mod.accel_update(s["xddot"], s["yddot"], 8.0)
+        out[f"{tag}_acc_alpha_a"], out[f"{tag}_acc_d_a"] = al, da
+        out[f"{tag}_v"] = mod.v_update(s["xdot"], s["ydot"], 0.1, 20.0)
+        gx, gy = mod.assemble_g(s["xi_x"], s["xi_y"], s["alpha"], s["d"], s["alpha_a"], s["d_a"],
+                                s["v"], s["psi"], 5.6, 3.1)
+        out[f"{tag}_g_x"], out[f"{tag}_g_y"] = gx, gy
+        rx, ry = mod.residual_vectors(s["x"], s["y"], s["xdot"], s["ydot"], s["xddot"], s["yddot"],
+                                      s["psi"], s["xi_x"], s["xi_y"], s["alpha"], s["d"],
+                                      s["alpha_a"], s["d_a"], s["v"], 5.6, 3.1)
+        out[f"{tag}_r_x"], out[f"{tag}_r_y"] = rx, ry
+    np.savez_compressed(HERE / "tail_case.npz", **out)
+    print("tail_case", len(out))
+
+
+def demo():
+    solver = demo_solver()
+    batch = make_demo_batch(solver, l=11, seed=0)
+    st, info = solver.solve(batch, max_iter=80, tol=0.0, record_iterates=True)
+    it = info.iterates
+    np.savez_compressed(
+        HERE / "demo.npz",
+        n=100, t_f=10.0, degree=10, m=10, l=11, iters=80,
+        xi_x=batch.xi_x, xi_y=batch.xi_y, b_xy=batch.b_xy, b_psi=batch.b_psi,
+        a=batch.a, b=batch.b, v_min=batch.v_min, v_max=batch.v_max, a_max=batch.a_max,
+        c_x=st.c_x, c_y=st.c_y, c_psi=st.c_psi, lambda_x=st.lambda_x, lambda_y=st.lambda_y,
+        lambda_psi=st.lambda_psi, v=st.v, d_a=st.d_a, alpha_a=st.alpha_a, d=st.d, alpha=st.alpha,
+        history=np.stack([[h.r_obs, h.r_acc, h.r_nonhol] for h in info.residual_history]),
+        iter_c_x=np.stack([c[0] for c in it]), iter_c_psi=np.stack([c[2] for c in it]),
+        g0_x=solver._g_parts(solver.init_state(batch), batch)[0],
+    )
+    print("demo")
+
+
+def reverse_case():
+    """Reversing ego with goals behind it: heading targets straddle +-pi."""
+    from paper_2109_10392_b200.scenes import CONFIGS
+
+    cfg = CONFIGS["c0"]
+    W = make_workload("c0", l=24)
+    l = 24
+    rng = np.random.default_rng(99)
+    b_xy = np.zeros((12, l))
+    b_xy[1] = -6.0                       # reversing start speed
+    vg = rng.uniform(-12.0, -4.0, l)
+    b_xy[3] = vg * cfg.t_f
+    b_xy[4] = vg
+    b_xy[6] = 0.0
+    b_xy[7] = rng.uniform(-0.5, 0.5, l)  # lateral start velocity: signs of ydot vary
+    b_xy[9] = rng.uniform(-4.0, 4.0, l)
+    W.b_xy, W.l = b_xy, l
+    W.b_psi = np.zeros((4, l))
+    W.xi_x = W.xi_x + 200.0              # obstacles far ahead: pure heading dynamics
+    workload_fixture("reverse", W, 40, screen=True)
+
+
+def main():
+    t = time.time()
+    tail_case()
+    demo()
+    workload_fixture("c0", make_workload("c0"), 100)
+    workload_fixture("c1", make_workload("c1"), 100)
+    workload_fixture("c3s", make_workload("c3", scenes=4, l=64), 100)
+    workload_fixture("c4s", make_workload("c4", scenes=2, l=32), 100)
+    reverse_case()
+    print(f"done in {time.time() - t:.1f}s; reference version {batchmpc.__version__}")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,90 @@
+"""Operator-level CUDA kernels vs the reference's compiled kernels (golden
+fixture) -- the reference's own backend-equivalence bars
+(tests/test_kernels.py:72-113): <= 1e-12 per kernel, tail_core <= 1e-10."""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _args(s):
+    return (s["x"], s["y"], s["xdot"], s["ydot"], s["xddot"], s["yddot"], s["psi"],
+            s["xi_x"], s["xi_y"], 0.1, 20.0, 8.0, 5.6, 3.1)
+
+
+def test_tail_core_vs_reference(cuda):
+    from paper_2109_10392_b200 import kernels
+
+    s = golden("tail_case")
+    got = kernels.tail_core(*_args(s))
+    names = ("d", "d_a", "v", "r_x", "r_y", "g_x", "g_y", "sq_obs", "sq_acc", "sq_nonhol")
+    for name, g in zip(names, got):
+        ref = s[f"ref_core_{name}"]
+        assert isinstance(g, np.ndarray) and g.shape == ref.shape
+        assert np.abs(g - ref).max() <= 1e-10, name
+    # obstacle and accel blocks use only IEEE add/mul/div/sqrt: bit-identical
+    for name in ("d", "d_a"):
+        np.testing.assert_array_equal(got[names.index(name)], s[f"ref_core_{name}"])
+    mn = s["xi_x"].shape[0]
+    np.testing.assert_array_equal(got[3][:mn], s["ref_core_r_x"][:mn])
+
+
+def test_tail_update_and_simple_kernels(cuda):
+    from paper_2109_10392_b200 import kernels
+
+    s = golden("tail_case")
+    for name, g in zip(("alpha", "d", "alpha_a", "d_a", "v", "r_x", "r_y", "g_x", "g_y"),
+                       kernels.tail_update(*_args(s))):
+        assert np.abs(g - s[f"ref_upd_{name}"]).max() <= 1e-12, name
+    al, d = kernels.obstacle_update(s["x"], s["y"], s["xi_x"], s["xi_y"], 5.6, 3.1)
+    assert np.abs(al - s["ref_obs_alpha"]).max() <= 1e-12
+    assert np.abs(d - s["ref_obs_d"]).max() <= 1e-12
+    al, da = kernels.accel_update(s["xddot"], s["yddot"], 8.0)
+    assert np.abs(al - s["ref_acc_alpha_a"]).max() <= 1e-12
+    np.testing.assert_array_equal(da, s["ref_acc_d_a"])
+    np.testing.assert_array_equal(kernels.v_update(s["xdot"], s["ydot"], 0.1, 20.0), s["ref_v"])
+    gx, gy = kernels.assemble_g(s["xi_x"], s["xi_y"], s["alpha"], s["d"], s["alpha_a"], s["d_a"],
+                                s["v"], s["psi"], 5.6, 3.1)
+    assert np.abs(gx - s["ref_g_x"]).max() <= 1e-12 and np.abs(gy - s["ref_g_y"]).max() <= 1e-12
+    rx, ry = kernels.residual_vectors(s["x"], s["y"], s["xdot"], s["ydot"], s["xddot"], s["yddot"],
+                                      s["psi"], s["xi_x"], s["xi_y"], s["alpha"], s["d"],
+                                      s["alpha_a"], s["d_a"], s["v"], 5.6, 3.1)
+    assert np.abs(rx - s["ref_r_x"]).max() <= 1e-12 and np.abs(ry - s["ref_r_y"]).max() <= 1e-12
+
+
+def test_zero_length_fallbacks(cuda):
+    from paper_2109_10392_b200 import kernels
+
+    s = golden("tail_case")
+    d, d_a, v, r_x, r_y, g_x, g_y, *_ = kernels.tail_core(*_args(s))
+    n = s["x"].shape[0]
+    mn = s["xi_x"].shape[0]
+    # xddot = yddot = 0 at (3, 2): (cos, sin) = (1, 0), d_a = 0 -> g_acc = 0
+    assert d_a[3, 2] == 0.0 and g_x[mn + 3, 2] == 0.0 and g_y[mn + 3, 2] == 0.0
+    # x == xi at obstacle row 5, column 1: r = 0 -> d = 1, (cos, sin) = (1, 0)
+    assert d[5, 1] == 1.0
+    assert g_x[5, 1] == s["xi_x"][5] + 5.6 and g_y[5, 1] == s["xi_y"][5]
+    del n
+
+
+def test_torch_in_torch_out(cuda):
+    from paper_2109_10392_b200 import kernels
+
+    s = golden("tail_case")
+    t = lambda a: cuda.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    v = kernels.v_update(t(s["xdot"]), t(s["ydot"]), 0.1, 20.0)
+    assert isinstance(v, cuda.Tensor) and v.is_cuda
+    np.testing.assert_array_equal(v.cpu().numpy(), s["ref_v"])
+    with pytest.raises(ValueError):
+        kernels.set_backend("numpy")
+    assert kernels.available_backends() == ("cuda",)
+
+
+def test_dfma_peak_positive(cuda):
+    from paper_2109_10392_b200.device import peak_fp64_tflops
+
+    tf = peak_fp64_tflops(2)
+    assert 1.0 < tf < 200.0

@@ -1,0 +1,253 @@
+"""Parity of the persistent sm_100a AM solver + fused scoring with the
+reference, on the golden fixtures produced by running the reference itself.
+
+Contract: fp64 trajectories x, y, psi within 1e-8
+relative (max_k |gpu - ref| / max(1, max_k |ref|)) on every column the
+reference's own 1-ulp self-sensitivity screen marks stable (divergence <= 1e-10);
+identical best index, identical unfiltered and heading+collision argmins, and
+meta costs within 1e-8 relative on stable columns.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+TRAJ_TOL = 1e-8
+SCREEN = 1e-10
+
+
+def _solver(z):
+    from paper_2109_10392_b200 import make_solver
+
+    return make_solver(int(z["n"]), float(z["t_f"]), int(z["degree"]), int(z["m"]))
+
+
+class _Scenes:
+    def __init__(self, z):
+        self.xi_x, self.xi_y = np.atleast_2d(z["xi_x"]), np.atleast_2d(z["xi_y"])
+        self.b_xy, self.b_psi = z["b_xy"], z["b_psi"]
+        self.l, self.S = int(z["l"]), self.xi_x.shape[0]
+        self.a, self.b = float(z["a"]), float(z["b"])
+        self.v_min, self.v_max, self.a_max = float(z["v_min"]), float(z["v_max"]), float(z["a_max"])
+
+
+def traj_err(P, got, ref):
+    err = np.zeros(got["c_x"].shape[1])
+    for k in ("c_x", "c_y", "c_psi"):
+        tr, tg = P @ ref[k], P @ got[k]
+        scale = np.maximum(1.0, np.abs(tr).max(axis=0))
+        err = np.maximum(err, np.abs(tg - tr).max(axis=0) / scale)
+    return err
+
+
+def _plan(z, kind="cruise"):
+    from paper_2109_10392_b200.planner import FilterLimits, MetaCostSpec, plan_batch
+
+    solver = _solver(z)
+    spec = (MetaCostSpec("cruise", v_cruise=20.0) if kind == "cruise"
+            else MetaCostSpec("highspeed", v_max=25.0, y_rl=-5.25, w1=1.0, w2=0.1))
+    res = plan_batch(solver, _Scenes(z), max_iter=int(z["iters"]), tol=0.0, spec=spec,
+                     limits=FilterLimits())
+    return solver, res
+
+
+@pytest.mark.parametrize("name", ["c0", "c1", "c3s", "c4s", "reverse"])
+def test_solve_and_score_parity(cuda, name):
+    z = golden(name)
+    solver, res = _plan(z)
+    got = dict(c_x=res.c_x, c_y=res.c_y, c_psi=res.c_psi)
+    err = traj_err(solver.basis.P, got, z)
+    stable = z["screen_div"] <= SCREEN
+    print(f"{name}: stable {stable.sum()}/{stable.size}, max rel traj err {err[stable].max():.3e}")
+    assert err[stable].max() <= TRAJ_TOL
+    assert res.iterations == int(z["iters"])
+    np.testing.assert_allclose(res.res_final[:, stable], z["res_final"][:, stable], rtol=1e-6, atol=1e-9)
+    l = int(z["l"])
+    for s in range(int(z["S"])):
+        assert (res.best_index[s] if res.best_index[s] is not None else -1) == int(z["cruise_best_index"][s])
+        assert int(res.argmin_all[s]) == int(z["cruise_argmin_all"][s])
+        assert int(res.argmin_hc[s]) == int(z["cruise_argmin_hc"][s])
+    mc = z["cruise_meta_cost"]
+    rel = np.abs(res.meta_cost - mc) / np.maximum(1.0, np.abs(mc))
+    assert rel[stable].max() <= 1e-8
+    np.testing.assert_array_equal(res.feasible[stable], z["cruise_feasible"][stable].astype(bool))
+    np.testing.assert_allclose(res.min_ratio[stable], z["cruise_min_ratio"][stable], rtol=1e-8)
+    np.testing.assert_allclose(res.heading_max[stable], z["cruise_heading_max"][stable], rtol=1e-7,
+                               atol=1e-12)
+    del l
+
+
+@pytest.mark.parametrize("name", ["c0", "c3s"])
+def test_highspeed_scoring_parity(cuda, name):
+    z = golden(name)
+    _, res = _plan(z, "highspeed")
+    for s in range(int(z["S"])):
+        assert (res.best_index[s] if res.best_index[s] is not None else -1) == int(z["highspeed_best_index"][s])
+        assert int(res.argmin_all[s]) == int(z["highspeed_argmin_all"][s])
+    stable = z["screen_div"] <= SCREEN
+    mc = z["highspeed_meta_cost"]
+    assert (np.abs(res.meta_cost - mc) / np.maximum(1.0, np.abs(mc)))[stable].max() <= 1e-8
+
+
+def _batch(z, cols=None, s=0):
+    from paper_2109_10392_b200 import ProblemBatch
+
+    l = int(z["l"])
+    cols = cols if cols is not None else slice(s * l, (s + 1) * l)
+    bx, bp = z["b_xy"][:, cols], z["b_psi"][:, cols]
+    xi_x = np.atleast_2d(z["xi_x"])[s]
+    xi_y = np.atleast_2d(z["xi_y"])[s]
+    return ProblemBatch(l=bx.shape[1], xi_x=xi_x, xi_y=xi_y, a=float(z["a"]), b=float(z["b"]),
+                        v_min=float(z["v_min"]), v_max=float(z["v_max"]), a_max=float(z["a_max"]),
+                        b_xy=np.ascontiguousarray(bx), b_psi=np.ascontiguousarray(bp))
+
+
+def test_demo_reference_api(cuda):
+    """BatchSolver.solve through the reference-shaped API (demo batch, 80 sweeps):
+    the reference's own cross-backend bars (tests/test_kernels.py:115-130) and
+    the tighter 1e-8 trajectory contract."""
+    z = golden("demo")
+    solver = _solver(z)
+    state, info = solver.solve(_batch(z), max_iter=80, tol=0.0)
+    assert info.iterations == 80 and not info.converged
+    scale = max(1.0, np.abs(z["c_x"]).max())
+    assert np.abs(state.c_x - z["c_x"]).max() <= 1e-7 * scale
+    assert np.abs(state.c_psi - z["c_psi"]).max() <= 1e-7
+    err = traj_err(solver.basis.P, dict(c_x=state.c_x, c_y=state.c_y, c_psi=state.c_psi), z)
+    assert err.max() <= TRAJ_TOL
+    hist = np.stack([[h.r_obs, h.r_acc, h.r_nonhol] for h in info.residual_history])
+    np.testing.assert_allclose(hist[-1], z["history"][-1], rtol=1e-5, atol=1e-9)
+    np.testing.assert_allclose(hist, z["history"], rtol=1e-6, atol=1e-9)
+    for k in ("v", "d_a", "alpha_a", "d", "alpha", "lambda_x", "lambda_y", "lambda_psi"):
+        ref = z[k]
+        assert np.abs(getattr(state, k) - ref).max() <= 1e-6 * max(1.0, np.abs(ref).max()), k
+    assert state.alpha.shape == (1000, 11) and state.iteration == 80
+    assert solver.kkt.n_factorizations == 2 and solver.kkt.n_solves == 2 * 80
+
+
+def test_batch_vs_sequential_bitwise(cuda):
+    z = golden("c0")
+    solver = _solver(z)
+    full, _ = solver.solve(_batch(z), max_iter=40, tol=0.0)
+    for i in (0, 7, 55, 109):
+        one, _ = solver.solve(_batch(z, cols=slice(i, i + 1)), max_iter=40, tol=0.0)
+        for k in ("c_x", "c_y", "c_psi", "lambda_x", "lambda_y", "lambda_psi", "v"):
+            np.testing.assert_array_equal(getattr(one, k)[:, 0], getattr(full, k)[:, i])
+
+
+def test_permutation_and_identical_columns_bitwise(cuda, rng):
+    z = golden("c0")
+    solver = _solver(z)
+    b = _batch(z)
+    perm = rng.permutation(b.l)
+    pb = _batch(z, cols=perm)
+    s1, _ = solver.solve(b, max_iter=30, tol=0.0)
+    s2, _ = solver.solve(pb, max_iter=30, tol=0.0)
+    np.testing.assert_array_equal(s1.c_x[:, perm], s2.c_x)
+    np.testing.assert_array_equal(s1.c_psi[:, perm], s2.c_psi)
+    same = _batch(z, cols=np.array([3, 3, 3, 3]))
+    s3, _ = solver.solve(same, max_iter=30, tol=0.0)
+    assert (s3.c_x == s3.c_x[:, :1]).all() and (s3.c_y == s3.c_y[:, :1]).all()
+
+
+def test_stacked_scenes_equal_single_scene(cuda):
+    from paper_2109_10392_b200.planner import plan_batch
+
+    z = golden("c3s")
+    solver = _solver(z)
+    stacked = plan_batch(solver, _Scenes(z), max_iter=50, tol=0.0)
+    l = int(z["l"])
+    for s in (1, 3):
+        one = plan_batch(solver, _batch(z, s=s), max_iter=50, tol=0.0)
+        np.testing.assert_array_equal(one.c_x, stacked.c_x[:, s * l:(s + 1) * l])
+        np.testing.assert_array_equal(one.meta_cost, stacked.meta_cost[s * l:(s + 1) * l])
+
+
+def test_record_iterates_matches_single_launch(cuda):
+    z = golden("demo")
+    solver = _solver(z)
+    s1, i1 = solver.solve(_batch(z), max_iter=12, tol=0.0, record_iterates=True)
+    s2, i2 = solver.solve(_batch(z), max_iter=12, tol=0.0)
+    np.testing.assert_array_equal(s1.c_x, s2.c_x)
+    np.testing.assert_array_equal(s1.lambda_psi, s2.lambda_psi)
+    assert len(i1.iterates) == 12
+    np.testing.assert_array_equal(i1.iterates[-1][0], s2.c_x)
+    ref = z["iter_c_x"]
+    for t in (0, 5, 11):
+        scale = max(1.0, np.abs(ref[t]).max())
+        assert np.abs(i1.iterates[t][0] - ref[t]).max() <= 1e-8 * scale
+
+
+def test_tol_early_stop_semantics(cuda):
+    import am_oracle as O
+
+    z = golden("demo")
+    solver = _solver(z)
+    b = _batch(z)
+    o = O.OracleSolver(100, 10.0, 10, 10)
+    full = o.solve(b.xi_x, b.xi_y, b.b_xy, b.b_psi, b.a, b.b, b.v_min, b.v_max, b.a_max, 60)
+    worst = full["history"].max(axis=(1, 2))
+    t_stop = 20
+    tol = float(worst[t_stop]) * (1 + 1e-6)
+    expect = int(np.argmax(worst <= tol)) + 1
+    state, info = solver.solve(b, max_iter=60, tol=tol)
+    assert info.converged and info.iterations == expect == len(info.residual_history)
+    state_exact, _ = solver.solve(b, max_iter=expect, tol=0.0)
+    np.testing.assert_array_equal(state.c_x, state_exact.c_x)
+    _, info2 = solver.solve(b, max_iter=5, tol=-1.0)
+    assert info2.iterations == 5 and not info2.converged
+
+
+def test_warm_start_keep_multipliers(cuda):
+    import am_oracle as O
+
+    z = golden("demo")
+    solver = _solver(z)
+    b = _batch(z)
+    first, _ = solver.solve(b, max_iter=25, tol=0.0)
+    o = O.OracleSolver(100, 10.0, 10, 10)
+    warm = {k: getattr(first, k) for k in ("c_x", "c_y", "c_psi", "alpha", "d", "alpha_a", "d_a",
+                                           "v", "lambda_x", "lambda_y", "lambda_psi")}
+    for keep in (False, True):
+        ref = o.solve(b.xi_x, b.xi_y, b.b_xy, b.b_psi, b.a, b.b, b.v_min, b.v_max, b.a_max, 20,
+                      warm=warm, keep_multipliers=keep)
+        st, info = solver.solve(b, max_iter=20, tol=0.0, warm=first, keep_multipliers=keep)
+        err = traj_err(solver.basis.P, dict(c_x=st.c_x, c_y=st.c_y, c_psi=st.c_psi), ref)
+        assert err.max() <= TRAJ_TOL, (keep, err.max())
+    init = solver.init_state(b, warm=first)
+    assert (init.lambda_x == 0).all() and init.iteration == 0
+
+
+def test_cold_init_state_matches_reference(cuda):
+    z = golden("demo")
+    solver = _solver(z)
+    st = solver.init_state(_batch(z))
+    import am_oracle as O
+
+    o = O.OracleSolver(100, 10.0, 10, 10)
+    b = _batch(z)
+    ref = o.init_cold(b.xi_x, b.xi_y, b.b_xy, b.a, b.b, b.v_min, b.v_max, O.kernels("c"))
+    np.testing.assert_array_equal(st.c_x, ref["c_x"])
+    assert np.abs(st.alpha - ref["alpha"]).max() <= 1e-12
+    assert np.abs(st.d - ref["d"]).max() <= 1e-12
+    assert (st.lambda_x == 0).all() and st.iteration == 0
+
+
+def test_solve_validation(cuda):
+    z = golden("demo")
+    solver = _solver(z)
+    with pytest.raises(ValueError):
+        solver.solve(_batch(z), max_iter=0)
+    first, _ = solver.solve(_batch(z), max_iter=2, tol=0.0)
+    first.c_x = first.c_x[:, :-1]
+    with pytest.raises(ValueError):
+        solver.solve(_batch(z), max_iter=2, warm=first)
+
+
+def test_smoke_entry(cuda):
+    import __graft_entry__
+
+    __graft_entry__.smoke()
