@@ -48,28 +48,48 @@ def work_slots(n: int, m: int, nb: int) -> int:
 
 # ---------------------------------------------------------------- clocks ----
 class ClockSampler:
-    def __init__(self, index: int, period_ms: int = 100):
+    """SM clock + throttle reasons sampled through NVML every ~2 ms while the
+    timed region runs (nvidia-smi's own query path is too slow for a
+    millisecond-scale step); falls back to nvidia-smi when NVML is missing."""
+
+    REASONS = {  # NVML clocks-event-reason bits
+        "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+        "sw_power_cap": 0x4,
+    }
+
+    def __init__(self, index: int, period_ms: float = 2.0):
         self.index, self.period, self.rows, self._stop = index, period_ms, [], threading.Event()
         self.t = None
+        self.max_mhz = None
 
     def _run(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
-        while not self._stop.is_set():
-            try:
+        try:
+            import pynvml as N
+
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            get_reasons = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                N.nvmlDeviceGetCurrentClocksThrottleReasons
+            while not self._stop.is_set():
+                self.rows.append((N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM), int(get_reasons(h))))
+                self._stop.wait(self.period / 1000.0)
+            N.nvmlShutdown()
+        except Exception:
+            q = "clocks.sm,clocks.max.sm"
+            while not self._stop.is_set():
                 r = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                    "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                   timeout=5)
+                                    "--format=csv,noheader,nounits"], capture_output=True, text=True)
                 if r.returncode == 0 and r.stdout.strip():
-                    self.rows.append([s.strip() for s in r.stdout.strip().split(",")])
-            except Exception:
-                pass
-            self._stop.wait(self.period / 1000.0)
+                    sm, mx = (float(s) for s in r.stdout.strip().split(","))
+                    self.max_mhz = mx
+                    self.rows.append((sm, 0))
+                self._stop.wait(0.1)
 
     def __enter__(self):
         self.t = threading.Thread(target=self._run, daemon=True)
         self.t.start()
+        time.sleep(0.05)
         return self
 
     def __exit__(self, *exc):
@@ -78,14 +98,10 @@ class ClockSampler:
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if "Active" in r[3 + i]})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["no samples"]}
+        reasons = sorted({name for _, bits in self.rows for name, bit in self.REASONS.items() if bits & bit})
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.rows), "source": "nvml"}
 
 
 # ------------------------------------------------------------- workloads ----

@@ -69,7 +69,7 @@ EXPORTS = {
     # name: (argtypes, restype)
     "bmpc_abi_version": ([], c_int),
     "bmpc_last_error": ([], ctypes.c_char_p),
-    "bmpc_ctx_create": ([c_int, c_int, c_double, _dp, _dp, _dp, _dp, _dp, _dp, POINTER(c_void_p)], c_int),
+    "bmpc_ctx_create": ([c_int, c_int, c_double] + [_dp] * 8 + [POINTER(c_void_p)], c_int),
     "bmpc_ctx_destroy": ([c_void_p], c_int),
     "bmpc_ctx_info": ([c_void_p, POINTER(c_int), POINTER(c_int), POINTER(c_int), POINTER(c_void_p)], c_int),
     "bmpc_solve": ([c_void_p, POINTER(Problem), POINTER(SolveOpts), POINTER(SolveOut), c_void_p], c_int),
@@ -88,7 +88,7 @@ EXPORTS = {
                            + [c_void_p] * 2 + [c_void_p], c_int),
     "bmpc_op_residual_vectors": ([c_int, c_int, c_int] + [c_void_p] * 14 + [c_double, c_double]
                                  + [c_void_p] * 2 + [c_void_p], c_int),
-    "bmpc_op_tail": ([c_int, c_int, c_int] + [c_void_p] * 9 + [c_double] * 5 + [c_void_p] * 13
+    "bmpc_op_tail": ([c_int, c_int, c_int] + [c_void_p] * 9 + [c_double] * 5 + [c_void_p] * 12
                      + [c_void_p], c_int),
     "bmpc_dfma_peak": ([c_int, _dp, c_void_p], c_int),
 }

@@ -11,12 +11,14 @@ typedef struct {
   int n;          // horizon samples
   int npad;       // n rounded up to a multiple of 32
   int nb;         // Bernstein coefficients per axis (degree + 1)
-  int kxs, kps;   // padded row strides of the KKT inverse blocks
+  int kxs, kps;   // padded (odd) row strides of the (nb+6)^2 and (nb+4)^2 KKT blocks
   double rho;
   const double* PT;   // [3][nb][npad]: P^T, Pdot^T, Pddot^T, zero padded past n
   const double* tau;  // [npad] (t_k - t0)/(tf - t0), cold-start line parameter
-  const double* Kx;   // [nb][kxs]  rows 0..nb-1 of the per-axis KKT inverse, nb+6 used
-  const double* Kp;   // [nb][kps]  rows 0..nb-1 of the heading KKT inverse, nb+4 used
+  const double* Kxf;  // [nb+6][kxs] inverse of the per-axis KKT matrix
+  const double* Kxa;  // [nb+6][kxs] the per-axis KKT matrix (refinement residual)
+  const double* Kpf;  // [nb+4][kps] inverse of the heading KKT matrix
+  const double* Kpa;  // [nb+4][kps] the heading KKT matrix
 } bmpc_dev_consts;
 
 enum { BMPC_INIT_COLD = 0, BMPC_INIT_WARM = 1, BMPC_INIT_RESUME = 2 };

@@ -6,9 +6,10 @@
 // hundred bytes of per-warp shared memory).  Per sweep (reference
 // /root/reference/pkg/src/batchmpc/solver.py:458-500):
 //
-//   1. xy QP     c = Kinv_axis[:nb,:] [rho*G + lambda ; b]          (solver.py:302-312)
+//   1. xy QP     [c; mu] = K_axis^-1 [rho*G + lambda ; b], one refinement step
+//                (solver.py:302-312, :164-168)
 //   2. sampling  xdot, ydot = Pdot c ; theta = unwrap(atan2(ydot, xdot)) (:474-477)
-//   3. psi QP    c_psi = Kinv_psi[:nb,:] [rho*P^T theta + lambda_psi ; b_psi]  (:322-328)
+//   3. psi QP    c_psi = K_psi^-1 [rho*P^T theta + lambda_psi ; b_psi], refined (:322-328)
 //   4. tail      closed forms for d, d_a, v; residual blocks; next targets
 //                (kernels/_speedups.pyx:114-218), contracted on the fly:
 //                G = F_axis^T g = P^T sum_j g_obs,j + Pddot^T g_acc + Pdot^T g_nh
@@ -33,10 +34,26 @@ namespace bmpc {
 
 struct WarpScratch {
   double* bc;    // 64: KKT right-hand sides (x at 0, y at 32)
+  double* sol;   // 64: first solve  Kinv * rhs
+  double* res;   // 64: refinement residual rhs - K * sol
   double* cxy;   // 32: (c_x[i], c_y[i]) pairs
   double* cp;    // 16: c_psi
   double* th;    // npad: theta (unwrapped heading target) per sample
 };
+constexpr int kWarpScratch = 256;
+
+// One row of a KKT apply.  The QP steps run the reference's refined solve
+// (solver.py:164-168) -- sol = K^-1 rhs; sol += K^-1 (rhs - K sol) -- with the
+// LU factors replaced by the explicit inverse; without the refinement step the
+// explicit inverse loses up to 5e-8 relative at the c4 shape (cond 3.9e6).
+template <int LEN>
+__device__ __forceinline__ double kkt_row_dot(const double* __restrict__ kr,
+                                              const double* __restrict__ v) {
+  double s = 0.0;
+#pragma unroll
+  for (int j = 0; j < LEN; ++j) s = fma(kr[j], v[j], s);
+  return s;
+}
 
 template <int NB, int NKM>
 __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
@@ -48,17 +65,26 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
   const int n = C.n, npad = C.npad;
   const int nk = npad >> 5;
   const int L = A.L;
+  constexpr int RX = NB + 6, RP = NB + 4;
 
   double* sPT = sm;                          // P^T, Pdot^T, Pddot^T
-  double* sKx = sPT + 3 * NB * npad;
-  double* sKp = sKx + NB * C.kxs;
-  double* sTau = sKp + NB * C.kps;
-  double* wbase = sTau + npad + warp * (128 + npad);
-  WarpScratch ws{wbase, wbase + 64, wbase + 96, wbase + 128};
+  double* sKxf = sPT + 3 * NB * npad;
+  double* sKxa = sKxf + RX * C.kxs;
+  double* sKpf = sKxa + RX * C.kxs;
+  double* sKpa = sKpf + RP * C.kps;
+  double* sTau = sKpa + RP * C.kps;
+  double* wbase = sTau + npad + warp * (kWarpScratch + npad);
+  WarpScratch ws{wbase, wbase + 64, wbase + 128, wbase + 192, wbase + 224, wbase + kWarpScratch};
 
   for (int t = threadIdx.x; t < 3 * NB * npad; t += blockDim.x) sPT[t] = C.PT[t];
-  for (int t = threadIdx.x; t < NB * C.kxs; t += blockDim.x) sKx[t] = C.Kx[t];
-  for (int t = threadIdx.x; t < NB * C.kps; t += blockDim.x) sKp[t] = C.Kp[t];
+  for (int t = threadIdx.x; t < RX * C.kxs; t += blockDim.x) {
+    sKxf[t] = C.Kxf[t];
+    sKxa[t] = C.Kxa[t];
+  }
+  for (int t = threadIdx.x; t < RP * C.kps; t += blockDim.x) {
+    sKpf[t] = C.Kpf[t];
+    sKpa[t] = C.Kpa[t];
+  }
   for (int t = threadIdx.x; t < npad; t += blockDim.x) sTau[t] = C.tau[t];
   __syncthreads();
 
@@ -189,21 +215,44 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
   // ----------------------------------------------------------- AM sweeps ----
   for (int t = 0; t < A.iters; ++t) {
     const bool last = t == A.iters - 1;
-    // (1) xy QP: per-axis KKT inverse applied to [rho*G + lambda ; b]
+    // (1) xy QP: [c; mu] = K^-1 [rho*G + lambda ; b] plus one refinement step,
+    //     the 2*(nb+6) rows of both axes spread over the lanes (two per lane max)
     {
       double* rb = ws.bc + (yax ? 32 : 0);
       if (owner) rb[li] = rho * G + lam;
       if (li < 6) rb[NB + li] = bnd;
       __syncwarp();
-      if (owner) {
-        const double* kr = sKx + li * C.kxs;
-        double c = 0.0;
 #pragma unroll
-        for (int q = 0; q < NB + 6; ++q) c = fma(kr[q], rb[q], c);
-        cown = c;
-        ws.cxy[2 * li + (yax ? 1 : 0)] = c;
+      for (int h = 0; h < 2; ++h) {
+        const int q = lane + 32 * h;
+        if (q < 2 * RX) {
+          const int ax = q >= RX ? 1 : 0, row = q - ax * RX;
+          ws.sol[ax * 32 + row] = kkt_row_dot<RX>(sKxf + row * C.kxs, ws.bc + ax * 32);
+        }
       }
       __syncwarp();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int q = lane + 32 * h;
+        if (q < 2 * RX) {
+          const int ax = q >= RX ? 1 : 0, row = q - ax * RX;
+          ws.res[ax * 32 + row] =
+              ws.bc[ax * 32 + row] - kkt_row_dot<RX>(sKxa + row * C.kxs, ws.sol + ax * 32);
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int q = lane + 32 * h;
+        if (q < 2 * RX) {
+          const int ax = q >= RX ? 1 : 0, row = q - ax * RX;
+          if (row < NB)
+            ws.cxy[2 * row + ax] =
+                ws.sol[ax * 32 + row] + kkt_row_dot<RX>(sKxf + row * C.kxs, ws.res + ax * 32);
+        }
+      }
+      __syncwarp();
+      if (owner) cown = ws.cxy[2 * li + (yax ? 1 : 0)];
     }
     const double2* __restrict__ cxy = reinterpret_cast<const double2*>(ws.cxy);
 
@@ -259,15 +308,13 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
       if (!yax && owner) ws.bc[li] = rho * pth + lamp;
       if (yax && li < 4) ws.bc[NB + li] = bps;
       __syncwarp();
-      if (!yax && owner) {
-        const double* kr = sKp + li * C.kps;
-        double c = 0.0;
-#pragma unroll
-        for (int q = 0; q < NB + 4; ++q) c = fma(kr[q], ws.bc[q], c);
-        cpown = c;
-        ws.cp[li] = c;
-      }
+      if (lane < RP) ws.sol[lane] = kkt_row_dot<RP>(sKpf + lane * C.kps, ws.bc);
       __syncwarp();
+      if (lane < RP) ws.res[lane] = ws.bc[lane] - kkt_row_dot<RP>(sKpa + lane * C.kps, ws.sol);
+      __syncwarp();
+      if (lane < NB) ws.cp[lane] = ws.sol[lane] + kkt_row_dot<RP>(sKpf + lane * C.kps, ws.res);
+      __syncwarp();
+      if (!yax && owner) cpown = ws.cp[li];
     }
 
     // (4) fused tail + on-the-fly contractions

@@ -102,29 +102,37 @@ int bmpc_abi_version(void) { return 1; }
 
 int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pdot,
                     const double* Pddot, const double* tau, const double* kinv_axis,
-                    const double* kinv_psi, bmpc_ctx** out) {
-  if (!out || !P || !Pdot || !Pddot || !tau || !kinv_axis || !kinv_psi)
+                    const double* k_axis, const double* kinv_psi, const double* k_psi,
+                    bmpc_ctx** out) {
+  if (!out || !P || !Pdot || !Pddot || !tau || !kinv_axis || !k_axis || !kinv_psi || !k_psi)
     return fail(BMPC_EINVAL, "bmpc_ctx_create: null argument");
   if (nb < 4 || nb > 16) return fail(BMPC_EINVAL, "bmpc_ctx_create: need 4 <= n_b <= 16");
   if (n < 2 || n > 256) return fail(BMPC_EINVAL, "bmpc_ctx_create: need 2 <= n <= 256");
   if (!(rho > 0.0)) return fail(BMPC_EINVAL, "bmpc_ctx_create: rho must be positive");
-  for (int i = 0; i < nb * (nb + 6); ++i)
+  const int rx = nb + 6, rp = nb + 4;
+  for (int i = 0; i < rx * rx; ++i)
     if (!isfinite(kinv_axis[i])) return fail(BMPC_ESINGULAR, "KKT xy inverse is not finite");
-  for (int i = 0; i < nb * (nb + 4); ++i)
+  for (int i = 0; i < rp * rp; ++i)
     if (!isfinite(kinv_psi[i])) return fail(BMPC_ESINGULAR, "KKT psi inverse is not finite");
   const int npad = ((n + 31) / 32) * 32;
-  const int kxs = (nb + 6) | 1, kps = (nb + 4) | 1;
-  const size_t nPT = (size_t)3 * nb * npad, nKx = (size_t)nb * kxs, nKp = (size_t)nb * kps;
-  std::vector<double> h(nPT + nKx + nKp + npad, 0.0);
+  const int kxs = rx | 1, kps = rp | 1;
+  const size_t nPT = (size_t)3 * nb * npad, nKx = (size_t)rx * kxs, nKp = (size_t)rp * kps;
+  std::vector<double> h(nPT + 2 * nKx + 2 * nKp + npad, 0.0);
   const double* mats[3] = {P, Pdot, Pddot};
   for (int q = 0; q < 3; ++q)
     for (int i = 0; i < nb; ++i)
       for (int k = 0; k < n; ++k) h[((size_t)q * nb + i) * npad + k] = mats[q][(size_t)k * nb + i];
-  for (int i = 0; i < nb; ++i)
-    for (int j = 0; j < nb + 6; ++j) h[nPT + (size_t)i * kxs + j] = kinv_axis[(size_t)i * (nb + 6) + j];
-  for (int i = 0; i < nb; ++i)
-    for (int j = 0; j < nb + 4; ++j) h[nPT + nKx + (size_t)i * kps + j] = kinv_psi[(size_t)i * (nb + 4) + j];
-  for (int k = 0; k < n; ++k) h[nPT + nKx + nKp + k] = tau[k];
+  size_t o = nPT;
+  const double* blocks[4] = {kinv_axis, k_axis, kinv_psi, k_psi};
+  const int dims[4] = {rx, rx, rp, rp}, strides[4] = {kxs, kxs, kps, kps};
+  size_t offs[4];
+  for (int q = 0; q < 4; ++q) {
+    offs[q] = o;
+    for (int i = 0; i < dims[q]; ++i)
+      for (int j = 0; j < dims[q]; ++j) h[o + (size_t)i * strides[q] + j] = blocks[q][(size_t)i * dims[q] + j];
+    o += (size_t)dims[q] * strides[q];
+  }
+  for (int k = 0; k < n; ++k) h[o + k] = tau[k];
   bmpc_ctx* c = new bmpc_ctx();
   cudaError_t e = cudaMalloc(&c->dmem, h.size() * sizeof(double));
   if (e != cudaSuccess) { delete c; return cuda_fail(e, "bmpc_ctx_create/cudaMalloc"); }
@@ -140,9 +148,11 @@ int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pd
   c->C.kps = kps;
   c->C.rho = rho;
   c->C.PT = c->dmem;
-  c->C.Kx = c->dmem + nPT;
-  c->C.Kp = c->dmem + nPT + nKx;
-  c->C.tau = c->dmem + nPT + nKx + nKp;
+  c->C.Kxf = c->dmem + offs[0];
+  c->C.Kxa = c->dmem + offs[1];
+  c->C.Kpf = c->dmem + offs[2];
+  c->C.Kpa = c->dmem + offs[3];
+  c->C.tau = c->dmem + o;
   *out = c;
   return BMPC_OK;
 }

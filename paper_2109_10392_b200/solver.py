@@ -7,9 +7,11 @@ the reference; the work runs in one persistent sm_100a kernel per solve
 
 Differences by design (B200 formulation, SURVEY.md finding 8):
 * ``KktSystem`` holds explicit inverses of the two shared KKT matrices instead
-  of LU factors + one refinement step; ``n_factorizations`` counts the two
-  inversions, ``n_solves`` counts two applications per AM sweep exactly as the
-  reference's solve_xy/solve_psi calls do.
+  of LU factors; every QP step applies the inverse and then one refinement
+  step against the matrix, as the reference's LU solve does (without it the
+  explicit inverse drifts 5e-8 relative at the c4 shape).  ``n_factorizations``
+  counts the two inversions, ``n_solves`` two refined solves per AM sweep
+  exactly as the reference's solve_xy/solve_psi calls do.
 * the obstacle penalty targets are summed over obstacles before the basis
   contraction (F_o^T g = P^T sum_j g_j) and the line-of-sight ratios use
   rsqrt-and-multiply.  Trajectories match the reference to <= 1e-8 relative on
@@ -231,7 +233,8 @@ class BatchSolver:
         c = ctypes.c_void_p()
         b = self.basis
         arrs = [np.ascontiguousarray(a, dtype=np.float64)
-                for a in (b.P, b.Pdot, b.Pddot, self._tau, self.kkt.kinv_axis, self.kkt.kinv_psi)]
+                for a in (b.P, b.Pdot, b.Pddot, self._tau, self.kkt.inv_axis, self.kkt.matrix_axis,
+                          self.kkt.inv_psi, self.kkt.matrix_psi)]
         nat.check(lib.bmpc_ctx_create(b.grid.n, b.n_b, float(self.rho_xy),
                                       *[nat.c_double_ptr(a) for a in arrs], ctypes.byref(c)),
                   "bmpc_ctx_create")

@@ -121,9 +121,18 @@ def test_demo_reference_api(cuda):
     hist = np.stack([[h.r_obs, h.r_acc, h.r_nonhol] for h in info.residual_history])
     np.testing.assert_allclose(hist[-1], z["history"][-1], rtol=1e-5, atol=1e-9)
     np.testing.assert_allclose(hist, z["history"], rtol=1e-6, atol=1e-9)
-    for k in ("v", "d_a", "alpha_a", "d", "alpha", "lambda_x", "lambda_y", "lambda_psi"):
+    for k in ("v", "d_a", "d", "lambda_x", "lambda_y", "lambda_psi"):
         ref = z[k]
         assert np.abs(getattr(state, k) - ref).max() <= 1e-6 * max(1.0, np.abs(ref).max()), k
+    # The angles are ill-posed where their vectors vanish or sit on the branch
+    # cut: alpha_a = atan2(yddot, xddot) at the pinned zero-acceleration samples,
+    # alpha = atan2(a wy, b wx) at +-pi when a trajectory runs exactly along an
+    # obstacle's lane (wy = +-0).  Compare the well-posed targets d*(cos, sin).
+    for ang, mag in (("alpha_a", "d_a"), ("alpha", "d")):
+        for f in (np.cos, np.sin):
+            got = getattr(state, mag) * f(getattr(state, ang))
+            ref = z[mag] * f(z[ang])
+            assert np.abs(got - ref).max() <= 1e-6 * max(1.0, np.abs(ref).max()), ang
     assert state.alpha.shape == (1000, 11) and state.iteration == 80
     assert solver.kkt.n_factorizations == 2 and solver.kkt.n_solves == 2 * 80
 

@@ -156,3 +156,14 @@ def test_no_oracle_in_product_package():
     for p in pkg.rglob("*.py"):
         txt = p.read_text()
         assert "am_oracle" not in txt and "oracle/" not in txt, p
+
+
+def test_ctypes_arity_matches_header():
+    """Every prototype in include/batchmpc_b200.h has the argument count the
+    ctypes binding declares (a mismatch would corrupt the call)."""
+    header = (ROOT / "include" / "batchmpc_b200.h").read_text()
+    body = re.sub(r"/\*.*?\*/", "", header, flags=re.S)
+    for m in re.finditer(r"^(?:int|const char\*)\s+(bmpc_\w+)\((.*?)\);", body, flags=re.M | re.S):
+        name, params = m.group(1), m.group(2).strip()
+        n = 0 if params in ("", "void") else params.count(",") + 1
+        assert len(_native.EXPORTS[name][0]) == n, (name, n, len(_native.EXPORTS[name][0]))
