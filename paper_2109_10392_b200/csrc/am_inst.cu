@@ -24,11 +24,12 @@ static cudaError_t launch_t(const bmpc_dev_consts& C, const bmpc_solve_args& A, 
 cudaError_t BMPC_CAT(launch_am_nb_, BMPC_INST_NB)(const bmpc_dev_consts& C,
                                                    const bmpc_solve_args& A, int warps,
                                                    cudaStream_t st) {
-  const int nk = C.npad / 32;
-  if (nk <= 2) return launch_t<BMPC_INST_NB, 2>(C, A, warps, st);
-  if (nk <= 4) return launch_t<BMPC_INST_NB, 4>(C, A, warps, st);
-  if (nk <= 8) return launch_t<BMPC_INST_NB, 8>(C, A, warps, st);
-  return cudaErrorInvalidValue;
+  switch (C.npad) {  // the host pads n to 64, 128 or 256 samples
+    case 64: return launch_t<BMPC_INST_NB, 2>(C, A, warps, st);
+    case 128: return launch_t<BMPC_INST_NB, 4>(C, A, warps, st);
+    case 256: return launch_t<BMPC_INST_NB, 8>(C, A, warps, st);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 }  // namespace bmpc

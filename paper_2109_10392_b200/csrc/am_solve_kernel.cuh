@@ -39,8 +39,76 @@ struct WarpScratch {
   double* cxy;   // 32: (c_x[i], c_y[i]) pairs
   double* cp;    // 16: c_psi
   double* th;    // npad: theta (unwrapped heading target) per sample
+  double* xd;    // npad: xdot per sample (phase 2 -> phase 4)
+  double* yd;    // npad: ydot per sample
+  double* red;   // 32 x kRedStride: transpose buffer of the sample contractions
 };
 constexpr int kWarpScratch = 256;
+constexpr int kRedStride = 33;
+constexpr int kRedSize = 32 * kRedStride;
+
+// Sum of column `col` of the 32-row transpose buffer, in a fixed order.
+__device__ __forceinline__ double column_sum(const double* __restrict__ red, int col) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+  for (int r = 0; r < 32; r += 4) {
+    s0 += red[(r + 0) * kRedStride + col];
+    s1 += red[(r + 1) * kRedStride + col];
+    s2 += red[(r + 2) * kRedStride + col];
+    s3 += red[(r + 3) * kRedStride + col];
+  }
+  return (s0 + s1) + (s2 + s3);
+}
+
+// Work slot r of a lane.  Samples are dealt round-robin (k = lane + 32 r) for
+// the F = n / 32 full rounds; the R = n % 32 leftover samples either take one
+// lane each (R > 16) or, in split mode, a group of g = 2^floor(log2(32/R))
+// lanes each, the group splitting that sample's obstacles (j = j0, j0+g, ...)
+// so the last round is not 32-R idle lanes deep.  Only the group leader owns
+// the per-sample terms.
+struct SlotLayout {
+  int F, R, g;  // g == 1: no split
+};
+struct Slot {
+  int k, j0, js;
+  bool valid, leader;
+};
+__device__ __forceinline__ SlotLayout slot_layout(int n) {
+  SlotLayout s;
+  s.F = n >> 5;
+  s.R = n & 31;
+  s.g = 1;
+  if (s.R > 0 && s.R <= 16) {
+    int g = 32 / s.R;
+    while (g & (g - 1)) g &= g - 1;
+    s.g = g;
+  }
+  return s;
+}
+__device__ __forceinline__ Slot slot(int r, int lane, const SlotLayout& sl) {
+  Slot S;
+  if (r < sl.F) {
+    S.k = lane + 32 * r;
+    S.j0 = 0;
+    S.js = 1;
+    S.valid = true;
+    S.leader = true;
+  } else if (r == sl.F && sl.R > 0) {
+    const int grp = lane / sl.g;
+    S.k = 32 * sl.F + grp;
+    S.j0 = lane - grp * sl.g;
+    S.js = sl.g;
+    S.valid = grp < sl.R;
+    S.leader = S.j0 == 0;
+  } else {
+    S.k = 0;
+    S.j0 = 0;
+    S.js = 1;
+    S.valid = false;
+    S.leader = false;
+  }
+  return S;
+}
 
 // One row of a KKT apply.  The QP steps run the reference's refined solve
 // (solver.py:164-168) -- sol = K^-1 rhs; sol += K^-1 (rhs - K sol) -- with the
@@ -55,6 +123,31 @@ __device__ __forceinline__ double kkt_row_dot(const double* __restrict__ kr,
   return s;
 }
 
+// Obstacle block of the fused tail for one (obstacle, sample) element
+// (_speedups.pyx:150-176): closed-form d, residual and next target, summed
+// over obstacles into the per-sample accumulators.  rsqrt-and-multiply replaces
+// sqrt and the three divisions (SURVEY.md finding 8).
+__device__ __forceinline__ void obstacle_term(double x, double y, double2 q, double a, double b,
+                                              double inv_ab, double& gsx, double& gsy,
+                                              double& rsx, double& rsy, double& sq) {
+  const double wx = x - q.x, wy = y - q.y;
+  const double px = b * wx, py = a * wy;
+  const double r2 = fma(px, px, py * py);
+  const double ri = rsqrt_nb(r2);
+  // r = 0 -> (cos, sin) = (1, 0), d = 1 (_speedups.pyx:158-166); py = 0 there
+  const double ca = r2 > 0.0 ? px * ri : 1.0;
+  const double sa = py * ri;
+  double dd = (r2 * ri) * inv_ab;
+  dd = dd < 1.0 ? 1.0 : dd;
+  const double adca = (a * dd) * ca, bdsa = (b * dd) * sa;
+  const double rx = wx - adca, ry = wy - bdsa;
+  sq = fma(rx, rx, fma(ry, ry, sq));
+  gsx += q.x + adca;
+  gsy += q.y + bdsa;
+  rsx += rx;
+  rsy += ry;
+}
+
 template <int NB, int NKM>
 __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
                                                        const bmpc_solve_args A) {
@@ -62,8 +155,9 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
   const int W = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int n = C.n, npad = C.npad;
-  const int nk = npad >> 5;
+  const int n = C.n;
+  constexpr int npad = 32 * NKM;  // host pads the basis to exactly this
+  constexpr int nk = NKM;
   const int L = A.L;
   constexpr int RX = NB + 6, RP = NB + 4;
 
@@ -73,8 +167,13 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
   double* sKpf = sKxa + RX * C.kxs;
   double* sKpa = sKpf + RP * C.kps;
   double* sTau = sKpa + RP * C.kps;
-  double* wbase = sTau + npad + warp * (kWarpScratch + npad);
-  WarpScratch ws{wbase, wbase + 64, wbase + 128, wbase + 192, wbase + 224, wbase + kWarpScratch};
+  double* wbase = sTau + npad + warp * (kWarpScratch + 3 * npad + kRedSize);
+  WarpScratch ws{wbase,       wbase + 64,   wbase + 128,
+                 wbase + 192, wbase + 224,  wbase + kWarpScratch,
+                 wbase + kWarpScratch + npad, wbase + kWarpScratch + 2 * npad,
+                 wbase + kWarpScratch + 3 * npad};
+  const SlotLayout sl = slot_layout(n);
+  const int nslots = sl.F + (sl.R > 0 ? 1 : 0);
 
   for (int t = threadIdx.x; t < 3 * NB * npad; t += blockDim.x) sPT[t] = C.PT[t];
   for (int t = threadIdx.x; t < RX * C.kxs; t += blockDim.x) {
@@ -256,29 +355,36 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
     }
     const double2* __restrict__ cxy = reinterpret_cast<const double2*>(ws.cxy);
 
-    // (2) heading target theta = unwrap(atan2(ydot, xdot)) and P^T theta
-    bool wrap = false;
-#pragma unroll
-    for (int r = 0; r < NKM; ++r) {
-      const int k = lane + 32 * r;
-      if (r < nk && k < n) {
+    // (2) heading target theta = unwrap(atan2(ydot, xdot)) and P^T theta.
+    //     Slot r < F: sample lane + 32 r.  Leftover slot (n % 32 samples): split
+    //     mode gives each sample a group of g lanes that share its obstacles.
+#pragma unroll 1
+    for (int r = 0; r < nslots; ++r) {
+      const Slot S = slot(r, lane, sl);
+      if (S.valid) {
         double xd = 0.0, yd = 0.0;
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
-          const double pd = sPd[i * npad + k];
+          const double pd = sPd[i * npad + S.k];
           const double2 c = cxy[i];
           xd = fma(pd, c.x, xd);
           yd = fma(pd, c.y, yd);
         }
-        ws.th[k] = atan2(yd, xd);
+        const double p = atan2(yd, xd);
+        if (S.leader) {
+          ws.th[S.k] = p;
+          ws.xd[S.k] = xd;
+          ws.yd[S.k] = yd;
+        }
       }
     }
     __syncwarp();
-#pragma unroll
-    for (int r = 0; r < NKM; ++r) {
-      const int k = lane + 32 * r;
-      if (r < nk && k < n && k > 0) {
-        const double dd = ws.th[k] - ws.th[k - 1];
+    bool wrap = false;
+#pragma unroll 1
+    for (int r = 0; r < nslots; ++r) {
+      const Slot S = slot(r, lane, sl);
+      if (S.valid && S.leader && S.k > 0) {
+        const double dd = ws.th[S.k] - ws.th[S.k - 1];
         if (!(fabs(dd) < CUDART_PI)) wrap = true;
       }
     }
@@ -288,19 +394,23 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
     }
     double pth;
     {
-      double pt[16];
+      double pt[NB];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) pt[i] = 0.0;
+      for (int i = 0; i < NB; ++i) pt[i] = 0.0;
+#pragma unroll 1
+      for (int r = 0; r < nslots; ++r) {
+        const Slot S = slot(r, lane, sl);
+        if (S.valid && S.leader) {
+          const double th = ws.th[S.k];
 #pragma unroll
-      for (int r = 0; r < NKM; ++r) {
-        const int k = lane + 32 * r;
-        if (r < nk && k < n) {
-          const double th = ws.th[k];
-#pragma unroll
-          for (int i = 0; i < NB; ++i) pt[i] = fma(sP[i * npad + k], th, pt[i]);
+          for (int i = 0; i < NB; ++i) pt[i] = fma(sP[i * npad + S.k], th, pt[i]);
         }
       }
-      pth = reduce_pairs16(pt);
+#pragma unroll
+      for (int i = 0; i < NB; ++i) ws.red[lane * kRedStride + i] = pt[i];
+      __syncwarp();
+      pth = owner ? column_sum(ws.red, li) : 0.0;  // lanes i and 16+i both get sum_k P_ki theta_k
+      __syncwarp();
     }
 
     // (3) psi QP
@@ -318,112 +428,131 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
     }
 
     // (4) fused tail + on-the-fly contractions
-    double Gx[NB], Gy[NB], Rx[NB], Ry[NB], Lp[NB];
+    double Gx[NB], Gy[NB], Rx[NB], Ry[NB];
 #pragma unroll
-    for (int i = 0; i < NB; ++i) { Gx[i] = Gy[i] = Rx[i] = Ry[i] = Lp[i] = 0.0; }
+    for (int i = 0; i < NB; ++i) { Gx[i] = Gy[i] = Rx[i] = Ry[i] = 0.0; }
     double sqo = 0.0, sqa = 0.0, sqn = 0.0;
-#pragma unroll
-    for (int r = 0; r < NKM; ++r) {
-      const int k = lane + 32 * r;
-      if (r < nk && k < n) {
-        double x = 0, y = 0, xd = 0, yd = 0, xdd = 0, ydd = 0, ps = 0;
+#pragma unroll 1
+    for (int r = 0; r < nslots; ++r) {
+      const Slot S = slot(r, lane, sl);
+      const int k = S.k;
+      double x = 0, y = 0, xdd = 0, ydd = 0, ps = 0;
+      double gsx = 0.0, gsy = 0.0, rsx = 0.0, rsy = 0.0, sq = 0.0;
+      if (S.valid) {
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
-          const double p = sP[i * npad + k], pd = sPd[i * npad + k], pdd = sPdd[i * npad + k];
+          const double p = sP[i * npad + k], pdd = sPdd[i * npad + k];
           const double2 c = cxy[i];
-          const double cpi = ws.cp[i];
           x = fma(p, c.x, x);
           y = fma(p, c.y, y);
-          xd = fma(pd, c.x, xd);
-          yd = fma(pd, c.y, yd);
           xdd = fma(pdd, c.x, xdd);
           ydd = fma(pdd, c.y, ydd);
-          ps = fma(p, cpi, ps);
+          ps = fma(p, ws.cp[i], ps);
         }
-        // obstacle block (_speedups.pyx:150-176), summed over obstacles
-        double gsx = 0.0, gsy = 0.0, rsx = 0.0, rsy = 0.0, sq = 0.0;
-#pragma unroll 2
-        for (int j = 0; j < m; ++j) {
-          const double2 q = __ldg(xi + j * n + k);
-          const double wx = x - q.x, wy = y - q.y;
-          const double px = b * wx, py = a * wy;
-          const double r2 = fma(px, px, py * py);
-          const double ri = rsqrt(r2);
-          const bool pos = r2 > 0.0;
-          const double ca = pos ? px * ri : 1.0;
-          const double sa = pos ? py * ri : 0.0;
-          const double rr = pos ? r2 * ri : 0.0;
-          const double dd = fmax(1.0, rr * inv_ab);
-          const double adca = (a * dd) * ca, bdsa = (b * dd) * sa;
-          const double rx = wx - adca, ry = wy - bdsa;
-          sq = fma(rx, rx, fma(ry, ry, sq));
-          gsx += q.x + adca;
-          gsy += q.y + bdsa;
-          rsx += rx;
-          rsy += ry;
+        // obstacle block (_speedups.pyx:150-176), summed over this lane's obstacles
+        const double2* qp = xi + S.j0 * n + k;
+        const int qstep = S.js * n;
+        int j = S.j0;
+        // two independent obstacle terms per trip so their latency chains interleave
+        for (; j + S.js < m; j += 2 * S.js, qp += 2 * qstep) {
+          const double2 q0 = __ldg(qp), q1 = __ldg(qp + qstep);
+          obstacle_term(x, y, q0, a, b, inv_ab, gsx, gsy, rsx, rsy, sq);
+          obstacle_term(x, y, q1, a, b, inv_ab, gsx, gsy, rsx, rsy, sq);
         }
-        sqo += sq;
-        // acceleration block (_speedups.pyx:179-198)
-        const double m2 = fma(xdd, xdd, ydd * ydd);
-        const double mi = rsqrt(m2);
-        const bool mpos = m2 > 0.0;
-        const double caa = mpos ? xdd * mi : 1.0, saa = mpos ? ydd * mi : 0.0;
-        const double mag = mpos ? m2 * mi : 0.0;
-        const double da = fmin(mag, A.a_max);
-        const double gax = da * caa, gay = da * saa;
-        const double rax = xdd - gax, ray = ydd - gay;
-        sqa = fma(rax, rax, fma(ray, ray, sqa));
-        // non-holonomic block (_speedups.pyx:200-216)
-        double s = sqrt(fma(xd, xd, yd * yd));
-        s = fmin(fmax(s, A.v_min), A.v_max);
-        double sp, cpv;
-        sincos(ps, &sp, &cpv);
-        const double gnx = s * cpv, gny = s * sp;
-        const double rnx = xd - gnx, rny = yd - gny;
-        sqn = fma(rnx, rnx, fma(rny, rny, sqn));
-        if (last && (A.flags & BMPC_F_V)) A.v_out[(size_t)k * L + inst] = s;
-        const double dpt = ps - ws.th[k];
+        if (j < m) obstacle_term(x, y, __ldg(qp), a, b, inv_ab, gsx, gsy, rsx, rsy, sq);
+      }
+      if (r == sl.F && sl.g > 1) {  // split slot (warp-uniform): combine the group's partials
+        for (int o = 1; o < sl.g; o <<= 1) {
+          gsx += __shfl_xor_sync(BMPC_FULL, gsx, o);
+          gsy += __shfl_xor_sync(BMPC_FULL, gsy, o);
+          rsx += __shfl_xor_sync(BMPC_FULL, rsx, o);
+          rsy += __shfl_xor_sync(BMPC_FULL, rsy, o);
+          sq += __shfl_xor_sync(BMPC_FULL, sq, o);
+        }
+      }
+      if (S.valid) {
+        const double xd = ws.xd[k], yd = ws.yd[k];
+        if (S.leader) {
+          sqo += sq;
+          // acceleration block (_speedups.pyx:179-198)
+          const double m2 = fma(xdd, xdd, ydd * ydd);
+          const double mi = rsqrt_nb(m2);
+          const double caa = m2 > 0.0 ? xdd * mi : 1.0, saa = ydd * mi;
+          const double mag = m2 * mi;
+          const double da = mag < A.a_max ? mag : A.a_max;
+          const double gax = da * caa, gay = da * saa;
+          const double rax = xdd - gax, ray = ydd - gay;
+          sqa = fma(rax, rax, fma(ray, ray, sqa));
+          // non-holonomic block (_speedups.pyx:200-216)
+          const double s2 = fma(xd, xd, yd * yd);
+          double s = s2 * rsqrt_nb(s2);
+          s = s < A.v_min ? A.v_min : (s > A.v_max ? A.v_max : s);
+          double sp, cpv;
+          sincos(ps, &sp, &cpv);
+          const double gnx = s * cpv, gny = s * sp;
+          const double rnx = xd - gnx, rny = yd - gny;
+          sqn = fma(rnx, rnx, fma(rny, rny, sqn));
+          if (last && (A.flags & BMPC_F_V)) A.v_out[(size_t)k * L + inst] = s;
+          ws.th[k] = ps - ws.th[k];  // psi - theta, contracted below (solver.py:494)
 #pragma unroll
-        for (int i = 0; i < NB; ++i) {
-          const double p = sP[i * npad + k], pd = sPd[i * npad + k], pdd = sPdd[i * npad + k];
-          Gx[i] = fma(p, gsx, Gx[i]);
-          Gx[i] = fma(pdd, gax, Gx[i]);
-          Gx[i] = fma(pd, gnx, Gx[i]);
-          Gy[i] = fma(p, gsy, Gy[i]);
-          Gy[i] = fma(pdd, gay, Gy[i]);
-          Gy[i] = fma(pd, gny, Gy[i]);
-          Rx[i] = fma(p, rsx, Rx[i]);
-          Rx[i] = fma(pdd, rax, Rx[i]);
-          Rx[i] = fma(pd, rnx, Rx[i]);
-          Ry[i] = fma(p, rsy, Ry[i]);
-          Ry[i] = fma(pdd, ray, Ry[i]);
-          Ry[i] = fma(pd, rny, Ry[i]);
-          Lp[i] = fma(p, dpt, Lp[i]);
+          for (int i = 0; i < NB; ++i) {
+            const double p = sP[i * npad + k], pd = sPd[i * npad + k], pdd = sPdd[i * npad + k];
+            Gx[i] = fma(p, gsx, Gx[i]);
+            Gx[i] = fma(pdd, gax, Gx[i]);
+            Gx[i] = fma(pd, gnx, Gx[i]);
+            Gy[i] = fma(p, gsy, Gy[i]);
+            Gy[i] = fma(pdd, gay, Gy[i]);
+            Gy[i] = fma(pd, gny, Gy[i]);
+            Rx[i] = fma(p, rsx, Rx[i]);
+            Rx[i] = fma(pdd, rax, Rx[i]);
+            Rx[i] = fma(pd, rnx, Rx[i]);
+            Ry[i] = fma(p, rsy, Ry[i]);
+            Ry[i] = fma(pdd, ray, Ry[i]);
+            Ry[i] = fma(pd, rny, Ry[i]);
+          }
         }
       }
     }
-    // warp contractions -> owner lanes
-    double v32[32];
+    // warp contractions over the samples -> owner lanes (shared-memory transpose,
+    // fixed summation order)
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      v32[i] = i < NB ? Gx[i] : 0.0;
-      v32[16 + i] = i < NB ? Gy[i] : 0.0;
+    for (int i = 0; i < NB; ++i) {
+      ws.red[lane * kRedStride + i] = Gx[i];
+      ws.red[lane * kRedStride + 16 + i] = Gy[i];
     }
-    G = reduce_scatter32(v32);
+    __syncwarp();
+    G = owner ? column_sum(ws.red, lane) : 0.0;
+    __syncwarp();
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      v32[i] = i < NB ? Rx[i] : 0.0;
-      v32[16 + i] = i < NB ? Ry[i] : 0.0;
+    for (int i = 0; i < NB; ++i) {
+      ws.red[lane * kRedStride + i] = Rx[i];
+      ws.red[lane * kRedStride + 16 + i] = Ry[i];
     }
-    const double R = reduce_scatter32(v32);
+    __syncwarp();
+    const double R = owner ? column_sum(ws.red, lane) : 0.0;
+    __syncwarp();
+    {
+      double Lp[NB];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v32[i] = i < NB ? Lp[i] : 0.0;
-    v32[16] = sqo;
-    v32[17] = sqa;
-    v32[18] = sqn;
+      for (int i = 0; i < NB; ++i) Lp[i] = 0.0;
+#pragma unroll 1
+      for (int r = 0; r < nslots; ++r) {
+        const Slot S = slot(r, lane, sl);
+        if (S.valid && S.leader) {
+          const double dpt = ws.th[S.k];
 #pragma unroll
-    for (int i = 19; i < 32; ++i) v32[i] = 0.0;
-    const double q3 = reduce_scatter32(v32);
+          for (int i = 0; i < NB; ++i) Lp[i] = fma(sP[i * npad + S.k], dpt, Lp[i]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < NB; ++i) ws.red[lane * kRedStride + i] = Lp[i];
+    }
+    ws.red[lane * kRedStride + 16] = sqo;
+    ws.red[lane * kRedStride + 17] = sqa;
+    ws.red[lane * kRedStride + 18] = sqn;
+    __syncwarp();
+    const double q3 = ((!yax && owner) || (lane >= 16 && lane < 19)) ? column_sum(ws.red, lane) : 0.0;
+    __syncwarp();
     if (owner) lam -= rho * R;
     if (!yax && owner) lamp -= rho * q3;
     if (lane >= 16 && lane < 19) {

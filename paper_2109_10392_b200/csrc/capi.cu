@@ -114,7 +114,7 @@ int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pd
     if (!isfinite(kinv_axis[i])) return fail(BMPC_ESINGULAR, "KKT xy inverse is not finite");
   for (int i = 0; i < rp * rp; ++i)
     if (!isfinite(kinv_psi[i])) return fail(BMPC_ESINGULAR, "KKT psi inverse is not finite");
-  const int npad = ((n + 31) / 32) * 32;
+  const int npad = n <= 64 ? 64 : (n <= 128 ? 128 : 256);  // = 32 * NKM of the kernel
   const int kxs = rx | 1, kps = rp | 1;
   const size_t nPT = (size_t)3 * nb * npad, nKx = (size_t)rx * kxs, nKp = (size_t)rp * kps;
   std::vector<double> h(nPT + 2 * nKx + 2 * nKp + npad, 0.0);
@@ -141,6 +141,13 @@ int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pd
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, dev);
+  // Per-call workspaces come from the stream-ordered pool; keep freed blocks
+  // cached instead of trimming them back to the OS at every synchronisation.
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    unsigned long long keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
   c->C.n = n;
   c->C.npad = npad;
   c->C.nb = nb;
