@@ -12,6 +12,7 @@ typedef struct {
   int npad;       // n rounded up to a multiple of 32
   int nb;         // Bernstein coefficients per axis (degree + 1)
   int kxs, kps;   // padded (odd) row strides of the (nb+6)^2 and (nb+4)^2 KKT blocks
+  int kms;        // padded (odd) row stride of M
   double rho;
   const double* PT;   // [3][nb][npad]: P^T, Pdot^T, Pddot^T, zero padded past n
   const double* tau;  // [npad] (t_k - t0)/(tf - t0), cold-start line parameter
@@ -19,6 +20,7 @@ typedef struct {
   const double* Kxa;  // [nb+6][kxs] the per-axis KKT matrix (refinement residual)
   const double* Kpf;  // [nb+4][kps] inverse of the heading KKT matrix
   const double* Kpa;  // [nb+4][kps] the heading KKT matrix
+  const double* M;    // [nb][kms]   F_axis^T F_axis (multiplier step identity)
 } bmpc_dev_consts;
 
 enum { BMPC_INIT_COLD = 0, BMPC_INIT_WARM = 1, BMPC_INIT_RESUME = 2 };

@@ -67,7 +67,7 @@ __device__ __forceinline__ double column_sum(const double* __restrict__ red, int
 // so the last round is not 32-R idle lanes deep.  Only the group leader owns
 // the per-sample terms.
 struct SlotLayout {
-  int F, R, g;  // g == 1: no split
+  int F, R, g, lg;  // g = 2^lg lanes per leftover sample; g == 1: no split
 };
 struct Slot {
   int k, j0, js;
@@ -78,10 +78,12 @@ __device__ __forceinline__ SlotLayout slot_layout(int n) {
   s.F = n >> 5;
   s.R = n & 31;
   s.g = 1;
+  s.lg = 0;
   if (s.R > 0 && s.R <= 16) {
     int g = 32 / s.R;
     while (g & (g - 1)) g &= g - 1;
     s.g = g;
+    s.lg = __ffs(g) - 1;
   }
   return s;
 }
@@ -94,9 +96,9 @@ __device__ __forceinline__ Slot slot(int r, int lane, const SlotLayout& sl) {
     S.valid = true;
     S.leader = true;
   } else if (r == sl.F && sl.R > 0) {
-    const int grp = lane / sl.g;
+    const int grp = lane >> sl.lg;
     S.k = 32 * sl.F + grp;
-    S.j0 = lane - grp * sl.g;
+    S.j0 = lane & (sl.g - 1);
     S.js = sl.g;
     S.valid = grp < sl.R;
     S.leader = S.j0 == 0;
@@ -117,10 +119,12 @@ __device__ __forceinline__ Slot slot(int r, int lane, const SlotLayout& sl) {
 template <int LEN>
 __device__ __forceinline__ double kkt_row_dot(const double* __restrict__ kr,
                                               const double* __restrict__ v) {
-  double s = 0.0;
+  // four interleaved partial sums: the QP steps sit on the critical path of
+  // every sweep, so their latency matters more than their (tiny) flop count
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-  for (int j = 0; j < LEN; ++j) s = fma(kr[j], v[j], s);
-  return s;
+  for (int j = 0; j < LEN; ++j) s[j & 3] = fma(kr[j], v[j], s[j & 3]);
+  return (s[0] + s[1]) + (s[2] + s[3]);
 }
 
 // Obstacle block of the fused tail for one (obstacle, sample) element
@@ -129,7 +133,7 @@ __device__ __forceinline__ double kkt_row_dot(const double* __restrict__ kr,
 // sqrt and the three divisions (SURVEY.md finding 8).
 __device__ __forceinline__ void obstacle_term(double x, double y, double2 q, double a, double b,
                                               double inv_ab, double& gsx, double& gsy,
-                                              double& rsx, double& rsy, double& sq) {
+                                              double& sq) {
   const double wx = x - q.x, wy = y - q.y;
   const double px = b * wx, py = a * wy;
   const double r2 = fma(px, px, py * py);
@@ -144,8 +148,131 @@ __device__ __forceinline__ void obstacle_term(double x, double y, double2 q, dou
   sq = fma(rx, rx, fma(ry, ry, sq));
   gsx += q.x + adca;
   gsy += q.y + bdsa;
-  rsx += rx;
-  rsy += ry;
+}
+
+// Two sample slots per pass when the accumulators leave register room.
+template <int NB>
+constexpr bool kPairSlots = NB <= 12;
+
+struct TailArgs {
+  const double *P, *Pd, *Pdd;
+  const double2* cxy;
+  const double* cp;
+  const double2* xi;
+  double *th, *xd, *yd;
+  int n, m;
+  double a, b, inv_ab, a_max, v_min, v_max;
+  double* v_out;
+  size_t L;
+  int inst;
+};
+
+// Fused tail (kernels/_speedups.pyx:114-218) for NS samples of one lane, with
+// the contractions onto the basis accumulated on the fly.  Obstacles j0, j0+js,
+// ...; `group` > 1 marks a split slot whose obstacle partials are summed over
+// `group` consecutive lanes (warp-uniform).  Accumulation order per sample
+// and across samples is the order of the sample list.
+template <int NS, int NB, int NPAD>
+__device__ __forceinline__ void tail_block(const TailArgs& T, const int (&k)[NS], int j0, int js,
+                                           int group, bool valid, bool leader, double (&Gx)[NB],
+                                           double (&Gy)[NB], double& sqo, double& sqa,
+                                           double& sqn) {
+  double x[NS], y[NS], xdd[NS], ydd[NS], ps[NS], gsx[NS], gsy[NS], sq[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) x[s] = y[s] = xdd[s] = ydd[s] = ps[s] = gsx[s] = gsy[s] = sq[s] = 0.0;
+  if (valid) {
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      const double2 c = T.cxy[i];
+      const double cpi = T.cp[i];
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const double p = T.P[i * NPAD + k[s]], pdd = T.Pdd[i * NPAD + k[s]];
+        x[s] = fma(p, c.x, x[s]);
+        y[s] = fma(p, c.y, y[s]);
+        xdd[s] = fma(pdd, c.x, xdd[s]);
+        ydd[s] = fma(pdd, c.y, ydd[s]);
+        ps[s] = fma(p, cpi, ps[s]);
+      }
+    }
+    // obstacle block (_speedups.pyx:150-176), summed over this lane's obstacles
+    const int qstep = js * T.n;
+    constexpr int U = NS == 1 ? 4 : 2;  // independent terms in flight per sample
+    const double2* qp[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) qp[s] = T.xi + j0 * T.n + k[s];
+    int j = j0;
+    for (; j + (U - 1) * js < T.m; j += U * js) {
+      double2 q[NS][U];
+#pragma unroll
+      for (int s = 0; s < NS; ++s)
+#pragma unroll
+        for (int u = 0; u < U; ++u) q[s][u] = __ldg(qp[s] + u * qstep);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+          obstacle_term(x[s], y[s], q[s][u], T.a, T.b, T.inv_ab, gsx[s], gsy[s], sq[s]);
+#pragma unroll
+      for (int s = 0; s < NS; ++s) qp[s] += U * qstep;
+    }
+    for (; j < T.m; j += js) {
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        obstacle_term(x[s], y[s], __ldg(qp[s]), T.a, T.b, T.inv_ab, gsx[s], gsy[s], sq[s]);
+        qp[s] += qstep;
+      }
+    }
+  }
+  if (NS == 1 && group > 1) {  // split slot: combine the group's partial sums
+    for (int o = 1; o < group; o <<= 1) {
+      gsx[0] += __shfl_xor_sync(BMPC_FULL, gsx[0], o);
+      gsy[0] += __shfl_xor_sync(BMPC_FULL, gsy[0], o);
+      sq[0] += __shfl_xor_sync(BMPC_FULL, sq[0], o);
+    }
+  }
+  if (!(valid && leader)) return;
+  double gax[NS], gay[NS], gnx[NS], gny[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    sqo += sq[s];
+    // acceleration block (_speedups.pyx:179-198)
+    const double m2 = fma(xdd[s], xdd[s], ydd[s] * ydd[s]);
+    const double mi = rsqrt_nb(m2);
+    const double caa = m2 > 0.0 ? xdd[s] * mi : 1.0, saa = ydd[s] * mi;
+    const double mag = m2 * mi;
+    const double da = mag < T.a_max ? mag : T.a_max;
+    gax[s] = da * caa;
+    gay[s] = da * saa;
+    const double rax = xdd[s] - gax[s], ray = ydd[s] - gay[s];
+    sqa = fma(rax, rax, fma(ray, ray, sqa));
+    // non-holonomic block (_speedups.pyx:200-216)
+    const double xd = T.xd[k[s]], yd = T.yd[k[s]];
+    const double s2 = fma(xd, xd, yd * yd);
+    double v = s2 * rsqrt_nb(s2);
+    v = v < T.v_min ? T.v_min : (v > T.v_max ? T.v_max : v);
+    double sp, cpv;
+    sincos(ps[s], &sp, &cpv);
+    gnx[s] = v * cpv;
+    gny[s] = v * sp;
+    const double rnx = xd - gnx[s], rny = yd - gny[s];
+    sqn = fma(rnx, rnx, fma(rny, rny, sqn));
+    if (T.v_out) T.v_out[(size_t)k[s] * T.L + T.inst] = v;
+    T.th[k[s]] = ps[s] - T.th[k[s]];  // psi - theta, contracted later (solver.py:494)
+  }
+#pragma unroll
+  for (int i = 0; i < NB; ++i) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const double p = T.P[i * NPAD + k[s]], pd = T.Pd[i * NPAD + k[s]], pdd = T.Pdd[i * NPAD + k[s]];
+      Gx[i] = fma(p, gsx[s], Gx[i]);
+      Gx[i] = fma(pdd, gax[s], Gx[i]);
+      Gx[i] = fma(pd, gnx[s], Gx[i]);
+      Gy[i] = fma(p, gsy[s], Gy[i]);
+      Gy[i] = fma(pdd, gay[s], Gy[i]);
+      Gy[i] = fma(pd, gny[s], Gy[i]);
+    }
+  }
 }
 
 template <int NB, int NKM>
@@ -166,7 +293,8 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
   double* sKxa = sKxf + RX * C.kxs;
   double* sKpf = sKxa + RX * C.kxs;
   double* sKpa = sKpf + RP * C.kps;
-  double* sTau = sKpa + RP * C.kps;
+  double* sM = sKpa + RP * C.kps;   // F_axis^T F_axis (lambda identity)
+  double* sTau = sM + ((NB * C.kms + 1) & ~1);  // keep the double2 scratch 16-byte aligned
   double* wbase = sTau + npad + warp * (kWarpScratch + 3 * npad + kRedSize);
   WarpScratch ws{wbase,       wbase + 64,   wbase + 128,
                  wbase + 192, wbase + 224,  wbase + kWarpScratch,
@@ -184,6 +312,7 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
     sKpf[t] = C.Kpf[t];
     sKpa[t] = C.Kpa[t];
   }
+  for (int t = threadIdx.x; t < NB * C.kms; t += blockDim.x) sM[t] = C.M[t];
   for (int t = threadIdx.x; t < npad; t += blockDim.x) sTau[t] = C.tau[t];
   __syncthreads();
 
@@ -428,90 +557,29 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
     }
 
     // (4) fused tail + on-the-fly contractions
-    double Gx[NB], Gy[NB], Rx[NB], Ry[NB];
+    double Gx[NB], Gy[NB];
 #pragma unroll
-    for (int i = 0; i < NB; ++i) { Gx[i] = Gy[i] = Rx[i] = Ry[i] = 0.0; }
+    for (int i = 0; i < NB; ++i) { Gx[i] = Gy[i] = 0.0; }
     double sqo = 0.0, sqa = 0.0, sqn = 0.0;
+    TailArgs T{sP, sPd, sPdd, cxy, ws.cp, xi, ws.th, ws.xd, ws.yd, n, m, a, b, inv_ab,
+               A.a_max, A.v_min, A.v_max, (last && (A.flags & BMPC_F_V)) ? A.v_out : nullptr,
+               (size_t)L, inst};
+    int r = 0;
+    if (kPairSlots<NB>) {
+      // two full sample slots per pass: twice the independent work in flight,
+      // same accumulation order as one slot at a time
 #pragma unroll 1
-    for (int r = 0; r < nslots; ++r) {
+      for (; r + 1 < sl.F; r += 2) {
+        const int ks[2] = {lane + 32 * r, lane + 32 * (r + 1)};
+        tail_block<2, NB, npad>(T, ks, 0, 1, 0, true, true, Gx, Gy, sqo, sqa, sqn);
+      }
+    }
+#pragma unroll 1
+    for (; r < nslots; ++r) {
       const Slot S = slot(r, lane, sl);
-      const int k = S.k;
-      double x = 0, y = 0, xdd = 0, ydd = 0, ps = 0;
-      double gsx = 0.0, gsy = 0.0, rsx = 0.0, rsy = 0.0, sq = 0.0;
-      if (S.valid) {
-#pragma unroll
-        for (int i = 0; i < NB; ++i) {
-          const double p = sP[i * npad + k], pdd = sPdd[i * npad + k];
-          const double2 c = cxy[i];
-          x = fma(p, c.x, x);
-          y = fma(p, c.y, y);
-          xdd = fma(pdd, c.x, xdd);
-          ydd = fma(pdd, c.y, ydd);
-          ps = fma(p, ws.cp[i], ps);
-        }
-        // obstacle block (_speedups.pyx:150-176), summed over this lane's obstacles
-        const double2* qp = xi + S.j0 * n + k;
-        const int qstep = S.js * n;
-        int j = S.j0;
-        // two independent obstacle terms per trip so their latency chains interleave
-        for (; j + S.js < m; j += 2 * S.js, qp += 2 * qstep) {
-          const double2 q0 = __ldg(qp), q1 = __ldg(qp + qstep);
-          obstacle_term(x, y, q0, a, b, inv_ab, gsx, gsy, rsx, rsy, sq);
-          obstacle_term(x, y, q1, a, b, inv_ab, gsx, gsy, rsx, rsy, sq);
-        }
-        if (j < m) obstacle_term(x, y, __ldg(qp), a, b, inv_ab, gsx, gsy, rsx, rsy, sq);
-      }
-      if (r == sl.F && sl.g > 1) {  // split slot (warp-uniform): combine the group's partials
-        for (int o = 1; o < sl.g; o <<= 1) {
-          gsx += __shfl_xor_sync(BMPC_FULL, gsx, o);
-          gsy += __shfl_xor_sync(BMPC_FULL, gsy, o);
-          rsx += __shfl_xor_sync(BMPC_FULL, rsx, o);
-          rsy += __shfl_xor_sync(BMPC_FULL, rsy, o);
-          sq += __shfl_xor_sync(BMPC_FULL, sq, o);
-        }
-      }
-      if (S.valid) {
-        const double xd = ws.xd[k], yd = ws.yd[k];
-        if (S.leader) {
-          sqo += sq;
-          // acceleration block (_speedups.pyx:179-198)
-          const double m2 = fma(xdd, xdd, ydd * ydd);
-          const double mi = rsqrt_nb(m2);
-          const double caa = m2 > 0.0 ? xdd * mi : 1.0, saa = ydd * mi;
-          const double mag = m2 * mi;
-          const double da = mag < A.a_max ? mag : A.a_max;
-          const double gax = da * caa, gay = da * saa;
-          const double rax = xdd - gax, ray = ydd - gay;
-          sqa = fma(rax, rax, fma(ray, ray, sqa));
-          // non-holonomic block (_speedups.pyx:200-216)
-          const double s2 = fma(xd, xd, yd * yd);
-          double s = s2 * rsqrt_nb(s2);
-          s = s < A.v_min ? A.v_min : (s > A.v_max ? A.v_max : s);
-          double sp, cpv;
-          sincos(ps, &sp, &cpv);
-          const double gnx = s * cpv, gny = s * sp;
-          const double rnx = xd - gnx, rny = yd - gny;
-          sqn = fma(rnx, rnx, fma(rny, rny, sqn));
-          if (last && (A.flags & BMPC_F_V)) A.v_out[(size_t)k * L + inst] = s;
-          ws.th[k] = ps - ws.th[k];  // psi - theta, contracted below (solver.py:494)
-#pragma unroll
-          for (int i = 0; i < NB; ++i) {
-            const double p = sP[i * npad + k], pd = sPd[i * npad + k], pdd = sPdd[i * npad + k];
-            Gx[i] = fma(p, gsx, Gx[i]);
-            Gx[i] = fma(pdd, gax, Gx[i]);
-            Gx[i] = fma(pd, gnx, Gx[i]);
-            Gy[i] = fma(p, gsy, Gy[i]);
-            Gy[i] = fma(pdd, gay, Gy[i]);
-            Gy[i] = fma(pd, gny, Gy[i]);
-            Rx[i] = fma(p, rsx, Rx[i]);
-            Rx[i] = fma(pdd, rax, Rx[i]);
-            Rx[i] = fma(pd, rnx, Rx[i]);
-            Ry[i] = fma(p, rsy, Ry[i]);
-            Ry[i] = fma(pdd, ray, Ry[i]);
-            Ry[i] = fma(pd, rny, Ry[i]);
-          }
-        }
-      }
+      const int ks[1] = {S.k};
+      tail_block<1, NB, npad>(T, ks, S.j0, S.js, (r == sl.F) ? sl.g : 1, S.valid, S.leader, Gx, Gy,
+                              sqo, sqa, sqn);
     }
     // warp contractions over the samples -> owner lanes (shared-memory transpose,
     // fixed summation order)
@@ -523,14 +591,16 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
     __syncwarp();
     G = owner ? column_sum(ws.red, lane) : 0.0;
     __syncwarp();
+    // lambda step F_axis^T r = F_axis^T (F_axis c - g) = (F_axis^T F_axis) c - G:
+    // the residual vectors never need their own contraction
+    double R = 0.0;
+    if (owner) {
+      const double* mr = sM + li * C.kms;
+      double s4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int i = 0; i < NB; ++i) {
-      ws.red[lane * kRedStride + i] = Rx[i];
-      ws.red[lane * kRedStride + 16 + i] = Ry[i];
+      for (int j = 0; j < NB; ++j) s4[j & 3] = fma(mr[j], ws.cxy[2 * j + (yax ? 1 : 0)], s4[j & 3]);
+      R = ((s4[0] + s4[1]) + (s4[2] + s4[3])) - G;
     }
-    __syncwarp();
-    const double R = owner ? column_sum(ws.red, lane) : 0.0;
-    __syncwarp();
     {
       double Lp[NB];
 #pragma unroll

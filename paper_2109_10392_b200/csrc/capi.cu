@@ -103,8 +103,9 @@ int bmpc_abi_version(void) { return 1; }
 int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pdot,
                     const double* Pddot, const double* tau, const double* kinv_axis,
                     const double* k_axis, const double* kinv_psi, const double* k_psi,
-                    bmpc_ctx** out) {
-  if (!out || !P || !Pdot || !Pddot || !tau || !kinv_axis || !k_axis || !kinv_psi || !k_psi)
+                    const double* ftf_axis, bmpc_ctx** out) {
+  if (!out || !P || !Pdot || !Pddot || !tau || !kinv_axis || !k_axis || !kinv_psi || !k_psi ||
+      !ftf_axis)
     return fail(BMPC_EINVAL, "bmpc_ctx_create: null argument");
   if (nb < 4 || nb > 16) return fail(BMPC_EINVAL, "bmpc_ctx_create: need 4 <= n_b <= 16");
   if (n < 2 || n > 256) return fail(BMPC_EINVAL, "bmpc_ctx_create: need 2 <= n <= 256");
@@ -115,18 +116,18 @@ int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pd
   for (int i = 0; i < rp * rp; ++i)
     if (!isfinite(kinv_psi[i])) return fail(BMPC_ESINGULAR, "KKT psi inverse is not finite");
   const int npad = n <= 64 ? 64 : (n <= 128 ? 128 : 256);  // = 32 * NKM of the kernel
-  const int kxs = rx | 1, kps = rp | 1;
+  const int kxs = rx | 1, kps = rp | 1, kms = nb | 1;
   const size_t nPT = (size_t)3 * nb * npad, nKx = (size_t)rx * kxs, nKp = (size_t)rp * kps;
-  std::vector<double> h(nPT + 2 * nKx + 2 * nKp + npad, 0.0);
+  std::vector<double> h(nPT + 2 * nKx + 2 * nKp + (size_t)nb * kms + npad, 0.0);
   const double* mats[3] = {P, Pdot, Pddot};
   for (int q = 0; q < 3; ++q)
     for (int i = 0; i < nb; ++i)
       for (int k = 0; k < n; ++k) h[((size_t)q * nb + i) * npad + k] = mats[q][(size_t)k * nb + i];
   size_t o = nPT;
-  const double* blocks[4] = {kinv_axis, k_axis, kinv_psi, k_psi};
-  const int dims[4] = {rx, rx, rp, rp}, strides[4] = {kxs, kxs, kps, kps};
-  size_t offs[4];
-  for (int q = 0; q < 4; ++q) {
+  const double* blocks[5] = {kinv_axis, k_axis, kinv_psi, k_psi, ftf_axis};
+  const int dims[5] = {rx, rx, rp, rp, nb}, strides[5] = {kxs, kxs, kps, kps, kms};
+  size_t offs[5];
+  for (int q = 0; q < 5; ++q) {
     offs[q] = o;
     for (int i = 0; i < dims[q]; ++i)
       for (int j = 0; j < dims[q]; ++j) h[o + (size_t)i * strides[q] + j] = blocks[q][(size_t)i * dims[q] + j];
@@ -153,12 +154,14 @@ int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pd
   c->C.nb = nb;
   c->C.kxs = kxs;
   c->C.kps = kps;
+  c->C.kms = kms;
   c->C.rho = rho;
   c->C.PT = c->dmem;
   c->C.Kxf = c->dmem + offs[0];
   c->C.Kxa = c->dmem + offs[1];
   c->C.Kpf = c->dmem + offs[2];
   c->C.Kpa = c->dmem + offs[3];
+  c->C.M = c->dmem + offs[4];
   c->C.tau = c->dmem + o;
   *out = c;
   return BMPC_OK;

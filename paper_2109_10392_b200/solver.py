@@ -168,6 +168,7 @@ class KktSystem:
         ra = mats.A_axis.shape[0]
         axis = np.r_[0:nb, 2 * nb:2 * nb + ra]
         self.matrix_axis = K[np.ix_(axis, axis)]
+        self.ftf_axis = mats.F_axis.T @ mats.F_axis
         self.inv_xy = self._invert(K)
         self.inv_axis = self._invert_quiet(self.matrix_axis)
         self.inv_psi = self._invert(Kp)
@@ -234,7 +235,7 @@ class BatchSolver:
         b = self.basis
         arrs = [np.ascontiguousarray(a, dtype=np.float64)
                 for a in (b.P, b.Pdot, b.Pddot, self._tau, self.kkt.inv_axis, self.kkt.matrix_axis,
-                          self.kkt.inv_psi, self.kkt.matrix_psi)]
+                          self.kkt.inv_psi, self.kkt.matrix_psi, self.kkt.ftf_axis)]
         nat.check(lib.bmpc_ctx_create(b.grid.n, b.n_b, float(self.rho_xy),
                                       *[nat.c_double_ptr(a) for a in arrs], ctypes.byref(c)),
                   "bmpc_ctx_create")
