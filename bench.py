@@ -292,12 +292,12 @@ def run_ours(args, rank, world, local_rank):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         procs = os.cpu_count() or 1
-        rate, secs, used = cpu_oracle_rate(args.config if cfg.scenes == 1 else "c1",
-                                           cfg.l if cfg.scenes == 1 else 1024, iters, procs)
+        goals = min(cfg.l, 1024)  # bounded sample: scene 0, at most 1024 goals of this config
+        rate, secs, used = cpu_oracle_rate(args.config, goals, iters, procs)
         cpu = {"value": rate, "unit": "problems/s", "cores": used, "kind": "port",
-               "sample": f"{args.config} scene 0, {cfg.l if cfg.scenes == 1 else 1024} goals x {iters} "
-                         f"sweeps + scoring, split over {used} processes (1 BLAS thread each), "
-                         f"{secs:.2f}s wall; oracle/am_oracle.py + am_oracle.c"}
+               "sample": f"{args.config} scene 0, {goals} goals x {iters} sweeps + scoring, split "
+                         f"over {used} processes (1 BLAS thread each), {secs:.2f}s wall; "
+                         f"oracle/am_oracle.py + am_oracle.c"}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "problems/s", "n_gpus": world,
@@ -331,13 +331,13 @@ def run_reference(args, rank, world):
 
     cfg = CONFIGS[args.config]
     iters = args.iters or cfg.iters
-    goals = cfg.l if cfg.scenes == 1 else 1024
+    goals = min(cfg.l, 1024)  # bounded sample of the workload per step: scene 0
     procs = os.cpu_count() or 1
     times = []
     import multiprocessing as mp
 
     per = int(math.ceil(goals / procs))
-    cfg_name = args.config if cfg.scenes == 1 else "c1"
+    cfg_name = args.config
     jobs = [(cfg_name, i * per, min(goals, (i + 1) * per), iters, goals) for i in range(procs)
             if i * per < goals]
     with mp.get_context("spawn").Pool(len(jobs)) as pool:

@@ -27,6 +27,7 @@ cudaError_t BMPC_CAT(launch_am_nb_, BMPC_INST_NB)(const bmpc_dev_consts& C,
   switch (C.npad) {  // the host pads n to 64, 128 or 256 samples
     case 64: return launch_t<BMPC_INST_NB, 2>(C, A, warps, st);
     case 128: return launch_t<BMPC_INST_NB, 4>(C, A, warps, st);
+    case 224: return launch_t<BMPC_INST_NB, 7>(C, A, warps, st);
     case 256: return launch_t<BMPC_INST_NB, 8>(C, A, warps, st);
     default: return cudaErrorInvalidValue;
   }

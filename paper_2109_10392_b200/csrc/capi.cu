@@ -58,6 +58,7 @@ struct bmpc_ctx {
   bmpc_dev_consts C;
   double* dmem = nullptr;  // one allocation for every constant
   int sms = 148;
+  int smem_optin = 227 * 1024;
 };
 
 static thread_local std::string g_err;
@@ -115,7 +116,8 @@ int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pd
     if (!isfinite(kinv_axis[i])) return fail(BMPC_ESINGULAR, "KKT xy inverse is not finite");
   for (int i = 0; i < rp * rp; ++i)
     if (!isfinite(kinv_psi[i])) return fail(BMPC_ESINGULAR, "KKT psi inverse is not finite");
-  const int npad = n <= 64 ? 64 : (n <= 128 ? 128 : 256);  // = 32 * NKM of the kernel
+  // = 32 * NKM of the kernel instantiations (csrc/am_inst.cu)
+  const int npad = n <= 64 ? 64 : (n <= 128 ? 128 : (n <= 224 ? 224 : 256));
   const int kxs = rx | 1, kps = rp | 1, kms = nb | 1;
   const size_t nPT = (size_t)3 * nb * npad, nKx = (size_t)rx * kxs, nKp = (size_t)rp * kps;
   std::vector<double> h(nPT + 2 * nKx + 2 * nKp + (size_t)nb * kms + npad, 0.0);
@@ -142,6 +144,7 @@ int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pd
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&c->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   // Per-call workspaces come from the stream-ordered pool; keep freed blocks
   // cached instead of trimming them back to the OS at every synchronisation.
   cudaMemPool_t pool;
@@ -195,11 +198,16 @@ static int check_problem(const bmpc_ctx* ctx, const bmpc_problem* p) {
   return BMPC_OK;
 }
 
+// Warps (= instances) per CTA: about one CTA per SM for small batches, at most
+// 8 (the register file holds 8 warps of this kernel), and never more than the
+// opt-in shared memory per block allows.
 static int auto_warps(const bmpc_ctx* ctx, int L, int req) {
-  if (req > 0) return req > 8 ? 8 : req;
-  int w = (L + ctx->sms - 1) / ctx->sms;
+  int w = req > 0 ? req : (L + ctx->sms - 1) / ctx->sms;
   if (w < 1) w = 1;
   if (w > 8) w = 8;
+  while (w > 1 && bmpc::am_solve_smem_bytes(ctx->C.nb, ctx->C.npad, ctx->C.kxs, ctx->C.kps, w) >
+                      (size_t)ctx->smem_optin)
+    --w;
   return w;
 }
 
