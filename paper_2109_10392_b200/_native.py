@@ -71,6 +71,7 @@ EXPORTS = {
     "bmpc_last_error": ([], ctypes.c_char_p),
     "bmpc_ctx_create": ([c_int, c_int, c_double] + [_dp] * 9 + [POINTER(c_void_p)], c_int),
     "bmpc_ctx_destroy": ([c_void_p], c_int),
+    "bmpc_carry_doubles": ([c_void_p], c_int),
     "bmpc_ctx_info": ([c_void_p, POINTER(c_int), POINTER(c_int), POINTER(c_int), POINTER(c_void_p)], c_int),
     "bmpc_solve": ([c_void_p, POINTER(Problem), POINTER(SolveOpts), POINTER(SolveOut), c_void_p], c_int),
     "bmpc_sweeps": ([c_void_p, POINTER(Problem), POINTER(SolveOpts), c_int, c_int, c_int, c_void_p,

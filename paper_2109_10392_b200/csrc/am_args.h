@@ -50,6 +50,13 @@ typedef struct {
   double* res_final;    // [3][L]
 } bmpc_solve_args;
 
+// Doubles of carried state per instance: lambda_x, lambda_y, lambda_psi, G_x,
+// G_y (5 nb), then the xy and psi KKT solutions [c; mu] (2 (nb+6) + nb+4).
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+static inline int carry_doubles(int nb) { return 5 * nb + 2 * (nb + 6) + (nb + 4); }
+
 // Fused scoring (sample_plan + filter_candidates + meta_cost), warp per instance.
 typedef struct {
   int n, npad, nb, m, l, L;

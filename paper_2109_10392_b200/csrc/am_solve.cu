@@ -11,7 +11,7 @@ size_t am_solve_smem_bytes(int nb, int npad, int kxs, int kps, int warps) {
   // basis, KKT inverse + matrix for both systems, tau, per-warp scratch
   return sizeof(double) *
          ((size_t)3 * nb * npad + 2 * (size_t)(nb + 6) * kxs + 2 * (size_t)(nb + 4) * kps + (size_t)((nb * (nb | 1) + 1) & ~1) + npad +
-          (size_t)warps * (256 + 3 * npad + 32 * 33));
+          (size_t)warps * (288 + 3 * npad + 32 * 33));
 }
 
 #define BMPC_DECL(NB)                                                                      \

@@ -34,16 +34,17 @@ namespace bmpc {
 
 struct WarpScratch {
   double* bc;    // 64: KKT right-hand sides (x at 0, y at 32)
-  double* sol;   // 64: first solve  Kinv * rhs
+  double* sol;   // 64: [c; mu] of the xy QP, kept across sweeps (x at 0, y at 32)
   double* res;   // 64: refinement residual rhs - K * sol
   double* cxy;   // 32: (c_x[i], c_y[i]) pairs
   double* cp;    // 16: c_psi
+  double* solp;  // 32: [c_psi; mu_psi], kept across sweeps
   double* th;    // npad: theta (unwrapped heading target) per sample
   double* xd;    // npad: xdot per sample (phase 2 -> phase 4)
   double* yd;    // npad: ydot per sample
   double* red;   // 32 x kRedStride: transpose buffer of the sample contractions
 };
-constexpr int kWarpScratch = 256;
+constexpr int kWarpScratch = 288;
 constexpr int kRedStride = 33;
 constexpr int kRedSize = 32 * kRedStride;
 
@@ -297,7 +298,7 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
   double* sTau = sM + ((NB * C.kms + 1) & ~1);  // keep the double2 scratch 16-byte aligned
   double* wbase = sTau + npad + warp * (kWarpScratch + 3 * npad + kRedSize);
   WarpScratch ws{wbase,       wbase + 64,   wbase + 128,
-                 wbase + 192, wbase + 224,  wbase + kWarpScratch,
+                 wbase + 192, wbase + 224,  wbase + 256, wbase + kWarpScratch,
                  wbase + kWarpScratch + npad, wbase + kWarpScratch + 2 * npad,
                  wbase + kWarpScratch + 3 * npad};
   const SlotLayout sl = slot_layout(n);
@@ -341,13 +342,22 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
   if (yax && li < 4) bps = A.b_psi[(size_t)li * L + inst];
 
   // ---------------------------------------------------------------- init ----
+  bool have_sol = false;  // [c; mu] of the previous sweep available for refinement
   if (A.init_mode == BMPC_INIT_RESUME) {
-    const double* cr = A.carry + (size_t)inst * 5 * NB;
+    const double* cr = A.carry + (size_t)inst * carry_doubles(NB);
     if (owner) {
       lam = cr[(yax ? 1 : 0) * NB + li];
       lamp = cr[2 * NB + li];
       G = cr[(yax ? 4 : 3) * NB + li];
     }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int q = lane + 32 * h;
+      if (q < 2 * RX) ws.sol[(q >= RX ? 32 : 0) + q - (q >= RX ? RX : 0)] = cr[5 * NB + q];
+    }
+    if (lane < RP) ws.solp[lane] = cr[5 * NB + 2 * RX + lane];
+    __syncwarp();
+    have_sol = true;
   } else {
     // Initial targets g = assemble_g(alpha, d, alpha_a, d_a, v, psi) contracted
     // to G = F_axis^T g (solver.py:431, :281-286; kernels/_speedups.pyx:81-111).
@@ -443,22 +453,27 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
   // ----------------------------------------------------------- AM sweeps ----
   for (int t = 0; t < A.iters; ++t) {
     const bool last = t == A.iters - 1;
-    // (1) xy QP: [c; mu] = K^-1 [rho*G + lambda ; b] plus one refinement step,
-    //     the 2*(nb+6) rows of both axes spread over the lanes (two per lane max)
+    // (1) xy QP: [c; mu] = K^-1 [rho*G + lambda ; b] with one refinement step,
+    //     the 2*(nb+6) rows of both axes spread over the lanes (two per lane max).
+    //     The first sweep refines the plain inverse apply; later sweeps refine
+    //     the previous sweep's [c; mu] instead -- the same accuracy
+    //     for one matrix pass less.
     {
       double* rb = ws.bc + (yax ? 32 : 0);
       if (owner) rb[li] = rho * G + lam;
       if (li < 6) rb[NB + li] = bnd;
       __syncwarp();
+      if (!have_sol) {
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int q = lane + 32 * h;
-        if (q < 2 * RX) {
-          const int ax = q >= RX ? 1 : 0, row = q - ax * RX;
-          ws.sol[ax * 32 + row] = kkt_row_dot<RX>(sKxf + row * C.kxs, ws.bc + ax * 32);
+        for (int h = 0; h < 2; ++h) {
+          const int q = lane + 32 * h;
+          if (q < 2 * RX) {
+            const int ax = q >= RX ? 1 : 0, row = q - ax * RX;
+            ws.sol[ax * 32 + row] = kkt_row_dot<RX>(sKxf + row * C.kxs, ws.bc + ax * 32);
+          }
         }
+        __syncwarp();
       }
-      __syncwarp();
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int q = lane + 32 * h;
@@ -472,11 +487,12 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int q = lane + 32 * h;
-        if (q < 2 * RX) {
+        if (q < 2 * RX) {  // each lane rewrites only its own rows of sol
           const int ax = q >= RX ? 1 : 0, row = q - ax * RX;
-          if (row < NB)
-            ws.cxy[2 * row + ax] =
-                ws.sol[ax * 32 + row] + kkt_row_dot<RX>(sKxf + row * C.kxs, ws.res + ax * 32);
+          const double s =
+              ws.sol[ax * 32 + row] + kkt_row_dot<RX>(sKxf + row * C.kxs, ws.res + ax * 32);
+          ws.sol[ax * 32 + row] = s;
+          if (row < NB) ws.cxy[2 * row + ax] = s;
         }
       }
       __syncwarp();
@@ -547,11 +563,17 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
       if (!yax && owner) ws.bc[li] = rho * pth + lamp;
       if (yax && li < 4) ws.bc[NB + li] = bps;
       __syncwarp();
-      if (lane < RP) ws.sol[lane] = kkt_row_dot<RP>(sKpf + lane * C.kps, ws.bc);
+      if (!have_sol) {
+        if (lane < RP) ws.solp[lane] = kkt_row_dot<RP>(sKpf + lane * C.kps, ws.bc);
+        __syncwarp();
+      }
+      if (lane < RP) ws.res[lane] = ws.bc[lane] - kkt_row_dot<RP>(sKpa + lane * C.kps, ws.solp);
       __syncwarp();
-      if (lane < RP) ws.res[lane] = ws.bc[lane] - kkt_row_dot<RP>(sKpa + lane * C.kps, ws.sol);
-      __syncwarp();
-      if (lane < NB) ws.cp[lane] = ws.sol[lane] + kkt_row_dot<RP>(sKpf + lane * C.kps, ws.res);
+      if (lane < RP) {
+        const double s = ws.solp[lane] + kkt_row_dot<RP>(sKpf + lane * C.kps, ws.res);
+        ws.solp[lane] = s;
+        if (lane < NB) ws.cp[lane] = s;
+      }
       __syncwarp();
       if (!yax && owner) cpown = ws.cp[li];
     }
@@ -631,6 +653,7 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
         A.hist[((size_t)(A.hist_offset + t) * 3 + (lane - 16)) * L + inst] = res;
       if (last && A.res_final) A.res_final[(size_t)(lane - 16) * L + inst] = res;
     }
+    have_sol = true;
     __syncwarp();
   }
 
@@ -647,11 +670,20 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
       if (A.l_y) A.l_y[o] = lam;
     }
     if (A.flags & BMPC_F_CARRY) {
-      double* cr = A.carry + (size_t)inst * 5 * NB;
+      double* cr = A.carry + (size_t)inst * carry_doubles(NB);
       cr[(yax ? 1 : 0) * NB + li] = lam;
       if (!yax) cr[2 * NB + li] = lamp;
       cr[(yax ? 4 : 3) * NB + li] = G;
     }
+  }
+  if (A.flags & BMPC_F_CARRY) {  // the refinement base of the next sweep
+    double* cr = A.carry + (size_t)inst * carry_doubles(NB);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int q = lane + 32 * h;
+      if (q < 2 * RX) cr[5 * NB + q] = ws.sol[(q >= RX ? 32 : 0) + q - (q >= RX ? RX : 0)];
+    }
+    if (lane < RP) cr[5 * NB + 2 * RX + lane] = ws.solp[lane];
   }
 }
 

@@ -101,6 +101,8 @@ extern "C" {
 const char* bmpc_last_error(void) { return g_err.c_str(); }
 int bmpc_abi_version(void) { return 1; }
 
+int bmpc_carry_doubles(const bmpc_ctx* ctx) { return ctx ? carry_doubles(ctx->C.nb) : -1; }
+
 int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pdot,
                     const double* Pddot, const double* tau, const double* kinv_axis,
                     const double* k_axis, const double* kinv_psi, const double* k_psi,

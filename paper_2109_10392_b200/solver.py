@@ -410,7 +410,7 @@ class BatchSolver:
         nb, n, L = self.basis.n_b, self.basis.grid.n, prob.L
         dev = prob.b_xy.device
         sol = D.alloc_solution(nb, n, L, max_iter, True, dev)
-        carry = torch.empty(L, 5 * nb, dtype=torch.float64, device=dev)
+        carry = torch.empty(L, nat.load().bmpc_carry_doubles(ctx), dtype=torch.float64, device=dev)
         opts = nat.SolveOpts(max_iter=int(max_iter), tol=float(tol),
                              keep_multipliers=int(bool(keep_multipliers)), want_v=1)
         if wd is not None:
