@@ -92,6 +92,7 @@ EXPORTS = {
     "bmpc_op_tail": ([c_int, c_int, c_int] + [c_void_p] * 9 + [c_double] * 5 + [c_void_p] * 12
                      + [c_void_p], c_int),
     "bmpc_dfma_peak": ([c_int, _dp, c_void_p], c_int),
+    "bmpc_math_check": ([c_int, c_longlong, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p], c_int),
 }
 
 _lock = threading.Lock()

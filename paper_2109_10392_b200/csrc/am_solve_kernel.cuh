@@ -233,7 +233,12 @@ __device__ __forceinline__ void tail_block(const TailArgs& T, const int (&k)[NS]
     }
   }
   if (!(valid && leader)) return;
-  double gax[NS], gay[NS], gnx[NS], gny[NS];
+  double gax[NS], gay[NS], gnx[NS], gny[NS], sps[NS], cps[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) sincos_nb(ps[s], &sps[s], &cps[s]);
+#pragma unroll
+  for (int s = 0; s < NS; ++s)  // huge / non-finite headings: CUDA's full-range sincos
+    if (!(fabs(ps[s]) < 1.0e5)) sincos(ps[s], &sps[s], &cps[s]);
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
     sqo += sq[s];
@@ -252,10 +257,8 @@ __device__ __forceinline__ void tail_block(const TailArgs& T, const int (&k)[NS]
     const double s2 = fma(xd, xd, yd * yd);
     double v = s2 * rsqrt_nb(s2);
     v = v < T.v_min ? T.v_min : (v > T.v_max ? T.v_max : v);
-    double sp, cpv;
-    sincos(ps[s], &sp, &cpv);
-    gnx[s] = v * cpv;
-    gny[s] = v * sp;
+    gnx[s] = v * cps[s];
+    gny[s] = v * sps[s];
     const double rnx = xd - gnx[s], rny = yd - gny[s];
     sqn = fma(rnx, rnx, fma(rny, rny, sqn));
     if (T.v_out) T.v_out[(size_t)k[s] * T.L + T.inst] = v;
@@ -503,21 +506,41 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
     // (2) heading target theta = unwrap(atan2(ydot, xdot)) and P^T theta.
     //     Slot r < F: sample lane + 32 r.  Leftover slot (n % 32 samples): split
     //     mode gives each sample a group of g lanes that share its obstacles.
+    {
+      int r = 0;
 #pragma unroll 1
-    for (int r = 0; r < nslots; ++r) {
-      const Slot S = slot(r, lane, sl);
-      if (S.valid) {
-        double xd = 0.0, yd = 0.0;
+      for (; r + 1 < sl.F; r += 2) {  // two full slots per pass
+        const int k0 = lane + 32 * r, k1 = k0 + 32;
+        double xd0 = 0.0, yd0 = 0.0, xd1 = 0.0, yd1 = 0.0;
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
-          const double pd = sPd[i * npad + S.k];
+          const double pd0 = sPd[i * npad + k0], pd1 = sPd[i * npad + k1];
           const double2 c = cxy[i];
-          xd = fma(pd, c.x, xd);
-          yd = fma(pd, c.y, yd);
+          xd0 = fma(pd0, c.x, xd0);
+          yd0 = fma(pd0, c.y, yd0);
+          xd1 = fma(pd1, c.x, xd1);
+          yd1 = fma(pd1, c.y, yd1);
         }
-        const double p = atan2(yd, xd);
-        if (S.leader) {
-          ws.th[S.k] = p;
+        ws.th[k0] = atan2_nb(yd0, xd0);
+        ws.th[k1] = atan2_nb(yd1, xd1);
+        ws.xd[k0] = xd0;
+        ws.yd[k0] = yd0;
+        ws.xd[k1] = xd1;
+        ws.yd[k1] = yd1;
+      }
+#pragma unroll 1
+      for (; r < nslots; ++r) {
+        const Slot S = slot(r, lane, sl);
+        if (S.valid && S.leader) {
+          double xd = 0.0, yd = 0.0;
+#pragma unroll
+          for (int i = 0; i < NB; ++i) {
+            const double pd = sPd[i * npad + S.k];
+            const double2 c = cxy[i];
+            xd = fma(pd, c.x, xd);
+            yd = fma(pd, c.y, yd);
+          }
+          ws.th[S.k] = atan2_nb(yd, xd);
           ws.xd[S.k] = xd;
           ws.yd[S.k] = yd;
         }

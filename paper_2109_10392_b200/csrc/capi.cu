@@ -52,6 +52,8 @@ cudaError_t op_pack_xi(long long total, const double* xi_x, const double* xi_y, 
 cudaError_t op_first_converged(int iters, long long L, const double* hist, double tol, int* tstar,
                                cudaStream_t st);
 cudaError_t dfma_peak_tflops(int reps, double* tflops, cudaStream_t st);
+cudaError_t op_math_check(int fn, long long n, const double* a, const double* b, double* out,
+                          double* out2, cudaStream_t st);
 }  // namespace bmpc
 
 struct bmpc_ctx {
@@ -539,6 +541,14 @@ int bmpc_op_tail(int n, int l, int mn, const double* x, const double* y, const d
   CK(bmpc::op_tail(with_angles, n, l, mn, x, y, xd, yd, xdd, ydd, psi, xi_x, xi_y, v_min, v_max, a_max,
                    a, b, alpha, d, alpha_a, d_a, v, r_x, r_y, g_x, g_y, sq_obs, sq_acc, sq_nonhol, S_(s)),
      "tail");
+  return BMPC_OK;
+}
+
+int bmpc_math_check(int fn, long long n, const double* a, const double* b, double* out,
+                    double* out2, void* s) {
+  if (fn < 0 || fn > 5 || !a || !out || (fn == 3 || fn == 4) && !out2)
+    return fail(BMPC_EINVAL, "bmpc_math_check: bad argument");
+  CK(bmpc::op_math_check(fn, n, a, b, out, out2, S_(s)), "math_check");
   return BMPC_OK;
 }
 

@@ -509,3 +509,30 @@ cudaError_t op_first_converged(int iters, long long L, const double* hist, doubl
 }
 
 }  // namespace bmpc
+
+// ---------------------------------------------------------- math checks --
+// Device-math validation hook for the tests: fn 0 atan2_nb, 1 CUDA atan2,
+// 2 rsqrt_nb, 3 sincos_nb, 4 CUDA sincos, 5 div_nb.
+namespace bmpc {
+__global__ void k_math_check(int fn, long long n, const double* __restrict__ a,
+                             const double* __restrict__ b, double* out, double* out2) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const double x = a[e], y = b ? b[e] : 0.0;
+  double s = 0.0, c = 0.0;
+  switch (fn) {
+    case 0: out[e] = atan2_nb(x, y); break;
+    case 1: out[e] = atan2(x, y); break;
+    case 2: out[e] = rsqrt_nb(x); break;
+    case 3: sincos_nb(x, &s, &c); out[e] = s; out2[e] = c; break;
+    case 4: sincos(x, &s, &c); out[e] = s; out2[e] = c; break;
+    case 5: out[e] = div_nb(x, y); break;
+    default: break;
+  }
+}
+cudaError_t op_math_check(int fn, long long n, const double* a, const double* b, double* out,
+                          double* out2, cudaStream_t st) {
+  if (n > 0) k_math_check<<<nblk(n), kTB, 0, st>>>(fn, n, a, b, out, out2);
+  return cudaGetLastError();
+}
+}  // namespace bmpc

@@ -88,3 +88,49 @@ def test_dfma_peak_positive(cuda):
 
     tf = peak_fp64_tflops(2)
     assert 1.0 < tf < 200.0
+
+
+def test_device_math(cuda):
+    """Branch-free atan2 / sincos / rsqrt / div used inside the AM kernel vs libm
+    (numpy): <= 2 ulp, i.e. as good as CUDA's own (also measured here)."""
+    import ctypes
+
+    from paper_2109_10392_b200 import _native as nat
+    from paper_2109_10392_b200.device import stream_ptr
+
+    rng = np.random.default_rng(3)
+    N = 1 << 20
+    y = np.concatenate([rng.normal(0, 1, N // 2), rng.normal(0, 30, N // 4),
+                        rng.uniform(-1e-3, 1e-3, N // 4)])
+    x = np.concatenate([rng.normal(15, 10, N // 2), rng.normal(0, 1e-2, N // 4),
+                        rng.uniform(-40, 40, N // 4)])
+    y[:6] = [0.0, -0.0, 0.0, -0.0, 1.0, -1.0]
+    x[:6] = [0.0, 0.0, -0.0, -0.0, 0.0, -0.0]
+    t = lambda a: cuda.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    ty, tx = t(y), t(x)
+    out, out2 = cuda.empty_like(ty), cuda.empty_like(ty)
+    lib = nat.load()
+    sp = ctypes.c_void_p(stream_ptr())
+
+    def run(fn, a, b=None):
+        nat.check(lib.bmpc_math_check(fn, a.numel(), a.data_ptr(), b.data_ptr() if b is not None else None,
+                                      out.data_ptr(), out2.data_ptr(), sp))
+        return out.cpu().numpy().copy(), out2.cpu().numpy().copy()
+
+    def ulps(got, ref):
+        return np.abs(got - ref) / np.spacing(np.maximum(np.abs(ref), 1e-300))
+
+    ref = np.arctan2(y, x)
+    got, _ = run(0, ty, tx)
+    np.testing.assert_array_equal(got[:6], ref[:6])  # signed zeros and axes exactly
+    assert ulps(got, ref).max() <= 2.0
+    cuda_a, _ = run(1, ty, tx)
+    assert ulps(cuda_a, ref).max() <= 2.0
+    th = np.concatenate([rng.normal(0, 0.3, N // 2), rng.uniform(-50, 50, N // 2)])
+    s, c = run(3, t(th))
+    assert ulps(s, np.sin(th)).max() <= 2.0 and ulps(c, np.cos(th)).max() <= 2.0
+    r2 = rng.uniform(1e-6, 1e6, N)
+    rs, _ = run(2, t(r2))
+    assert ulps(rs, 1.0 / np.sqrt(r2)).max() <= 2.0
+    q, _ = run(5, t(y), t(x + 50.0))
+    assert ulps(q, y / (x + 50.0)).max() <= 1.0
