@@ -192,7 +192,8 @@ def run_ours(args, rank, world, local_rank):
     pstruct = prob.c_struct()
     sol = D.alloc_solution(nb, n, L, iters, False, dev)
     sc = D.alloc_score(L, prob.S, dev)
-    opts = nat.SolveOpts(max_iter=iters, tol=0.0)
+    prec = 1 if args.precision == "fp32" else 0
+    opts = nat.SolveOpts(max_iter=iters, tol=0.0, precision=prec)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     launches_per_step = 6  # solve: pack, am_solve, first_converged; score: pack, score, argmin
 
@@ -270,14 +271,16 @@ def run_ours(args, rank, world, local_rank):
     H.xi_x, H.xi_y, H.b_xy, H.b_psi = pin(W.xi_x), pin(W.xi_y), pin(W.b_xy), pin(W.b_psi)
     H.l, H.S, H.a, H.b, H.v_min, H.v_max, H.a_max = W.l, W.S, W.a, W.b, W.v_min, W.v_max, W.a_max
     for _ in range(args.warmup):
-        plan_batch(solver, H, max_iter=iters, tol=0.0, spec=spec, limits=limits)
+        plan_batch(solver, H, max_iter=iters, tol=0.0, spec=spec, limits=limits,
+                   precision=args.precision)
     e2e_ms = []
     best_e2e = None
     for i in range(args.steps):
         flush.fill_(float(i))
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        res = plan_batch(solver, H, max_iter=iters, tol=0.0, spec=spec, limits=limits)
+        res = plan_batch(solver, H, max_iter=iters, tol=0.0, spec=spec, limits=limits,
+                         precision=args.precision)
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
         best_e2e = res.best_index[0]
     e2e_local = sum(e2e_ms)
@@ -302,7 +305,8 @@ def run_ours(args, rank, world, local_rank):
         line = {
             "metric": METRIC, "value": value, "unit": "problems/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64" if prec == 0 else "f64+f32 (fp32 obstacle block)",
             "data": "synthetic (seeded scene generator, paper_2109_10392_b200/scenes.py)",
             "config": {"workload": args.config, "problems_per_gpu": L, "iters": iters, "n": n,
                        "m": W.m, "n_b": nb, "scenes_per_gpu": W.S, "tol": 0.0,
@@ -373,6 +377,8 @@ def main():
     ap.add_argument("--iters", type=int, default=0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"],
+                    help="fp32: mixed precision, fp32 obstacle block (tolerance in DESIGN.md)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

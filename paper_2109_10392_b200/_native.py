@@ -32,7 +32,7 @@ class Problem(Structure):
 class SolveOpts(Structure):
     _fields_ = [
         ("max_iter", c_int), ("tol", c_double), ("keep_multipliers", c_int),
-        ("warps_per_block", c_int), ("want_v", c_int),
+        ("warps_per_block", c_int), ("want_v", c_int), ("precision", c_int),
         ("w_alpha", c_void_p), ("w_d", c_void_p), ("w_alpha_a", c_void_p), ("w_d_a", c_void_p),
         ("w_v", c_void_p), ("w_c_psi", c_void_p),
         ("w_l_x", c_void_p), ("w_l_y", c_void_p), ("w_l_psi", c_void_p),

@@ -28,6 +28,7 @@ enum {
   BMPC_F_HISTORY = 1,   // write residual history rows
   BMPC_F_V = 2,         // write the last tail's clipped speed v (n, L)
   BMPC_F_CARRY = 4,     // write the carried state (for chunked / resumed solves)
+  BMPC_F_F32 = 8,       // mixed precision: fp32 obstacle block
 };
 
 typedef struct {

@@ -6,11 +6,11 @@ namespace bmpc {
 
 size_t am_solve_smem_bytes(int nb, int npad, int kxs, int kps, int warps);
 
-template <int NB, int NKM>
+template <int NB, int NKM, bool F32>
 static cudaError_t launch_t(const bmpc_dev_consts& C, const bmpc_solve_args& A, int warps,
                             cudaStream_t st) {
   const size_t smem = am_solve_smem_bytes(NB, C.npad, C.kxs, C.kps, warps);
-  auto kfn = am_solve_kernel<NB, NKM>;
+  auto kfn = am_solve_kernel<NB, NKM, F32>;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int grid = (A.L + warps - 1) / warps;
@@ -24,11 +24,16 @@ static cudaError_t launch_t(const bmpc_dev_consts& C, const bmpc_solve_args& A, 
 cudaError_t BMPC_CAT(launch_am_nb_, BMPC_INST_NB)(const bmpc_dev_consts& C,
                                                    const bmpc_solve_args& A, int warps,
                                                    cudaStream_t st) {
-  switch (C.npad) {  // the host pads n to 64, 128 or 256 samples
-    case 64: return launch_t<BMPC_INST_NB, 2>(C, A, warps, st);
-    case 128: return launch_t<BMPC_INST_NB, 4>(C, A, warps, st);
-    case 224: return launch_t<BMPC_INST_NB, 7>(C, A, warps, st);
-    case 256: return launch_t<BMPC_INST_NB, 8>(C, A, warps, st);
+  const bool f32 = (A.flags & BMPC_F_F32) != 0;
+  switch (C.npad) {  // the host pads n to 64, 128, 224 or 256 samples
+    case 64: return f32 ? launch_t<BMPC_INST_NB, 2, true>(C, A, warps, st)
+                                 : launch_t<BMPC_INST_NB, 2, false>(C, A, warps, st);
+    case 128: return f32 ? launch_t<BMPC_INST_NB, 4, true>(C, A, warps, st)
+                                 : launch_t<BMPC_INST_NB, 4, false>(C, A, warps, st);
+    case 224: return f32 ? launch_t<BMPC_INST_NB, 7, true>(C, A, warps, st)
+                                 : launch_t<BMPC_INST_NB, 7, false>(C, A, warps, st);
+    case 256: return f32 ? launch_t<BMPC_INST_NB, 8, true>(C, A, warps, st)
+                                 : launch_t<BMPC_INST_NB, 8, false>(C, A, warps, st);
     default: return cudaErrorInvalidValue;
   }
 }

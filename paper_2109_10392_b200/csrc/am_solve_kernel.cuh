@@ -173,7 +173,29 @@ struct TailArgs {
 // ...; `group` > 1 marks a split slot whose obstacle partials are summed over
 // `group` consecutive lanes (warp-uniform).  Accumulation order per sample
 // and across samples is the order of the sample list.
-template <int NS, int NB, int NPAD>
+// fp32 mode obstacle term.  In exact arithmetic the reference's closed forms
+// give r = w - a d (cos, sin) = 0 and g = x whenever the sample is outside the
+// ellipse (d = r/(ab) > 1), and d = 1 inside; so only inside terms carry a
+// residual, r = w - (a cos, b sin), and g = x - r always.  Evaluating that
+// form in fp32 (w rounded from the fp64 difference) keeps far and virtual
+// obstacles (+1e4 m) exact instead of rounding |w| ~ 1e4 m in fp32.
+__device__ __forceinline__ void obstacle_term_f32(double x, double y, double2 q, float a, float b,
+                                                  float ab2, float& srx, float& sry, float& sq) {
+  const float wx = (float)(x - q.x), wy = (float)(y - q.y);
+  const float px = b * wx, py = a * wy;
+  const float r2 = fmaf(px, px, py * py);
+  const float ri = rsqrtf(r2);
+  const bool pos = r2 > 0.f;
+  const float ca = pos ? px * ri : 1.f, sa = pos ? py * ri : 0.f;
+  const bool inside = r2 < ab2;  // r / (ab) < 1  <=>  d = 1
+  const float rx = inside ? fmaf(-a, ca, wx) : 0.f;
+  const float ry = inside ? fmaf(-b, sa, wy) : 0.f;
+  sq = fmaf(rx, rx, fmaf(ry, ry, sq));
+  srx += rx;
+  sry += ry;
+}
+
+template <int NS, int NB, int NPAD, bool F32>
 __device__ __forceinline__ void tail_block(const TailArgs& T, const int (&k)[NS], int j0, int js,
                                            int group, bool valid, bool leader, double (&Gx)[NB],
                                            double (&Gy)[NB], double& sqo, double& sqa,
@@ -198,30 +220,66 @@ __device__ __forceinline__ void tail_block(const TailArgs& T, const int (&k)[NS]
     }
     // obstacle block (_speedups.pyx:150-176), summed over this lane's obstacles
     const int qstep = js * T.n;
-    constexpr int U = NS == 1 ? 4 : 2;  // independent terms in flight per sample
+    constexpr int U = F32 ? 4 : (NS == 1 ? 4 : 2);  // independent terms in flight per sample
     const double2* qp[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) qp[s] = T.xi + j0 * T.n + k[s];
+    float srx[NS], sry[NS], sqf[NS];  // fp32 mode: sum_j r_j and sum_j |r_j|^2
+#pragma unroll
+    for (int s = 0; s < NS; ++s) srx[s] = sry[s] = sqf[s] = 0.f;
+    const float af = (float)T.a, bf = (float)T.b, ab2 = (float)(T.a * T.b * T.a * T.b);
     int j = j0;
+    // software pipeline: the next group's predictions are in flight while the
+    // current group computes (xi comes from L2 once it outgrows L1, e.g. c4)
+    double2 qn[NS][U];
+    if (j + (U - 1) * js < T.m) {
+#pragma unroll
+      for (int s = 0; s < NS; ++s)
+#pragma unroll
+        for (int u = 0; u < U; ++u) qn[s][u] = __ldg(qp[s] + u * qstep);
+    }
     for (; j + (U - 1) * js < T.m; j += U * js) {
       double2 q[NS][U];
 #pragma unroll
       for (int s = 0; s < NS; ++s)
 #pragma unroll
-        for (int u = 0; u < U; ++u) q[s][u] = __ldg(qp[s] + u * qstep);
+        for (int u = 0; u < U; ++u) q[s][u] = qn[s][u];
+      if (j + (2 * U - 1) * js < T.m) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+#pragma unroll
+          for (int u = 0; u < U; ++u) qn[s][u] = __ldg(qp[s] + (U + u) * qstep);
+      }
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int s = 0; s < NS; ++s)
-          obstacle_term(x[s], y[s], q[s][u], T.a, T.b, T.inv_ab, gsx[s], gsy[s], sq[s]);
+        for (int s = 0; s < NS; ++s) {
+          if constexpr (F32)
+            obstacle_term_f32(x[s], y[s], q[s][u], af, bf, ab2, srx[s], sry[s], sqf[s]);
+          else
+            obstacle_term(x[s], y[s], q[s][u], T.a, T.b, T.inv_ab, gsx[s], gsy[s], sq[s]);
+        }
 #pragma unroll
       for (int s = 0; s < NS; ++s) qp[s] += U * qstep;
     }
     for (; j < T.m; j += js) {
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
-        obstacle_term(x[s], y[s], __ldg(qp[s]), T.a, T.b, T.inv_ab, gsx[s], gsy[s], sq[s]);
+        if constexpr (F32)
+          obstacle_term_f32(x[s], y[s], __ldg(qp[s]), af, bf, ab2, srx[s], sry[s], sqf[s]);
+        else
+          obstacle_term(x[s], y[s], __ldg(qp[s]), T.a, T.b, T.inv_ab, gsx[s], gsy[s], sq[s]);
         qp[s] += qstep;
+      }
+    }
+    if constexpr (F32) {
+      // g_j = x - r_j exactly, so sum_j g_j = (#obstacles) x - sum_j r_j
+      const double cnt = j0 < T.m ? (double)((T.m - j0 + js - 1) / js) : 0.0;
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        gsx[s] = fma(cnt, x[s], -(double)srx[s]);
+        gsy[s] = fma(cnt, y[s], -(double)sry[s]);
+        sq[s] = (double)sqf[s];
       }
     }
   }
@@ -279,7 +337,7 @@ __device__ __forceinline__ void tail_block(const TailArgs& T, const int (&k)[NS]
   }
 }
 
-template <int NB, int NKM>
+template <int NB, int NKM, bool F32>
 __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
                                                        const bmpc_solve_args A) {
   extern __shared__ __align__(16) double sm[];
@@ -396,15 +454,18 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
         if (cold) {
           const double xl = __dadd_rn(x0, __dmul_rn(sTau[k], __dsub_rn(xf, x0)));
           const double yl = __dadd_rn(y0, __dmul_rn(sTau[k], __dsub_rn(yf, y0)));
+#pragma unroll 2
           for (int j = 0; j < m; ++j) {
             const double2 q = __ldg(xi + j * n + k);
             const double wx = xl - q.x, wy = yl - q.y;
-            const double al = atan2(a * wy, b * wx);
+            // the reference's trig form (obstacle_update, _speedups.pyx:12-39) with
+            // the branch-free <=2-ulp atan2/sincos (alpha is in [-pi, pi])
+            const double al = atan2_nb(a * wy, b * wx);
             double sa, ca;
-            sincos(al, &sa, &ca);
+            sincos_nb(al, &sa, &ca);
             const double num = __dadd_rn(__dmul_rn(__dmul_rn(a, ca), wx), __dmul_rn(__dmul_rn(b, sa), wy));
             const double den = __dadd_rn(__dmul_rn(a * ca, a * ca), __dmul_rn(b * sa, b * sa));
-            double d = num / den;
+            double d = div_nb(num, den);  // den >= b^2 > 0
             d = d < 1.0 ? 1.0 : d;
             gsx += q.x + __dmul_rn(a * d, ca);
             gsy += q.y + __dmul_rn(b * d, sa);
@@ -616,14 +677,14 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
 #pragma unroll 1
       for (; r + 1 < sl.F; r += 2) {
         const int ks[2] = {lane + 32 * r, lane + 32 * (r + 1)};
-        tail_block<2, NB, npad>(T, ks, 0, 1, 0, true, true, Gx, Gy, sqo, sqa, sqn);
+        tail_block<2, NB, npad, F32>(T, ks, 0, 1, 0, true, true, Gx, Gy, sqo, sqa, sqn);
       }
     }
 #pragma unroll 1
     for (; r < nslots; ++r) {
       const Slot S = slot(r, lane, sl);
       const int ks[1] = {S.k};
-      tail_block<1, NB, npad>(T, ks, S.j0, S.js, (r == sl.F) ? sl.g : 1, S.valid, S.leader, Gx, Gy,
+      tail_block<1, NB, npad, F32>(T, ks, S.j0, S.js, (r == sl.F) ? sl.g : 1, S.valid, S.leader, Gx, Gy,
                               sqo, sqa, sqn);
     }
     // warp contractions over the samples -> owner lanes (shared-memory transpose,

@@ -229,7 +229,7 @@ static int launch_sweeps(bmpc_ctx* ctx, const bmpc_problem* p, const double* xi2
   A.iters = iters;
   A.init_mode = init_mode;
   A.flags = (out->history ? BMPC_F_HISTORY : 0) | ((o->want_v && out->v) ? BMPC_F_V : 0) |
-            (write_carry ? BMPC_F_CARRY : 0);
+            (write_carry ? BMPC_F_CARRY : 0) | (o->precision == 1 ? BMPC_F_F32 : 0);
   A.hist_offset = hist_offset;
   A.a = p->a;
   A.b = p->b;
@@ -304,6 +304,7 @@ int bmpc_solve(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opts* o,
   int rc = check_problem(ctx, p);
   if (rc) return rc;
   if (!o || !out) return fail(BMPC_EINVAL, "null opts/out");
+  if (o->precision != 0 && o->precision != 1) return fail(BMPC_EINVAL, "precision must be 0 (fp64) or 1 (fp32 obstacle block)");
   if (o->max_iter < 1) return fail(BMPC_EINVAL, "max_iter must be >= 1");
   if (!out->history || !out->res_final)
     return fail(BMPC_EINVAL, "history and res_final outputs are required");

@@ -22,7 +22,7 @@ import numpy as np
 
 from . import _native as nat
 from .basis import BoundarySpec, build_basis, build_constant_matrices, build_time_grid
-from .solver import AmState, BatchSolver, ProblemBatch, Residuals
+from .solver import AmState, BatchSolver, ProblemBatch, Residuals, _precision_code
 from .traffic import VehicleState, predict_constant_velocity, select_nearest
 
 
@@ -319,7 +319,7 @@ class PlanResult:
 
 def plan_batch(solver: BatchSolver, scenes, max_iter: int = 100, tol: float = 0.0,
                spec: MetaCostSpec | None = None, limits: FilterLimits | None = None,
-               stream=None) -> PlanResult:
+               stream=None, precision: str = "fp64") -> PlanResult:
     """Solve + score S stacked scenes in one C-ABI call from host buffers
     (``bmpc_plan_host``): the end-to-end path the benchmark times.
 
@@ -345,7 +345,7 @@ def plan_batch(solver: BatchSolver, scenes, max_iter: int = 100, tol: float = 0.
     prob = nat.Problem(xi_x.shape[1] // n, l, S, xi_x.ctypes.data, xi_y.ctypes.data,
                        b_xy.ctypes.data, b_psi.ctypes.data, scenes.a, scenes.b, scenes.v_min,
                        scenes.v_max, scenes.a_max)
-    opts = nat.SolveOpts(max_iter=int(max_iter), tol=float(tol))
+    opts = nat.SolveOpts(max_iter=int(max_iter), tol=float(tol), precision=_precision_code(precision))
     coef = np.empty((3, nb, L))
     res = np.empty((3, L))
     out = nat.SolveOut(coef[0].ctypes.data, coef[1].ctypes.data, coef[2].ctypes.data, None, None,

@@ -116,6 +116,15 @@ class SolveInfo:
     iterates: list[tuple[np.ndarray, np.ndarray, np.ndarray]] | None = None
 
 
+def _precision_code(precision: str) -> int:
+    """"fp64": everything in double; "fp32": the obstacle block in single
+    precision (QP steps, sampling, contractions and multipliers stay fp64)."""
+    codes = {"fp64": 0, "fp32": 1}
+    if precision not in codes:
+        raise ValueError(f"precision must be one of {sorted(codes)}, got {precision!r}")
+    return codes[precision]
+
+
 def _inverse_ext(K: np.ndarray) -> np.ndarray:
     """Gauss-Jordan inverse with partial pivoting in x87 extended precision,
     rounded once to float64 (the KKT blocks are at most 22 x 22)."""
@@ -283,7 +292,8 @@ class BatchSolver:
                                        non_blocking=non_blocking)
 
     def solve_device(self, prob, max_iter: int = 150, tol: float = 1e-3, warm: dict | None = None,
-                     keep_multipliers: bool = False, want_v: bool = True, warps_per_block: int = 0):
+                     keep_multipliers: bool = False, want_v: bool = True, warps_per_block: int = 0,
+                     precision: str = "fp64"):
         """Solve a DeviceProblem (one or many scenes) with every buffer in HBM.
 
         ``warm`` maps AmState field names to device tensors.  Returns a
@@ -300,7 +310,8 @@ class BatchSolver:
         sol = D.alloc_solution(self.basis.n_b, self.basis.grid.n, prob.L, max_iter, want_v, dev)
         opts = nat.SolveOpts(max_iter=int(max_iter), tol=float(tol),
                              keep_multipliers=int(bool(keep_multipliers)),
-                             warps_per_block=int(warps_per_block), want_v=int(bool(want_v)))
+                             warps_per_block=int(warps_per_block), want_v=int(bool(want_v)),
+                             precision=_precision_code(precision))
         if warm is not None:
             for fld, key in (("w_alpha", "alpha"), ("w_d", "d"), ("w_alpha_a", "alpha_a"),
                              ("w_d_a", "d_a"), ("w_v", "v"), ("w_c_psi", "c_psi"),
