@@ -26,6 +26,7 @@ UNITS = [
     ("ops.cu", "ops", ["-fmad=false"]),
     ("capi.cu", "capi", []),
     ("peak.cu", "peak", []),
+    ("steps.cu", "steps", []),
 ] + [("am_inst.cu", f"am_inst_nb{nb}", [f"-DBMPC_INST_NB={nb}"]) for nb in range(4, 17)]
 
 

@@ -54,6 +54,17 @@ cudaError_t op_first_converged(int iters, long long L, const double* hist, doubl
 cudaError_t dfma_peak_tflops(int reps, double* tflops, cudaStream_t st);
 cudaError_t op_math_check(int fn, long long n, const double* a, const double* b, double* out,
                           double* out2, cudaStream_t st);
+cudaError_t op_project(const bmpc_dev_consts& C, int mode, int m, long long L, const double* g,
+                       double* out, cudaStream_t st);
+cudaError_t op_kkt_apply(const bmpc_dev_consts& C, int which, long long L, const double* rhs,
+                         double* out_x, double* out_y, cudaStream_t st);
+cudaError_t op_heading(const bmpc_dev_consts& C, long long L, const double* c_x, const double* c_y,
+                       double* theta, cudaStream_t st);
+cudaError_t op_d_obs(int n, long long l, long long mn, const double* x, const double* y,
+                     const double* xi_x, const double* xi_y, const double* alpha, double a,
+                     double b, double* d, cudaStream_t st);
+cudaError_t op_block_norms(int n, long long l, long long mn, const double* r_x, const double* r_y,
+                           double* out, cudaStream_t st);
 }  // namespace bmpc
 
 struct bmpc_ctx {
@@ -556,6 +567,37 @@ int bmpc_math_check(int fn, long long n, const double* a, const double* b, doubl
 int bmpc_dfma_peak(int reps, double* tflops, void* s) {
   if (!tflops) return fail(BMPC_EINVAL, "null output");
   CK(bmpc::dfma_peak_tflops(reps < 1 ? 1 : reps, tflops, S_(s)), "dfma_peak");
+  return BMPC_OK;
+}
+
+// ------------------------------------------------------- step-wise API ----
+int bmpc_project(bmpc_ctx* ctx, int mode, int m, int L, const double* g, double* out, void* s) {
+  if (!ctx || (mode != 0 && mode != 1) || m < 0 || L < 0 || !g || !out)
+    return fail(BMPC_EINVAL, "bmpc_project: bad argument");
+  CK(bmpc::op_project(ctx->C, mode, m, L, g, out, S_(s)), "project");
+  return BMPC_OK;
+}
+int bmpc_kkt_apply(bmpc_ctx* ctx, int which, int L, const double* rhs, double* out_a,
+                   double* out_b, void* s) {
+  if (!ctx || (which != 0 && which != 1) || L < 0 || !rhs || !out_a || (which == 0 && !out_b))
+    return fail(BMPC_EINVAL, "bmpc_kkt_apply: bad argument");
+  CK(bmpc::op_kkt_apply(ctx->C, which, L, rhs, out_a, out_b, S_(s)), "kkt_apply");
+  return BMPC_OK;
+}
+int bmpc_heading(bmpc_ctx* ctx, int L, const double* c_x, const double* c_y, double* theta, void* s) {
+  if (!ctx || L < 0 || !c_x || !c_y || !theta) return fail(BMPC_EINVAL, "bmpc_heading: bad argument");
+  CK(bmpc::op_heading(ctx->C, L, c_x, c_y, theta, S_(s)), "heading");
+  return BMPC_OK;
+}
+int bmpc_op_d_obs(int n, int l, int mn, const double* x, const double* y, const double* xi_x,
+                  const double* xi_y, const double* alpha, double a, double b, double* d, void* s) {
+  if (n < 1 || l < 0 || mn < 0 || mn % n) return fail(BMPC_EINVAL, "d_obs: bad shape");
+  CK(bmpc::op_d_obs(n, l, mn, x, y, xi_x, xi_y, alpha, a, b, d, S_(s)), "d_obs");
+  return BMPC_OK;
+}
+int bmpc_block_norms(int n, int l, int mn, const double* r_x, const double* r_y, double* out,
+                     void* s) {
+  CK(bmpc::op_block_norms(n, l, mn, r_x, r_y, out, S_(s)), "block_norms");
   return BMPC_OK;
 }
 

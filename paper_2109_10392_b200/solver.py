@@ -460,3 +460,187 @@ class BatchSolver:
         return AmState(c_x=h(sol.c_x), c_y=h(sol.c_y), c_psi=h(sol.c_psi), alpha=h(alpha), d=h(d),
                        alpha_a=h(alpha_a), d_a=h(d_a), v=h(sol.v), lambda_x=h(sol.l_x),
                        lambda_y=h(sol.l_y), lambda_psi=h(sol.l_psi), iteration=sol.iterations)
+
+    # -- step-wise API (solver.py:288-410) --------------------------------------
+    # The same math as the fused sweep, one reference step at a time, on host
+    # AmState arrays; every step runs on the device (csrc/steps.cu, csrc/ops.cu).
+    def _dev(self, a):
+        import torch
+
+        self._context()
+        return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+    def _samples(self, state: AmState, which):
+        from .device import DeviceSolution
+
+        d = self._dev
+        sol = DeviceSolution(d(state.c_x), d(state.c_y), d(state.c_psi), None, None, None, None,
+                             None, None, 0, False)
+        return self.sample_device(sol, which=which)
+
+    def _project(self, g, mode: int, m: int):
+        import torch
+
+        from .device import stream_ptr
+
+        g = self._dev(g) if isinstance(g, np.ndarray) else g.contiguous()
+        L = g.shape[1]
+        out = torch.empty(self.basis.n_b, L, dtype=torch.float64, device=g.device)
+        nat.check(nat.load().bmpc_project(self._context(), mode, m, L, g.data_ptr(), out.data_ptr(),
+                                          ctypes.c_void_p(stream_ptr())), "project")
+        return out
+
+    def _heading(self, c_x, c_y):
+        import torch
+
+        from .device import stream_ptr
+
+        L = c_x.shape[1]
+        th = torch.empty(self.basis.grid.n, L, dtype=torch.float64, device=c_x.device)
+        nat.check(nat.load().bmpc_heading(self._context(), L, c_x.data_ptr(), c_y.data_ptr(),
+                                          th.data_ptr(), ctypes.c_void_p(stream_ptr())), "heading")
+        return th
+
+    def _g_parts(self, state: AmState, batch: ProblemBatch):
+        """Penalty targets of a state (solver.py:281-286)."""
+        from . import kernels
+
+        psi = self._samples(state, ("psi",))["psi"]
+        d = self._dev
+        return kernels.assemble_g(d(batch.xi_x), d(batch.xi_y), d(state.alpha), d(state.d),
+                                  d(state.alpha_a), d(state.d_a), d(state.v), psi, batch.a, batch.b)
+
+    def build_g(self, state: AmState, batch: ProblemBatch) -> np.ndarray:
+        g_x, g_y = self._g_parts(state, batch)
+        return np.vstack([g_x.cpu().numpy(), g_y.cpu().numpy()])
+
+    def step_xy(self, state: AmState, batch: ProblemBatch):
+        """Equality-constrained QP update of c_x, c_y (solver.py:295-312)."""
+        g_x, g_y = self._g_parts(state, batch)
+        self._apply_xy(state, batch, g_x, g_y)
+        return state.c_x, state.c_y
+
+    def _apply_xy(self, state, batch, g_x, g_y):
+        import torch
+
+        from .device import stream_ptr
+
+        nb, l, m = self.basis.n_b, batch.l, self.mats.m
+        rho = batch.rho_xy
+        rhs = torch.empty(2 * nb + 12, l, dtype=torch.float64, device="cuda")
+        rhs[:nb] = rho * self._project(g_x, 0, m) + self._dev(state.lambda_x)
+        rhs[nb:2 * nb] = rho * self._project(g_y, 0, m) + self._dev(state.lambda_y)
+        rhs[2 * nb:] = self._dev(batch.b_xy)
+        cx = torch.empty(nb, l, dtype=torch.float64, device="cuda")
+        cy = torch.empty_like(cx)
+        nat.check(nat.load().bmpc_kkt_apply(self._context(), 0, l, rhs.data_ptr(), cx.data_ptr(),
+                                            cy.data_ptr(), ctypes.c_void_p(stream_ptr())), "kkt")
+        self.kkt.n_solves += 1
+        state.c_x, state.c_y = cx.cpu().numpy(), cy.cpu().numpy()
+
+    def step_psi(self, state: AmState, batch: ProblemBatch) -> np.ndarray:
+        """Heading QP on the unwrapped velocity angle (solver.py:314-328)."""
+        th = self._heading(self._dev(state.c_x), self._dev(state.c_y))
+        self._apply_psi(state, batch, th)
+        return state.c_psi
+
+    def _apply_psi(self, state, batch, theta):
+        import torch
+
+        from .device import stream_ptr
+
+        nb, l = self.basis.n_b, batch.l
+        theta = self._dev(theta) if isinstance(theta, np.ndarray) else theta
+        rhs = torch.empty(nb + 4, l, dtype=torch.float64, device="cuda")
+        rhs[:nb] = batch.rho_xy * self._project(theta, 1, 0) + self._dev(state.lambda_psi)
+        rhs[nb:] = self._dev(batch.b_psi)
+        cp = torch.empty(nb, l, dtype=torch.float64, device="cuda")
+        nat.check(nat.load().bmpc_kkt_apply(self._context(), 1, l, rhs.data_ptr(), cp.data_ptr(),
+                                            None, ctypes.c_void_p(stream_ptr())), "kkt")
+        self.kkt.n_solves += 1
+        state.c_psi = cp.cpu().numpy()
+
+    def step_v(self, state: AmState, batch: ProblemBatch) -> np.ndarray:
+        from . import kernels
+
+        s = self._samples(state, ("xdot", "ydot"))
+        state.v = kernels.v_update(s["xdot"], s["ydot"], batch.v_min, batch.v_max).cpu().numpy()
+        return state.v
+
+    def step_alpha_obs(self, state: AmState, batch: ProblemBatch) -> np.ndarray:
+        from . import kernels
+
+        s = self._samples(state, ("x", "y"))
+        alpha, _ = kernels.obstacle_update(s["x"], s["y"], self._dev(batch.xi_x), self._dev(batch.xi_y),
+                                           batch.a, batch.b)
+        state.alpha = alpha.cpu().numpy()
+        return state.alpha
+
+    def step_d_obs(self, state: AmState, batch: ProblemBatch) -> np.ndarray:
+        """1-D bound-constrained QP over each separation ratio, given alpha."""
+        import torch
+
+        from .device import stream_ptr
+
+        s = self._samples(state, ("x", "y"))
+        n, l = s["x"].shape
+        mn = batch.xi_x.shape[0]
+        al = self._dev(state.alpha)
+        d = torch.empty(mn, l, dtype=torch.float64, device="cuda")
+        xi_x, xi_y = self._dev(batch.xi_x), self._dev(batch.xi_y)
+        nat.check(nat.load().bmpc_op_d_obs(n, l, mn, s["x"].data_ptr(), s["y"].data_ptr(),
+                                           xi_x.data_ptr(), xi_y.data_ptr(), al.data_ptr(),
+                                           float(batch.a), float(batch.b), d.data_ptr(),
+                                           ctypes.c_void_p(stream_ptr())), "d_obs")
+        state.d = d.cpu().numpy()
+        return state.d
+
+    def step_alpha_acc(self, state: AmState, batch: ProblemBatch) -> np.ndarray:
+        from . import kernels
+
+        s = self._samples(state, ("xddot", "yddot"))
+        state.alpha_a = kernels.accel_update(s["xddot"], s["yddot"], batch.a_max)[0].cpu().numpy()
+        return state.alpha_a
+
+    def step_d_acc(self, state: AmState, batch: ProblemBatch) -> np.ndarray:
+        from . import kernels
+
+        s = self._samples(state, ("xddot", "yddot"))
+        state.d_a = kernels.accel_update(s["xddot"], s["yddot"], batch.a_max)[1].cpu().numpy()
+        return state.d_a
+
+    def _residual_parts(self, state: AmState, batch: ProblemBatch):
+        from . import kernels
+
+        s = self._samples(state, ("x", "y", "xdot", "ydot", "xddot", "yddot", "psi"))
+        d = self._dev
+        return kernels.residual_vectors(s["x"], s["y"], s["xdot"], s["ydot"], s["xddot"], s["yddot"],
+                                        s["psi"], d(batch.xi_x), d(batch.xi_y), d(state.alpha),
+                                        d(state.d), d(state.alpha_a), d(state.d_a), d(state.v),
+                                        batch.a, batch.b)
+
+    def update_multipliers(self, state: AmState, batch: ProblemBatch) -> None:
+        """Gradient-style multiplier update on the current residuals (solver.py:368-378)."""
+        r_x, r_y = self._residual_parts(state, batch)
+        m, rho = self.mats.m, batch.rho_xy
+        state.lambda_x = state.lambda_x - rho * self._project(r_x, 0, m).cpu().numpy()
+        state.lambda_y = state.lambda_y - rho * self._project(r_y, 0, m).cpu().numpy()
+        dc = self._dev
+        th = self._heading(dc(state.c_x), dc(state.c_y))
+        psi = self._samples(state, ("psi",))["psi"]
+        state.lambda_psi = state.lambda_psi - rho * self._project(psi - th, 1, 0).cpu().numpy()
+
+    def compute_residuals(self, state: AmState, batch: ProblemBatch) -> Residuals:
+        """Block L2 norms of the residual vectors (solver.py:392-410)."""
+        import torch
+
+        from .device import stream_ptr
+
+        r_x, r_y = self._residual_parts(state, batch)
+        n, l = self.basis.grid.n, batch.l
+        mn = batch.xi_x.shape[0]
+        out = torch.empty(3, l, dtype=torch.float64, device=r_x.device)
+        nat.check(nat.load().bmpc_block_norms(n, l, mn, r_x.data_ptr(), r_y.data_ptr(),
+                                              out.data_ptr(), ctypes.c_void_p(stream_ptr())), "norms")
+        o = out.cpu().numpy()
+        return Residuals(r_obs=o[0], r_acc=o[1], r_nonhol=o[2])
