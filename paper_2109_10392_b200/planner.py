@@ -211,6 +211,89 @@ def rank(plan: RankedPlan, spec: MetaCostSpec) -> RankedPlan:
     return plan
 
 
+@dataclass(frozen=True)
+class LaneGeometry:
+    """Straight road with equally spaced lanes; lane 0 is the right lane (planner.py:43-64)."""
+
+    n_lanes: int
+    width: float
+    y0: float = 0.0
+
+    def __post_init__(self):
+        if self.n_lanes < 1 or self.width <= 0:
+            raise ValueError("need at least one lane of positive width")
+
+    @property
+    def centers(self) -> np.ndarray:
+        return self.y0 + self.width * np.arange(self.n_lanes)
+
+    @property
+    def y_right(self) -> float:
+        return self.y0
+
+    def lane_of(self, y: float) -> int:
+        return int(np.argmin(np.abs(self.centers - y)))
+
+
+def sample_goals_cruise(ego: EgoState, lanes: LaneGeometry, spec: MetaCostSpec, l: int,
+                        t_f: float) -> list[Goal]:
+    """Round-robin lanes, all at the cruise distance (planner.py:96-110)."""
+    c = lanes.centers
+    return [Goal(x=ego.x + spec.v_cruise * t_f, y=float(c[i % lanes.n_lanes]), vx=spec.v_cruise,
+                 vy=0.0, ax=0.0, ay=0.0, lane=i % lanes.n_lanes) for i in range(l)]
+
+
+def sample_goals_highspeed(ego: EgoState, lanes: LaneGeometry, spec: MetaCostSpec, l: int,
+                           t_f: float) -> list[Goal]:
+    """~60% of the goals staggered on the right lane, the rest wide (planner.py:113-138)."""
+    if l < 2:
+        raise ValueError("high-speed sampling needs at least 2 goals")
+    n_right = math.ceil(0.6 * l)
+    c = lanes.centers
+    reach = spec.v_max * t_f
+    goals = [Goal(x=ego.x + dist, y=float(c[0]), vx=spec.v_max, vy=0.0, ax=0.0, ay=0.0, lane=0)
+             for dist in np.linspace(0.5 * reach, reach, n_right)]
+    other = list(range(1, lanes.n_lanes)) or [0]
+    for i in range(l - n_right):
+        lane = other[i % len(other)]
+        goals.append(Goal(x=ego.x + reach, y=float(c[lane]), vx=spec.v_max, vy=0.0, ax=0.0, ay=0.0,
+                          lane=lane))
+    return goals
+
+
+def sample_goals(ego: EgoState, lanes: LaneGeometry, spec: MetaCostSpec, l: int,
+                 t_f: float) -> list[Goal]:
+    if spec.kind == "cruise":
+        return sample_goals_cruise(ego, lanes, spec, l, t_f)
+    return sample_goals_highspeed(ego, lanes, spec, l, t_f)
+
+
+@dataclass
+class ControlCommand:
+    accel: float
+    steering: float
+
+
+def extract_control(traj: Candidate, h: float, dt_grid: float, dt_ctrl: float | None = None
+                    ) -> ControlCommand:
+    """Finite-difference accel and bicycle steering, read one control period
+    ahead (planner.py:260-274)."""
+    k = 1 if dt_ctrl is None else max(1, int(round(dt_ctrl / dt_grid)))
+    k = min(k, len(traj.v) - 1)
+    accel = (traj.v[k] - traj.v[k - 1]) / dt_grid
+    steering = math.atan(traj.psidot[k] * h / max(traj.v[k], 1e-6))
+    return ControlCommand(accel=accel, steering=steering)
+
+
+@dataclass
+class CycleResult:
+    command: ControlCommand
+    plan: RankedPlan
+    solve_time: float
+    info: object
+    fallback: bool
+
+
 def sample_goals_uniform(rng: np.random.Generator, ego: EgoState, l: int, t_f: float,
                          y_range=(-5.25, 5.25), v_range=(10.0, 30.0)) -> list[Goal]:
     """The BASELINE c1-c4 goal sampler: lateral target and terminal speed uniform."""
@@ -254,6 +337,15 @@ class Planner:
         self.basis = build_basis(grid, cfg.degree)
         self.mats = build_constant_matrices(self.basis, cfg.m, BoundarySpec())
         self.solver = BatchSolver(self.basis, self.mats, cfg.rho_xy)
+        self._prev_state = None
+        self._prev_steering = 0.0
+        # exact time-shift map in coefficient space (planner.py:326-334): the
+        # basis evaluated one control period later, projected back
+        from .basis import bernstein
+
+        span = grid.tf - grid.t0
+        u = (grid.times + cfg.dt_cycle - grid.t0) / span
+        self._shift_map = np.linalg.pinv(self.basis.P) @ bernstein(u, cfg.degree)
 
     def boundary_vectors(self, ego: EgoState, goals: list[Goal]) -> tuple[np.ndarray, np.ndarray]:
         l = len(goals)
@@ -291,6 +383,80 @@ class Planner:
         return RankedPlan(goals=goals, x=h["x"], y=h["y"], psi=h["psi"], psidot=h["psidot"], v=h["v"],
                           xddot=h["xddot"], yddot=h["yddot"], residuals=residuals,
                           _dev=dict(solver=self.solver, c_x=cx, c_y=cy, c_psi=cp, res=res, batch=batch))
+
+    def _warm_state(self, batch: ProblemBatch) -> AmState | None:
+        """Cold state with the near-converged previous instances shifted one
+        cycle, multipliers carried (planner.py:362-410); the shift and the
+        closed forms run on the device."""
+        import torch
+
+        from . import kernels
+        from .device import DeviceSolution
+
+        if self._prev_state is None:
+            return None
+        prev, prev_res = self._prev_state
+        if prev.c_x.shape[1] != batch.l:
+            return None
+        eligible = prev_res.max_per_instance() <= self.cfg.warm_residual_cap
+        if not eligible.any():
+            return None
+        idx = np.where(eligible)[0]
+        state = self.solver.init_state(batch)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        up = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)  # noqa: E731
+        S = up(self._shift_map)
+        cx, cy, cp = (S @ up(getattr(prev, k)[:, idx]) for k in ("c_x", "c_y", "c_psi"))
+        smp = self.solver.sample_device(
+            DeviceSolution(cx.contiguous(), cy.contiguous(), cp.contiguous(), None, None, None, None,
+                           None, None, 0, False), which=("x", "y", "xdot", "ydot", "xddot", "yddot"))
+        c = self.cfg
+        v = kernels.v_update(smp["xdot"], smp["ydot"], batch.v_min, batch.v_max)
+        alpha, d = kernels.obstacle_update(smp["x"], smp["y"], up(batch.xi_x), up(batch.xi_y),
+                                           batch.a, batch.b)
+        alpha_a, d_a = kernels.accel_update(smp["xddot"], smp["yddot"], batch.a_max)
+        h = lambda t: t.cpu().numpy()  # noqa: E731
+        state.c_x[:, idx], state.c_y[:, idx], state.c_psi[:, idx] = h(cx), h(cy), h(cp)
+        state.v[:, idx] = h(v)
+        state.alpha[:, idx], state.d[:, idx] = h(alpha), h(d)
+        state.alpha_a[:, idx], state.d_a[:, idx] = h(alpha_a), h(d_a)
+        for k in ("lambda_x", "lambda_y", "lambda_psi"):
+            getattr(state, k)[:, idx] = getattr(prev, k)[:, idx]
+        del c
+        return state
+
+    def fallback_command(self, ego: EgoState) -> ControlCommand:
+        """Hold steering, bleed speed toward v_min over the horizon (planner.py:425-430)."""
+        accel = max(-self.cfg.a_max, (self.cfg.v_min - ego.speed) / self.cfg.t_f)
+        return ControlCommand(accel=float(min(accel, self.cfg.a_max)), steering=self._prev_steering)
+
+    def mpc_cycle(self, ego: EgoState, vehicles: list[VehicleState]) -> CycleResult:
+        """One receding-horizon cycle (planner.py:432-462): goals, batch, warm
+        start, device solve with carried multipliers, fused scoring, control."""
+        import time
+
+        c = self.cfg
+        goals = sample_goals(ego, self.lanes, self.meta, c.l, c.t_f)
+        batch = self.build_batch(ego, vehicles, goals)
+        warm = self._warm_state(batch) if c.warm_start else None
+        start = time.perf_counter()
+        state, info = self.solver.solve(batch, max_iter=c.max_iter, tol=c.tol, warm=warm,
+                                        keep_multipliers=True)
+        solve_time = time.perf_counter() - start
+        plan = self.sample_plan(state, goals, info.residual_history[-1], batch)
+        filter_candidates(plan, batch, c.limits)
+        rank(plan, self.meta)
+        self._prev_state = (state, plan.residuals)
+        if plan.best_index is None:
+            command, fallback = self.fallback_command(ego), True
+        else:
+            command = extract_control(plan.candidate(plan.best_index), c.h, self.basis.grid.dt,
+                                      c.dt_cycle)
+            command.accel = float(np.clip(command.accel, -c.a_max, c.a_max))
+            fallback = False
+            self._prev_steering = command.steering
+        return CycleResult(command=command, plan=plan, solve_time=solve_time, info=info,
+                           fallback=fallback)
 
 
 @dataclass

@@ -226,8 +226,68 @@ def reverse_case():
     workload_fixture("reverse", W, 40, screen=True)
 
 
+def mpc_kat(cycles: int = 3):
+    """Closed-loop cruise_idm replay (seed 7, l=11, warm starts, tol=1e-3,
+    200 sweeps) through the reference's own harness objects, full precision.
+    Cross-checked against the reference's recorded testdata/run.jsonl."""
+    import json
+
+    from batchmpc import harness as H
+    from batchmpc.planner import EgoState, Planner
+    from batchmpc.traffic import VehicleState
+
+    cfg = H.load_config("/root/reference/pkg/configs/cruise_idm.toml")
+    rng = np.random.default_rng(cfg.seed)
+    lanes = cfg.lane_geometry
+    world = H.build_traffic(cfg, rng)
+    pc = cfg.planner_config
+    planner = Planner(pc, lanes, cfg.meta_spec)
+    ego = EgoState(x=cfg.ego_x, y=float(lanes.centers[cfg.ego_lane]), psi=0.0, psidot=0.0,
+                   vx=cfg.ego_v, vy=0.0, ax=0.0, ay=0.0)
+    kat = [json.loads(s) for s in open("/root/reference/pkg/frontend/testdata/run.jsonl")][1:]
+    out = dict(l=pc.l, n=pc.n, t_f=pc.t_f, degree=pc.degree, rho=pc.rho_xy, max_iter=pc.max_iter,
+               tol=pc.tol, m=pc.m, a=pc.a, b=pc.b, v_min=pc.v_min, v_max=pc.v_max, a_max=pc.a_max,
+               h=pc.h, dt_cycle=pc.dt_cycle, warm_residual_cap=pc.warm_residual_cap,
+               heading_limit=pc.limits.heading_limit, residual_tol=pc.limits.residual_tol,
+               collision_margin=pc.limits.collision_margin, n_lanes=lanes.n_lanes,
+               lane_width=lanes.width, lane_y0=lanes.y0, v_cruise=cfg.meta_spec.v_cruise,
+               meta_v_max=cfg.meta_spec.v_max, y_rl=cfg.meta_spec.y_rl, w1=cfg.meta_spec.w1,
+               w2=cfg.meta_spec.w2, cycles=cycles)
+    for c in range(cycles):
+        states = world.states()
+        res = planner.mpc_cycle(ego, states)
+        plan = res.plan
+        hist = np.stack([[r.r_obs, r.r_acc, r.r_nonhol] for r in res.info.residual_history])
+        # the reference's own recorded run (rounded by its log writer) must agree
+        rec = kat[c]
+        assert rec["best_index"] == plan.best_index
+        assert np.allclose(rec["meta_costs"], plan.meta_cost, atol=1e-9, rtol=0)
+        assert rec["command"]["accel"] == res.command.accel
+        p = f"c{c}_"
+        out[p + "ego"] = np.array([ego.x, ego.y, ego.psi, ego.psidot, ego.vx, ego.vy, ego.ax, ego.ay])
+        out[p + "obstacles"] = np.array([[s.id, s.x, s.y, s.vx, s.vy, s.lane] for s in states])
+        out[p + "meta_cost"] = plan.meta_cost
+        out[p + "feasible"] = plan.feasible.astype(np.uint8)
+        out[p + "min_ratio"] = plan.min_ratio
+        out[p + "heading_max"] = plan.heading_max
+        out[p + "best_index"] = np.int64(-1 if plan.best_index is None else plan.best_index)
+        out[p + "command"] = np.array([res.command.accel, res.command.steering])
+        out[p + "fallback"] = np.int64(res.fallback)
+        out[p + "iterations"] = np.int64(res.info.iterations)
+        out[p + "converged"] = np.int64(res.info.converged)
+        out[p + "history"] = hist
+        for k in ("x", "y", "psi", "psidot", "v"):
+            out[p + k] = getattr(plan, k)
+        ego = H._apply_command(ego, res.command, cfg.dt, cfg.h)
+        world.step(cfg.dt, ego=VehicleState(id=-100, x=ego.x, y=ego.y, vx=ego.vx, vy=ego.vy,
+                                            lane=lanes.lane_of(ego.y)))
+    np.savez_compressed(HERE / "mpc_kat.npz", **out)
+    print("mpc_kat", cycles, "cycles; matches testdata/run.jsonl")
+
+
 def main():
     t = time.time()
+    mpc_kat()
     tail_case()
     demo()
     workload_fixture("c0", make_workload("c0"), 100)
