@@ -93,6 +93,7 @@ EXPORTS = {
                      + [c_void_p], c_int),
     "bmpc_dfma_peak": ([c_int, _dp, c_void_p], c_int),
     "bmpc_math_check": ([c_int, c_longlong, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p], c_int),
+    "bmpc_latency_probe": ([c_int, _dp, c_void_p], c_int),
     "bmpc_project": ([c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p], c_int),
     "bmpc_kkt_apply": ([c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p], c_int),
     "bmpc_heading": ([c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p], c_int),

@@ -54,6 +54,7 @@ cudaError_t op_first_converged(int iters, long long L, const double* hist, doubl
 cudaError_t dfma_peak_tflops(int reps, double* tflops, cudaStream_t st);
 cudaError_t op_math_check(int fn, long long n, const double* a, const double* b, double* out,
                           double* out2, cudaStream_t st);
+cudaError_t latency_probe(int which, double* cyc_per_op, cudaStream_t st);
 cudaError_t op_project(const bmpc_dev_consts& C, int mode, int m, long long L, const double* g,
                        double* out, cudaStream_t st);
 cudaError_t op_kkt_apply(const bmpc_dev_consts& C, int which, long long L, const double* rhs,
@@ -567,6 +568,12 @@ int bmpc_math_check(int fn, long long n, const double* a, const double* b, doubl
 int bmpc_dfma_peak(int reps, double* tflops, void* s) {
   if (!tflops) return fail(BMPC_EINVAL, "null output");
   CK(bmpc::dfma_peak_tflops(reps < 1 ? 1 : reps, tflops, S_(s)), "dfma_peak");
+  return BMPC_OK;
+}
+
+int bmpc_latency_probe(int which, double* cycles_per_op, void* s) {
+  if (!cycles_per_op || which < 0 || which > 7) return fail(BMPC_EINVAL, "latency_probe: bad argument");
+  CK(bmpc::latency_probe(which, cycles_per_op, S_(s)), "latency_probe");
   return BMPC_OK;
 }
 

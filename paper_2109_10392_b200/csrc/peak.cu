@@ -5,6 +5,8 @@
 // reported against this measured DFMA rate (2 flops per DFMA).
 #include <cuda_runtime.h>
 
+#include "common.cuh"
+
 namespace bmpc {
 
 constexpr int kChains = 8;
@@ -59,4 +61,59 @@ cudaError_t dfma_peak_tflops(int reps, double* tflops, cudaStream_t st) {
   return e;
 }
 
+}  // namespace bmpc
+
+// ------------------------------------------------------ latency probes --
+// Dependent-chain latency (SM cycles per instruction, one thread):
+// 0 DFMA, 1 DADD, 2 DMUL, 3 MUFU.RSQ64H (+ 0 ALU, via rsqrt.approx), 4 FFMA,
+// 5 LDS.64 (pointer chase in shared memory), 6 SHFL (64-bit), 7 fp64 rsqrt_nb.
+namespace bmpc {
+template <int WHICH>
+__global__ void k_latency(int iters, double seed, long long* cycles, double* sink) {
+  __shared__ long long chase[64];
+  if (threadIdx.x == 0)
+    for (int i = 0; i < 64; ++i) chase[i] = (i + 1) & 63;
+  __syncwarp();
+  double x = seed, y = 1.0000001, z = 1e-9;
+  float xf = (float)seed;
+  long long p = 0;
+  const long long t0 = clock64();
+#pragma unroll 8
+  for (int i = 0; i < iters; ++i) {
+    if (WHICH == 0) x = fma(x, y, z);
+    if (WHICH == 1) x = x + z;
+    if (WHICH == 2) x = x * y;
+    if (WHICH == 3) asm volatile("rsqrt.approx.ftz.f64 %0, %0;" : "+d"(x));
+    if (WHICH == 4) xf = fmaf(xf, 1.0000001f, 1e-9f);
+    if (WHICH == 5) p = chase[p];
+    if (WHICH == 6) x = __shfl_xor_sync(0xffffffffu, x, 1);
+    if (WHICH == 7) x = rsqrt_nb(x) + 0.5;
+  }
+  const long long t1 = clock64();
+  if (threadIdx.x == 0) {
+    cycles[0] = t1 - t0;
+    sink[0] = x + xf + (double)p;
+  }
+}
+
+cudaError_t latency_probe(int which, double* cyc_per_op, cudaStream_t st) {
+  long long* c = nullptr;
+  double* s = nullptr;
+  cudaMalloc(&c, sizeof(long long));
+  cudaMalloc(&s, sizeof(double));
+  const int iters = 4096;
+  void (*fns[8])(int, double, long long*, double*) = {
+      k_latency<0>, k_latency<1>, k_latency<2>, k_latency<3>,
+      k_latency<4>, k_latency<5>, k_latency<6>, k_latency<7>};
+  if (which < 0 || which > 7) return cudaErrorInvalidValue;
+  fns[which]<<<1, 32, 0, st>>>(64, 1.5, c, s);
+  fns[which]<<<1, 32, 0, st>>>(iters, 1.5, c, s);
+  long long h = 0;
+  cudaMemcpyAsync(&h, c, sizeof(long long), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  cudaFree(c);
+  cudaFree(s);
+  *cyc_per_op = (double)h / iters;
+  return cudaGetLastError();
+}
 }  // namespace bmpc
