@@ -195,14 +195,13 @@ def run_ours(args, rank, world, local_rank):
     prec = 1 if args.precision == "fp32" else 0
     opts = nat.SolveOpts(max_iter=iters, tol=0.0, precision=prec)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    launches_per_step = 6  # solve: pack, am_solve, first_converged; score: pack, score, argmin
+    launches_per_step = 4  # pack_xi, am_solve (+ fused scoring), first_converged, argmin
 
     def step():
+        # one persistent launch (all sweeps + fused scoring epilogue) + per-scene argmin
         out = D.solution_struct(sol)
-        nat.check(lib.bmpc_solve(ctx, ctypes.byref(pstruct), ctypes.byref(opts), ctypes.byref(out), sp))
-        nat.check(lib.bmpc_score(ctx, ctypes.byref(pstruct), D.ptr(sol.c_x), D.ptr(sol.c_y),
-                                 D.ptr(sol.c_psi), D.ptr(sol.res_final), ctypes.byref(sspec),
-                                 ctypes.byref(D.score_struct(sc)), sp))
+        nat.check(lib.bmpc_plan(ctx, ctypes.byref(pstruct), ctypes.byref(opts), ctypes.byref(out),
+                                ctypes.byref(sspec), ctypes.byref(D.score_struct(sc)), sp))
         return out
 
     def kernel_only():

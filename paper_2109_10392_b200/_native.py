@@ -80,6 +80,8 @@ EXPORTS = {
                     POINTER(ScoreSpec), POINTER(ScoreOut), c_void_p], c_int),
     "bmpc_plan_host": ([c_void_p, POINTER(Problem), POINTER(SolveOpts), POINTER(SolveOut),
                         POINTER(ScoreSpec), POINTER(ScoreOut), c_void_p], c_int),
+    "bmpc_plan": ([c_void_p, POINTER(Problem), POINTER(SolveOpts), POINTER(SolveOut),
+                   POINTER(ScoreSpec), POINTER(ScoreOut), c_void_p], c_int),
     "bmpc_sample": ([c_void_p, c_int] + [c_void_p] * 12 + [c_void_p], c_int),
     "bmpc_op_obstacle_update": ([c_int, c_int, c_int] + [c_void_p] * 4 + [c_double, c_double]
                                 + [c_void_p] * 2 + [c_void_p], c_int),

@@ -29,7 +29,17 @@ enum {
   BMPC_F_V = 2,         // write the last tail's clipped speed v (n, L)
   BMPC_F_CARRY = 4,     // write the carried state (for chunked / resumed solves)
   BMPC_F_F32 = 8,       // mixed precision: fp32 obstacle block
+  BMPC_F_SCORE = 16,    // fused planner scoring after the last sweep
 };
+
+// Planner scoring parameters and outputs for the fused epilogue.
+typedef struct {
+  int kind;  // 0 cruise, 1 highspeed
+  double v_cruise, v_max, y_rl, w1, w2;
+  double heading_limit, residual_tol, ratio_min;
+  double *meta, *min_ratio, *heading_max;  // (L)
+  unsigned char* flags;                    // (L)
+} bmpc_fused_score;
 
 typedef struct {
   int m, l, L, S;       // obstacles, goals per scene, instances, scenes (L = S*l)
@@ -49,6 +59,7 @@ typedef struct {
   double* v_out;        // (n, L)
   double* hist;         // [rows][3][L]
   double* res_final;    // [3][L]
+  bmpc_fused_score score;  // used with BMPC_F_SCORE
 } bmpc_solve_args;
 
 // Doubles of carried state per instance: lambda_x, lambda_y, lambda_psi, G_x,

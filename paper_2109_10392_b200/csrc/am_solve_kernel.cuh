@@ -29,6 +29,7 @@
 
 #include "am_args.h"
 #include "common.cuh"
+#include "score.cuh"
 
 namespace bmpc {
 
@@ -736,9 +737,41 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
       if (A.flags & BMPC_F_HISTORY)
         A.hist[((size_t)(A.hist_offset + t) * 3 + (lane - 16)) * L + inst] = res;
       if (last && A.res_final) A.res_final[(size_t)(lane - 16) * L + inst] = res;
+      if (last) ws.res[60 + lane - 16] = res;  // for the fused scoring below
     }
     have_sol = true;
     __syncwarp();
+  }
+
+  // ------------------------------------------------- fused planner scoring ----
+  // sample_plan + filter_candidates + meta_cost of this instance straight from
+  // the on-chip coefficients (planner.py:210-245, :412-423; csrc/score.cuh).
+  if ((A.flags & BMPC_F_SCORE) && A.iters > 0) {
+    const bmpc_fused_score& F = A.score;
+    const ScoreParams sp{n, m, F.kind, a, b, F.v_cruise, F.v_max, F.y_rl, F.w1, F.w2,
+                         F.heading_limit, F.residual_tol, F.ratio_min};
+    const double2* __restrict__ cxy2 = reinterpret_cast<const double2*>(ws.cxy);
+    auto sample = [&](int k, double& x, double& y, double& xd, double& yd, double& ps) {
+      x = y = xd = yd = ps = 0.0;
+      for (int i = 0; i < NB; ++i) {
+        const double p = sP[i * npad + k], pd = sPd[i * npad + k];
+        const double2 c = cxy2[i];
+        x = __fma_rn(p, c.x, x);
+        y = __fma_rn(p, c.y, y);
+        xd = __fma_rn(pd, c.x, xd);
+        yd = __fma_rn(pd, c.y, yd);
+        ps = __fma_rn(p, ws.cp[i], ps);
+      }
+    };
+    double cost, rmin, hmax;
+    unsigned char f;
+    score_instance(sp, xi, sample, ws.res[60], ws.res[61], ws.res[62], cost, rmin, hmax, f);
+    if (lane == 0) {
+      F.meta[inst] = cost;
+      F.min_ratio[inst] = rmin;
+      F.heading_max[inst] = hmax;
+      F.flags[inst] = f;
+    }
   }
 
   // ------------------------------------------------------------- outputs ----

@@ -230,7 +230,8 @@ static int auto_warps(const bmpc_ctx* ctx, int L, int req) {
 // Launch `iters` sweeps; xi2 is the packed (S, m, n) double2 buffer.
 static int launch_sweeps(bmpc_ctx* ctx, const bmpc_problem* p, const double* xi2,
                          const bmpc_solve_opts* o, int iters, int init_mode, int hist_offset,
-                         double* carry, int write_carry, bmpc_solve_out* out, cudaStream_t st) {
+                         double* carry, int write_carry, bmpc_solve_out* out, cudaStream_t st,
+                         const bmpc_fused_score* fsc = nullptr) {
   const int L = p->S * p->l;
   bmpc_solve_args A;
   memset(&A, 0, sizeof(A));
@@ -271,6 +272,10 @@ static int launch_sweeps(bmpc_ctx* ctx, const bmpc_problem* p, const double* xi2
   A.v_out = out->v;
   A.hist = out->history;
   A.res_final = out->res_final;
+  if (fsc) {
+    A.flags |= BMPC_F_SCORE;
+    A.score = *fsc;
+  }
   if (L == 0 || iters <= 0) return BMPC_OK;
   CK(bmpc::launch_am_solve(ctx->C, A, auto_warps(ctx, L, o->warps_per_block), st), "am_solve launch");
   return BMPC_OK;
@@ -311,8 +316,56 @@ int bmpc_sweeps(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opts* o, 
   return rc;
 }
 
+static int solve_impl(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opts* o,
+                      bmpc_solve_out* out, const bmpc_fused_score* fsc, void* stream);
+
 int bmpc_solve(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opts* o,
                bmpc_solve_out* out, void* stream) {
+  return solve_impl(ctx, p, o, out, nullptr, stream);
+}
+
+static int check_spec(const bmpc_score_spec* spec) {
+  if (!spec) return fail(BMPC_EINVAL, "null score spec");
+  if (spec->kind != 0 && spec->kind != 1) return fail(BMPC_EINVAL, "unknown meta-cost kind");
+  if (spec->w1 < 0 || spec->w2 < 0) return fail(BMPC_EINVAL, "meta-cost weights must be nonnegative");
+  return BMPC_OK;
+}
+
+static bmpc_fused_score fused_from(const bmpc_score_spec* spec, const bmpc_score_out* so) {
+  bmpc_fused_score f;
+  f.kind = spec->kind;
+  f.v_cruise = spec->v_cruise;
+  f.v_max = spec->v_max;
+  f.y_rl = spec->y_rl;
+  f.w1 = spec->w1;
+  f.w2 = spec->w2;
+  f.heading_limit = spec->heading_limit;
+  f.residual_tol = spec->residual_tol;
+  f.ratio_min = 1.0 - spec->collision_margin;  // planner.py:244
+  f.meta = so->meta_cost;
+  f.min_ratio = so->min_ratio;
+  f.heading_max = so->heading_max;
+  f.flags = so->flags;
+  return f;
+}
+
+int bmpc_plan(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opts* o, bmpc_solve_out* out,
+              const bmpc_score_spec* spec, bmpc_score_out* so, void* stream) {
+  int rc = check_spec(spec);
+  if (rc) return rc;
+  if (!so || !so->meta_cost || !so->min_ratio || !so->heading_max || !so->flags)
+    return fail(BMPC_EINVAL, "bmpc_plan: per-instance score outputs required");
+  const bmpc_fused_score f = fused_from(spec, so);
+  if ((rc = solve_impl(ctx, p, o, out, &f, stream))) return rc;
+  if (so->best_index && so->argmin_all && so->argmin_hc && so->n_feasible)
+    CK(bmpc::op_argmin(p->S, p->l, so->meta_cost, so->flags, so->best_index, so->argmin_all,
+                       so->argmin_hc, so->n_feasible, S_(stream)),
+       "argmin");
+  return BMPC_OK;
+}
+
+static int solve_impl(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opts* o,
+                      bmpc_solve_out* out, const bmpc_fused_score* fsc, void* stream) {
   int rc = check_problem(ctx, p);
   if (rc) return rc;
   if (!o || !out) return fail(BMPC_EINVAL, "null opts/out");
@@ -331,7 +384,7 @@ int bmpc_solve(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opts* o,
     CK(bmpc::op_pack_xi(tot, p->xi_x, p->xi_y, xi2, st), "pack_xi");
   }
   const int mode = is_warm(o) ? BMPC_INIT_WARM : BMPC_INIT_COLD;
-  rc = launch_sweeps(ctx, p, xi2, o, o->max_iter, mode, 0, nullptr, 0, out, st);
+  rc = launch_sweeps(ctx, p, xi2, o, o->max_iter, mode, 0, nullptr, 0, out, st, fsc);
   int iters = o->max_iter, converged = 0;
   if (!rc && L > 0) {
     // Global early stop (solver.py:437-439): find the first sweep whose worst
@@ -348,7 +401,7 @@ int bmpc_solve(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opts* o,
       converged = 1;
       iters = t + 1;
       if (iters < o->max_iter)
-        rc = launch_sweeps(ctx, p, xi2, o, iters, mode, 0, nullptr, 0, out, st);
+        rc = launch_sweeps(ctx, p, xi2, o, iters, mode, 0, nullptr, 0, out, st, fsc);
     }
   }
   if (xi2) cudaFreeAsync(xi2, st);
@@ -464,13 +517,9 @@ int bmpc_plan_host(bmpc_ctx* ctx, const bmpc_problem* hp, const bmpc_solve_opts*
   dout.res_final = B.alloc<double>(3 * L);
   dout.v = (o->want_v && ho->v) ? B.alloc<double>(n * L) : nullptr;
   if (!coef || !dout.history || !dout.res_final) return fail(BMPC_ECUDA, "device allocation failed");
-  rc = bmpc_solve(ctx, &dp, o, &dout, stream);
-  if (rc) return rc;
-  ho->iterations = dout.iterations;
-  ho->converged = dout.converged;
   bmpc_score_out ds;
   memset(&ds, 0, sizeof(ds));
-  if (spec && hs) {
+  if (spec && hs) {  // solve with the fused scoring epilogue, then the per-scene argmin
     ds.meta_cost = B.alloc<double>(L);
     ds.min_ratio = B.alloc<double>(L);
     ds.heading_max = B.alloc<double>(L);
@@ -479,9 +528,13 @@ int bmpc_plan_host(bmpc_ctx* ctx, const bmpc_problem* hp, const bmpc_solve_opts*
     ds.argmin_all = B.alloc<long long>(hp->S);
     ds.argmin_hc = B.alloc<long long>(hp->S);
     ds.n_feasible = B.alloc<long long>(hp->S);
-    rc = bmpc_score(ctx, &dp, dout.c_x, dout.c_y, dout.c_psi, dout.res_final, spec, &ds, stream);
-    if (rc) return rc;
+    rc = bmpc_plan(ctx, &dp, o, &dout, spec, &ds, stream);
+  } else {
+    rc = bmpc_solve(ctx, &dp, o, &dout, stream);
   }
+  if (rc) return rc;
+  ho->iterations = dout.iterations;
+  ho->converged = dout.converged;
   struct Cp { void* h; const void* d; size_t bytes; };
   const Cp cps[] = {
       {ho->c_x, dout.c_x, nb * L * 8}, {ho->c_y, dout.c_y, nb * L * 8},

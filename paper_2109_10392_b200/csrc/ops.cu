@@ -15,6 +15,7 @@
 
 #include "am_args.h"
 #include "common.cuh"
+#include "score.cuh"
 
 namespace bmpc {
 
@@ -273,10 +274,10 @@ __global__ void k_score(const ScoreArgs S) {
   const double2* xi = reinterpret_cast<const double2*>(S.xi) + (size_t)(inst / S.l) * S.m * S.n;
   const double* P = S.PT;
   const double* Pd = S.PT + (size_t)S.nb * S.npad;
-  double hmax = 0.0, rmin = INFINITY, cost = 0.0;
-  bool any_nan = false;
-  for (int k = lane; k < S.n; k += 32) {
-    double x = 0, y = 0, xd = 0, yd = 0, ps = 0;
+  const ScoreParams sp{S.n, S.m, S.kind, S.a, S.b, S.v_cruise, S.v_max, S.y_rl, S.w1, S.w2,
+                       S.heading_limit, S.residual_tol, S.ratio_min};
+  auto sample = [&](int k, double& x, double& y, double& xd, double& yd, double& ps) {
+    x = y = xd = yd = ps = 0.0;
     for (int i = 0; i < S.nb; ++i) {
       const double p = P[i * S.npad + k], pd = Pd[i * S.npad + k];
       const size_t o = (size_t)i * S.L + inst;
@@ -286,36 +287,12 @@ __global__ void k_score(const ScoreArgs S) {
       yd = __fma_rn(pd, S.c_y[o], yd);
       ps = __fma_rn(p, S.c_psi[o], ps);
     }
-    const double v = sqrt(xd * xd + yd * yd);
-    const double ah = fabs(ps);
-    if (ah != ah) any_nan = true;
-    hmax = fmax(hmax, ah);
-    for (int j = 0; j < S.m; ++j) {
-      const double2 q = __ldg(xi + j * S.n + k);
-      const double wx = (x - q.x) / S.a, wy = (y - q.y) / S.b;
-      rmin = fmin(rmin, sqrt(wx * wx + wy * wy));
-    }
-    if (S.kind == 0) {
-      const double dv = v - S.v_cruise;
-      cost += dv * dv;
-    } else {
-      const double dv = v - S.v_max, dy = y - S.y_rl;
-      cost += S.w1 * (dv * dv) + S.w2 * (dy * dy);
-    }
-  }
-  hmax = warp_max(hmax);
-  rmin = warp_min(rmin);
-  cost = warp_sum(cost);
-  any_nan = __any_sync(BMPC_FULL, any_nan);
+  };
+  double cost, rmin, hmax;
+  unsigned char f;
+  score_instance(sp, xi, sample, S.res_final[inst], S.res_final[(size_t)S.L + inst],
+                 S.res_final[2 * (size_t)S.L + inst], cost, rmin, hmax, f);
   if (lane == 0) {
-    if (any_nan) hmax = NAN;
-    const double r0 = S.res_final[inst], r1 = S.res_final[(size_t)S.L + inst],
-                 r2 = S.res_final[2 * (size_t)S.L + inst];
-    const double rmax = fmax(r0, fmax(r1, r2));
-    uint8_t f = 0;
-    if (hmax <= S.heading_limit) f |= 1;
-    if (rmax <= S.residual_tol) f |= 2;
-    if (rmin >= S.ratio_min) f |= 4;
     S.meta[inst] = cost;
     S.min_ratio[inst] = rmin;
     S.heading_max[inst] = hmax;
@@ -337,10 +314,10 @@ __global__ void k_argmin(int l, const double* __restrict__ meta, const uint8_t* 
                          long long* best, long long* best_all, long long* best_hc,
                          long long* nfeas) {
   const int s = blockIdx.x;
-  __shared__ double sc[3][256];
-  __shared__ long long si[3][256];
-  __shared__ int scount[256];
-  __shared__ int shc[256];
+  constexpr int kW = 8;  // warps per block (launched with 256 threads)
+  __shared__ double sc[3][kW];
+  __shared__ long long si[3][kW];
+  __shared__ int scount[kW], shc[kW];
   double bc[3] = {INFINITY, INFINITY, INFINITY};
   long long bi[3] = {-1, -1, -1};
   int cnt = 0, cnt_hc = 0;
@@ -356,13 +333,29 @@ __global__ void k_argmin(int l, const double* __restrict__ meta, const uint8_t* 
     if (better(c, i, bc[1], bi[1])) { bc[1] = c; bi[1] = i; }
     if (better(chc, i, bc[2], bi[2])) { bc[2] = chc; bi[2] = i; }
   }
-  for (int q = 0; q < 3; ++q) { sc[q][threadIdx.x] = bc[q]; si[q][threadIdx.x] = bi[q]; }
-  scount[threadIdx.x] = cnt;
-  shc[threadIdx.x] = cnt_hc;
+  // warp tree, then the 8 warp winners (the comparison is order-independent:
+  // lexicographic on (cost, index) with numpy's NaN rule)
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const double oc = __shfl_xor_sync(BMPC_FULL, bc[q], o);
+      const long long oi = __shfl_xor_sync(BMPC_FULL, bi[q], o);
+      if (oi >= 0 && better(oc, oi, bc[q], bi[q])) { bc[q] = oc; bi[q] = oi; }
+    }
+    cnt += __shfl_xor_sync(BMPC_FULL, cnt, o);
+    cnt_hc += __shfl_xor_sync(BMPC_FULL, cnt_hc, o);
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    for (int q = 0; q < 3; ++q) { sc[q][w] = bc[q]; si[q][w] = bi[q]; }
+    scount[w] = cnt;
+    shc[w] = cnt_hc;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     int tot = 0, tot_hc = 0;
-    for (int t = 0; t < (int)blockDim.x; ++t) {
+    for (int t = 0; t < (int)(blockDim.x >> 5); ++t) {
       tot += scount[t];
       tot_hc += shc[t];
       for (int q = 0; q < 3; ++q)

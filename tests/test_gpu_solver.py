@@ -280,3 +280,37 @@ def test_smoke_entry(cuda):
     import __graft_entry__
 
     __graft_entry__.smoke()
+
+
+def test_fused_scoring_equals_standalone(cuda):
+    """bmpc_plan's in-kernel scoring epilogue == bmpc_score on the solved
+    coefficients, bit for bit (same shared code, csrc/score.cuh)."""
+    import ctypes
+
+    from paper_2109_10392_b200 import _native as nat
+    from paper_2109_10392_b200 import device as D
+    from paper_2109_10392_b200.planner import FilterLimits, MetaCostSpec, _spec_struct
+
+    z = golden("c3s")
+    solver = _solver(z)
+    S = _Scenes(z)
+    prob = D.DeviceProblem.from_host(int(z["n"]), S.xi_x, S.xi_y, S.b_xy, S.b_psi, S.l, S.a, S.b,
+                                     S.v_min, S.v_max, S.a_max)
+    spec = _spec_struct(MetaCostSpec("highspeed", v_max=25.0, y_rl=-5.25, w1=1.0, w2=0.1),
+                        FilterLimits())
+    lib, ctx = nat.load(), solver._context()
+    sp = ctypes.c_void_p(D.stream_ptr())
+    dev = prob.b_xy.device
+    sol = D.alloc_solution(solver.basis.n_b, solver.basis.grid.n, prob.L, 40, False, dev)
+    opts = nat.SolveOpts(max_iter=40, tol=0.0)
+    fused = D.alloc_score(prob.L, prob.S, dev)
+    nat.check(lib.bmpc_plan(ctx, ctypes.byref(prob.c_struct()), ctypes.byref(opts),
+                            ctypes.byref(D.solution_struct(sol)), ctypes.byref(spec),
+                            ctypes.byref(D.score_struct(fused)), sp))
+    alone = D.alloc_score(prob.L, prob.S, dev)
+    nat.check(lib.bmpc_score(ctx, ctypes.byref(prob.c_struct()), D.ptr(sol.c_x), D.ptr(sol.c_y),
+                             D.ptr(sol.c_psi), D.ptr(sol.res_final), ctypes.byref(spec),
+                             ctypes.byref(D.score_struct(alone)), sp))
+    for k in ("meta_cost", "min_ratio", "heading_max", "flags", "best_index", "argmin_all",
+              "argmin_hc", "n_feasible"):
+        assert cuda.equal(getattr(fused, k), getattr(alone, k)), k
