@@ -17,6 +17,9 @@ CSRC = PKG / "csrc"
 LIBDIR = PKG / "_lib"
 LIB = LIBDIR / "libbatchmpc_b200.so"
 OBJDIR = ROOT / "build" / "obj"
+# BMPC_VARIANT=prof builds the phase-profiling library (tools/phase_prof.py)
+# next to the product one; it is never loaded by the package itself.
+VARIANTS = {"prof": ["-DBMPC_PHASE_PROF"]}
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
@@ -39,24 +42,28 @@ def _stale(out: Path, deps: list[Path]) -> bool:
     return not out.exists() or any(d.stat().st_mtime > out.stat().st_mtime for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
+def build(force: bool = False, verbose: bool = False, variant: str | None = None) -> Path:
+    variant = variant if variant is not None else os.environ.get("BMPC_VARIANT", "")
+    vflags = VARIANTS[variant] if variant else []
+    lib = LIB.with_name(f"libbatchmpc_b200_{variant}.so") if variant else LIB
+    objdir = OBJDIR.with_name(f"obj_{variant}") if variant else OBJDIR
     LIBDIR.mkdir(parents=True, exist_ok=True)
-    OBJDIR.mkdir(parents=True, exist_ok=True)
+    objdir.mkdir(parents=True, exist_ok=True)
     headers = list(CSRC.glob("*.h")) + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "batchmpc_b200.h"]
     from concurrent.futures import ThreadPoolExecutor
 
     jobs, objs = [], []
     for src, name, extra in UNITS:
         s = CSRC / src
-        o = OBJDIR / (name + ".o")
+        o = objdir / (name + ".o")
         objs.append(o)
         if force or _stale(o, [s, *headers]):
-            jobs.append(([nvcc(), *ARCH, *COMMON, *extra, "-c", str(s), "-o", str(o)], name))
+            jobs.append(([nvcc(), *ARCH, *COMMON, *vflags, *extra, "-c", str(s), "-o", str(o)], name))
 
     def run(job):
         cmd, name = job
         r = subprocess.run(cmd, capture_output=True, text=True)
-        (OBJDIR / (name + ".ptxas.log")).write_text(r.stdout + r.stderr)
+        (objdir / (name + ".ptxas.log")).write_text(r.stdout + r.stderr)
         return name, r
 
     with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
@@ -66,13 +73,13 @@ def build(force: bool = False, verbose: bool = False) -> Path:
                 raise RuntimeError(f"nvcc failed on {name}")
             if verbose:
                 sys.stderr.write(r.stderr)
-    if force or _stale(LIB, objs):
-        cmd = [nvcc(), *ARCH, "-shared", "-o", str(LIB), *map(str, objs)]
+    if force or _stale(lib, objs):
+        cmd = [nvcc(), *ARCH, "-shared", "-o", str(lib), *map(str, objs)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("nvcc link failed")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -7,6 +7,7 @@ is visible, every entry point raises.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from ctypes import POINTER, Structure, c_double, c_int, c_longlong, c_ubyte, c_void_p
 from pathlib import Path
@@ -14,6 +15,8 @@ from pathlib import Path
 import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libbatchmpc_b200.so"
+if os.environ.get("BMPC_LIB"):  # e.g. the phase-profiling build (tools/phase_prof.py)
+    LIB_PATH = Path(os.environ["BMPC_LIB"]).resolve()
 
 BMPC_OK, BMPC_EINVAL, BMPC_ECUDA, BMPC_ESINGULAR = 0, 1, 2, 3
 

@@ -20,7 +20,7 @@ typedef struct {
   const double* Kxa;  // [nb+6][kxs] the per-axis KKT matrix (refinement residual)
   const double* Kpf;  // [nb+4][kps] inverse of the heading KKT matrix
   const double* Kpa;  // [nb+4][kps] the heading KKT matrix
-  const double* M;    // [nb][kms]   F_axis^T F_axis (multiplier step identity)
+  const double* M;    // [2][nb][kms] F_axis^T F_axis, then P^T P (multiplier step identities)
 } bmpc_dev_consts;
 
 enum { BMPC_INIT_COLD = 0, BMPC_INIT_WARM = 1, BMPC_INIT_RESUME = 2 };
@@ -84,5 +84,21 @@ typedef struct {
 } bmpc_score_args;
 
 #ifdef __cplusplus
+}
+#endif
+
+#ifdef __cplusplus
+#ifdef __CUDACC__
+#define BMPC_HD __host__ __device__
+#else
+#define BMPC_HD
+#endif
+// Per-warp shared scratch of the persistent kernel (csrc/am_solve_kernel.cuh):
+// 288 doubles of KKT vectors, the per-sample arrays (theta, xdot, ydot and,
+// for npad <= 128, x and y), and the 32 x 33 transpose buffer.
+BMPC_HD constexpr bool bmpc_stores_xy(int npad) { return npad <= 128; }
+BMPC_HD constexpr int bmpc_sample_arrays(int npad) { return bmpc_stores_xy(npad) ? 5 : 3; }
+BMPC_HD constexpr int bmpc_warp_scratch_doubles(int npad) {
+  return 288 + bmpc_sample_arrays(npad) * npad + 32 * 33;
 }
 #endif

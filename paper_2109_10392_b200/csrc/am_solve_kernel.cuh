@@ -33,6 +33,47 @@
 
 namespace bmpc {
 
+// Phase profiling build (-DBMPC_PHASE_PROF, tools/phase_prof.py): lane 0 of
+// every warp adds the clock64 cycles of each kernel phase to a per-unit
+// device counter.  Compiled out of the product library.
+#ifdef BMPC_PHASE_PROF
+static __device__ unsigned long long g_phase_cycles[16];
+__shared__ unsigned long long s_prof[8][16];
+__shared__ long long s_prof_t[8];
+#define BMPC_PROF_DECL                                               \
+  if ((threadIdx.x & 31) == 0) {                                     \
+    for (int _i = 0; _i < 16; ++_i) s_prof[threadIdx.x >> 5][_i] = 0; \
+    s_prof_t[threadIdx.x >> 5] = clock64();                          \
+  }
+#define BMPC_PROF(ph)                                                \
+  do {                                                               \
+    __syncwarp();                                                    \
+    const long long _t = clock64();                                  \
+    if ((threadIdx.x & 31) == 0) {                                   \
+      s_prof[threadIdx.x >> 5][ph] += _t - s_prof_t[threadIdx.x >> 5]; \
+      s_prof_t[threadIdx.x >> 5] = _t;                               \
+    }                                                                \
+  } while (0)
+// lane-0 view without a warp sync (usable in divergent code)
+#define BMPC_PROF_NS(ph)                                             \
+  do {                                                               \
+    const long long _t = clock64();                                  \
+    if ((threadIdx.x & 31) == 0) {                                   \
+      s_prof[threadIdx.x >> 5][ph] += _t - s_prof_t[threadIdx.x >> 5]; \
+      s_prof_t[threadIdx.x >> 5] = _t;                               \
+    }                                                                \
+  } while (0)
+#define BMPC_PROF_FLUSH                                               \
+  if ((threadIdx.x & 31) == 0)                                        \
+    for (int _i = 0; _i < 16; ++_i)                                   \
+      atomicAdd(&g_phase_cycles[_i], s_prof[threadIdx.x >> 5][_i]);
+#else
+#define BMPC_PROF_DECL
+#define BMPC_PROF(ph) do {} while (0)
+#define BMPC_PROF_NS(ph) do {} while (0)
+#define BMPC_PROF_FLUSH
+#endif
+
 struct WarpScratch {
   double* bc;    // 64: KKT right-hand sides (x at 0, y at 32)
   double* sol;   // 64: [c; mu] of the xy QP, kept across sweeps (x at 0, y at 32)
@@ -40,9 +81,11 @@ struct WarpScratch {
   double* cxy;   // 32: (c_x[i], c_y[i]) pairs
   double* cp;    // 16: c_psi
   double* solp;  // 32: [c_psi; mu_psi], kept across sweeps
-  double* th;    // npad: theta (unwrapped heading target) per sample
-  double* xd;    // npad: xdot per sample (phase 2 -> phase 4)
+  double* th;    // npad: theta per sample (read back only by the unwrap slow path)
+  double* xd;    // npad: xdot per sample (pass A -> pass B)
   double* yd;    // npad: ydot per sample
+  double* x;     // npad: x per sample (pass A -> obstacle block), if stored
+  double* y;     // npad: y per sample
   double* red;   // 32 x kRedStride: transpose buffer of the sample contractions
 };
 constexpr int kWarpScratch = 288;
@@ -129,51 +172,47 @@ __device__ __forceinline__ double kkt_row_dot(const double* __restrict__ kr,
   return (s[0] + s[1]) + (s[2] + s[3]);
 }
 
-// Obstacle block of the fused tail for one (obstacle, sample) element
-// (_speedups.pyx:150-176): closed-form d, residual and next target, summed
-// over obstacles into the per-sample accumulators.  rsqrt-and-multiply replaces
-// sqrt and the three divisions (SURVEY.md finding 8).
-__device__ __forceinline__ void obstacle_term(double x, double y, double2 q, double a, double b,
-                                              double inv_ab, double& gsx, double& gsy,
-                                              double& sq) {
+// Exact form of the same closed forms (fp64 path): outside the ellipse
+// (d = r/(ab) > 1) g_j = q + (a d cos, b d sin) = q + w = x and r_j = 0
+// identically, so a term needs only the outside test; inside (d = 1)
+// g_j = q + (a cos, b sin), r_j = w - (a cos, b sin).  On the BASELINE scenes
+// about 1% of lane groups hold an inside term.  NaN distances test
+// as inside, so they propagate like the reference's.
+__device__ __forceinline__ bool obstacle_inside(double x, double y, double2 q, double a, double b,
+                                                double ab2) {
+  const double px = b * (x - q.x), py = a * (y - q.y);
+  return !(fma(px, px, py * py) >= ab2);
+}
+__device__ __forceinline__ void obstacle_inside_term(double x, double y, double2 q, double a,
+                                                     double b, double& gix, double& giy,
+                                                     double& sq, double& cin) {
   const double wx = x - q.x, wy = y - q.y;
   const double px = b * wx, py = a * wy;
   const double r2 = fma(px, px, py * py);
   const double ri = rsqrt_nb(r2);
-  // r = 0 -> (cos, sin) = (1, 0), d = 1 (_speedups.pyx:158-166); py = 0 there
-  const double ca = r2 > 0.0 ? px * ri : 1.0;
-  const double sa = py * ri;
-  double dd = (r2 * ri) * inv_ab;
-  dd = dd < 1.0 ? 1.0 : dd;
-  const double adca = (a * dd) * ca, bdsa = (b * dd) * sa;
-  const double rx = wx - adca, ry = wy - bdsa;
+  // r = 0 -> (cos, sin) = (1, 0) (_speedups.pyx:158-166); py = 0 there
+  const double ca = r2 > 0.0 ? px * ri : 1.0, sa = py * ri;
+  const double ax = a * ca, by = b * sa;
+  const double rx = wx - ax, ry = wy - by;
   sq = fma(rx, rx, fma(ry, ry, sq));
-  gsx += q.x + adca;
-  gsy += q.y + bdsa;
+  gix += q.x + ax;
+  giy += q.y + by;
+  cin += 1.0;
 }
 
-// Two sample slots per pass when the accumulators leave register room.
+// Two sample slots per obstacle pass when the accumulators leave register room.
 template <int NB>
 constexpr bool kPairSlots = NB <= 12;
 
 struct TailArgs {
-  const double *P, *Pd, *Pdd;
+  const double* P;
   const double2* cxy;
-  const double* cp;
   const double2* xi;
-  double *th, *xd, *yd;
+  const double *xs, *ys;  // sampled positions (pass A) or nullptr: recompute from c
   int n, m;
-  double a, b, inv_ab, a_max, v_min, v_max;
-  double* v_out;
-  size_t L;
-  int inst;
+  double a, b, inv_ab;
 };
 
-// Fused tail (kernels/_speedups.pyx:114-218) for NS samples of one lane, with
-// the contractions onto the basis accumulated on the fly.  Obstacles j0, j0+js,
-// ...; `group` > 1 marks a split slot whose obstacle partials are summed over
-// `group` consecutive lanes (warp-uniform).  Accumulation order per sample
-// and across samples is the order of the sample list.
 // fp32 mode obstacle term.  In exact arithmetic the reference's closed forms
 // give r = w - a d (cos, sin) = 0 and g = x whenever the sample is outside the
 // ellipse (d = r/(ab) > 1), and d = 1 inside; so only inside terms carry a
@@ -196,32 +235,41 @@ __device__ __forceinline__ void obstacle_term_f32(double x, double y, double2 q,
   sry += ry;
 }
 
+// Obstacle block of the fused tail (kernels/_speedups.pyx:150-176) for NS
+// samples of one lane: sum_j g_obs,j contracted onto P on the fly, and the
+// squared residual.  Obstacles j0, j0+js, ...; `group` > 1 marks a split slot
+// whose obstacle partials are summed over `group` consecutive lanes
+// (warp-uniform) before the group leader contracts them.  The acceleration
+// and non-holonomic blocks run in passes A and B of the sweep.
 template <int NS, int NB, int NPAD, bool F32>
-__device__ __forceinline__ void tail_block(const TailArgs& T, const int (&k)[NS], int j0, int js,
-                                           int group, bool valid, bool leader, double (&Gx)[NB],
-                                           double (&Gy)[NB], double& sqo, double& sqa,
-                                           double& sqn) {
-  double x[NS], y[NS], xdd[NS], ydd[NS], ps[NS], gsx[NS], gsy[NS], sq[NS];
+__device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)[NS], int j0, int js,
+                                               int group, bool valid, bool leader,
+                                               double (&Gx)[NB], double (&Gy)[NB], double& sqo) {
+  double x[NS], y[NS], gsx[NS], gsy[NS], sq[NS];
 #pragma unroll
-  for (int s = 0; s < NS; ++s) x[s] = y[s] = xdd[s] = ydd[s] = ps[s] = gsx[s] = gsy[s] = sq[s] = 0.0;
+  for (int s = 0; s < NS; ++s) x[s] = y[s] = gsx[s] = gsy[s] = sq[s] = 0.0;
   if (valid) {
-#pragma unroll
-    for (int i = 0; i < NB; ++i) {
-      const double2 c = T.cxy[i];
-      const double cpi = T.cp[i];
+    if (T.xs) {
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
-        const double p = T.P[i * NPAD + k[s]], pdd = T.Pdd[i * NPAD + k[s]];
-        x[s] = fma(p, c.x, x[s]);
-        y[s] = fma(p, c.y, y[s]);
-        xdd[s] = fma(pdd, c.x, xdd[s]);
-        ydd[s] = fma(pdd, c.y, ydd[s]);
-        ps[s] = fma(p, cpi, ps[s]);
+        x[s] = T.xs[k[s]];
+        y[s] = T.ys[k[s]];
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        const double2 c = T.cxy[i];
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          const double p = T.P[i * NPAD + k[s]];
+          x[s] = fma(p, c.x, x[s]);
+          y[s] = fma(p, c.y, y[s]);
+        }
       }
     }
-    // obstacle block (_speedups.pyx:150-176), summed over this lane's obstacles
+    BMPC_PROF_NS(10);
     const int qstep = js * T.n;
-    constexpr int U = F32 ? 4 : (NS == 1 ? 4 : 2);  // independent terms in flight per sample
+    constexpr int U = (F32 || NS == 1) ? 4 : 2;  // obstacles in flight per sample
     const double2* qp[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) qp[s] = T.xi + j0 * T.n + k[s];
@@ -229,6 +277,10 @@ __device__ __forceinline__ void tail_block(const TailArgs& T, const int (&k)[NS]
 #pragma unroll
     for (int s = 0; s < NS; ++s) srx[s] = sry[s] = sqf[s] = 0.f;
     const float af = (float)T.a, bf = (float)T.b, ab2 = (float)(T.a * T.b * T.a * T.b);
+    const double abd2 = (T.a * T.b) * (T.a * T.b);
+    double cin[NS];  // fp64 mode: inside terms per sample
+#pragma unroll
+    for (int s = 0; s < NS; ++s) cin[s] = 0.0;
     int j = j0;
     // software pipeline: the next group's predictions are in flight while the
     // current group computes (xi comes from L2 once it outgrows L1, e.g. c4)
@@ -251,31 +303,55 @@ __device__ __forceinline__ void tail_block(const TailArgs& T, const int (&k)[NS]
 #pragma unroll
           for (int u = 0; u < U; ++u) qn[s][u] = __ldg(qp[s] + (U + u) * qstep);
       }
+      if constexpr (F32) {
 #pragma unroll
-      for (int u = 0; u < U; ++u)
+        for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int s = 0; s < NS; ++s) {
-          if constexpr (F32)
+          for (int s = 0; s < NS; ++s)
             obstacle_term_f32(x[s], y[s], q[s][u], af, bf, ab2, srx[s], sry[s], sqf[s]);
-          else
-            obstacle_term(x[s], y[s], q[s][u], T.a, T.b, T.inv_ab, gsx[s], gsy[s], sq[s]);
+      } else {
+        bool in[NS][U], any = false;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int s = 0; s < NS; ++s) {
+            in[s][u] = obstacle_inside(x[s], y[s], q[s][u], T.a, T.b, abd2);
+            any |= in[s][u];
+          }
+        if (any) {
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int s = 0; s < NS; ++s)
+              if (in[s][u])
+                obstacle_inside_term(x[s], y[s], q[s][u], T.a, T.b, gsx[s], gsy[s], sq[s], cin[s]);
         }
+      }
 #pragma unroll
       for (int s = 0; s < NS; ++s) qp[s] += U * qstep;
     }
     for (; j < T.m; j += js) {
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
+        const double2 q = __ldg(qp[s]);
         if constexpr (F32)
-          obstacle_term_f32(x[s], y[s], __ldg(qp[s]), af, bf, ab2, srx[s], sry[s], sqf[s]);
-        else
-          obstacle_term(x[s], y[s], __ldg(qp[s]), T.a, T.b, T.inv_ab, gsx[s], gsy[s], sq[s]);
+          obstacle_term_f32(x[s], y[s], q, af, bf, ab2, srx[s], sry[s], sqf[s]);
+        else if (obstacle_inside(x[s], y[s], q, T.a, T.b, abd2))
+          obstacle_inside_term(x[s], y[s], q, T.a, T.b, gsx[s], gsy[s], sq[s], cin[s]);
         qp[s] += qstep;
       }
     }
-    if constexpr (F32) {
+    // terms this lane evaluated per sample (obstacles j0, j0 + js, ...)
+    const double cnt = j0 < T.m ? (double)((T.m - j0 + js - 1) / js) : 0.0;
+    if constexpr (!F32) {
+      // outside terms contribute g_j = x each
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        gsx[s] = fma(cnt - cin[s], x[s], gsx[s]);
+        gsy[s] = fma(cnt - cin[s], y[s], gsy[s]);
+      }
+    } else {
       // g_j = x - r_j exactly, so sum_j g_j = (#obstacles) x - sum_j r_j
-      const double cnt = j0 < T.m ? (double)((T.m - j0 + js - 1) / js) : 0.0;
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
         gsx[s] = fma(cnt, x[s], -(double)srx[s]);
@@ -284,6 +360,7 @@ __device__ __forceinline__ void tail_block(const TailArgs& T, const int (&k)[NS]
       }
     }
   }
+  BMPC_PROF_NS(11);
   if (NS == 1 && group > 1) {  // split slot: combine the group's partial sums
     for (int o = 1; o < group; o <<= 1) {
       gsx[0] += __shfl_xor_sync(BMPC_FULL, gsx[0], o);
@@ -292,77 +369,50 @@ __device__ __forceinline__ void tail_block(const TailArgs& T, const int (&k)[NS]
     }
   }
   if (!(valid && leader)) return;
-  double gax[NS], gay[NS], gnx[NS], gny[NS], sps[NS], cps[NS];
 #pragma unroll
-  for (int s = 0; s < NS; ++s) sincos_nb(ps[s], &sps[s], &cps[s]);
-#pragma unroll
-  for (int s = 0; s < NS; ++s)  // huge / non-finite headings: CUDA's full-range sincos
-    if (!(fabs(ps[s]) < 1.0e5)) sincos(ps[s], &sps[s], &cps[s]);
-#pragma unroll
-  for (int s = 0; s < NS; ++s) {
-    sqo += sq[s];
-    // acceleration block (_speedups.pyx:179-198)
-    const double m2 = fma(xdd[s], xdd[s], ydd[s] * ydd[s]);
-    const double mi = rsqrt_nb(m2);
-    const double caa = m2 > 0.0 ? xdd[s] * mi : 1.0, saa = ydd[s] * mi;
-    const double mag = m2 * mi;
-    const double da = mag < T.a_max ? mag : T.a_max;
-    gax[s] = da * caa;
-    gay[s] = da * saa;
-    const double rax = xdd[s] - gax[s], ray = ydd[s] - gay[s];
-    sqa = fma(rax, rax, fma(ray, ray, sqa));
-    // non-holonomic block (_speedups.pyx:200-216)
-    const double xd = T.xd[k[s]], yd = T.yd[k[s]];
-    const double s2 = fma(xd, xd, yd * yd);
-    double v = s2 * rsqrt_nb(s2);
-    v = v < T.v_min ? T.v_min : (v > T.v_max ? T.v_max : v);
-    gnx[s] = v * cps[s];
-    gny[s] = v * sps[s];
-    const double rnx = xd - gnx[s], rny = yd - gny[s];
-    sqn = fma(rnx, rnx, fma(rny, rny, sqn));
-    if (T.v_out) T.v_out[(size_t)k[s] * T.L + T.inst] = v;
-    T.th[k[s]] = ps[s] - T.th[k[s]];  // psi - theta, contracted later (solver.py:494)
-  }
+  for (int s = 0; s < NS; ++s) sqo += sq[s];
 #pragma unroll
   for (int i = 0; i < NB; ++i) {
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
-      const double p = T.P[i * NPAD + k[s]], pd = T.Pd[i * NPAD + k[s]], pdd = T.Pdd[i * NPAD + k[s]];
+      const double p = T.P[i * NPAD + k[s]];
       Gx[i] = fma(p, gsx[s], Gx[i]);
-      Gx[i] = fma(pdd, gax[s], Gx[i]);
-      Gx[i] = fma(pd, gnx[s], Gx[i]);
       Gy[i] = fma(p, gsy[s], Gy[i]);
-      Gy[i] = fma(pdd, gay[s], Gy[i]);
-      Gy[i] = fma(pd, gny[s], Gy[i]);
     }
   }
+  BMPC_PROF_NS(13);
 }
 
 template <int NB, int NKM, bool F32>
-__global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
+__global__ void __launch_bounds__(256, 1) am_solve_kernel(const bmpc_dev_consts C,
                                                        const bmpc_solve_args A) {
   extern __shared__ __align__(16) double sm[];
   const int W = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  BMPC_PROF_DECL
   const int n = C.n;
   constexpr int npad = 32 * NKM;  // host pads the basis to exactly this
   constexpr int nk = NKM;
   const int L = A.L;
   constexpr int RX = NB + 6, RP = NB + 4;
 
+  constexpr bool kStoreXY = bmpc_stores_xy(npad);  // else the obstacle block re-evaluates x, y
+  constexpr int CH = NKM < 4 ? NKM : 4;              // sample slots per pass A / B chunk
   double* sPT = sm;                          // P^T, Pdot^T, Pddot^T
   double* sKxf = sPT + 3 * NB * npad;
   double* sKxa = sKxf + RX * C.kxs;
   double* sKpf = sKxa + RX * C.kxs;
   double* sKpa = sKpf + RP * C.kps;
   double* sM = sKpa + RP * C.kps;   // F_axis^T F_axis (lambda identity)
-  double* sTau = sM + ((NB * C.kms + 1) & ~1);  // keep the double2 scratch 16-byte aligned
-  double* wbase = sTau + npad + warp * (kWarpScratch + 3 * npad + kRedSize);
-  WarpScratch ws{wbase,       wbase + 64,   wbase + 128,
-                 wbase + 192, wbase + 224,  wbase + 256, wbase + kWarpScratch,
-                 wbase + kWarpScratch + npad, wbase + kWarpScratch + 2 * npad,
-                 wbase + kWarpScratch + 3 * npad};
+  double* sMp = sM + NB * C.kms;    // P^T P (lambda_psi identity)
+  double* sTau = sM + ((2 * NB * C.kms + 1) & ~1);  // keep the double2 scratch 16-byte aligned
+  double* wbase = sTau + npad + warp * bmpc_warp_scratch_doubles(npad);
+  double* arr = wbase + kWarpScratch;
+  WarpScratch ws{wbase,       wbase + 64,   wbase + 128, wbase + 192, wbase + 224, wbase + 256,
+                 arr,         arr + npad,   arr + 2 * npad,
+                 kStoreXY ? arr + 3 * npad : nullptr, kStoreXY ? arr + 4 * npad : nullptr,
+                 arr + bmpc_sample_arrays(npad) * npad};
   const SlotLayout sl = slot_layout(n);
   const int nslots = sl.F + (sl.R > 0 ? 1 : 0);
 
@@ -375,7 +425,7 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
     sKpf[t] = C.Kpf[t];
     sKpa[t] = C.Kpa[t];
   }
-  for (int t = threadIdx.x; t < NB * C.kms; t += blockDim.x) sM[t] = C.M[t];
+  for (int t = threadIdx.x; t < 2 * NB * C.kms; t += blockDim.x) sM[t] = C.M[t];  // M, then P^T P
   for (int t = threadIdx.x; t < npad; t += blockDim.x) sTau[t] = C.tau[t];
   __syncthreads();
 
@@ -514,6 +564,7 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
     }
     G = reduce_scatter32(v32);
   }
+  BMPC_PROF(0);
 
   // ----------------------------------------------------------- AM sweeps ----
   for (int t = 0; t < A.iters; ++t) {
@@ -563,79 +614,114 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
       __syncwarp();
       if (owner) cown = ws.cxy[2 * li + (yax ? 1 : 0)];
     }
+    BMPC_PROF(1);
     const double2* __restrict__ cxy = reinterpret_cast<const double2*>(ws.cxy);
 
-    // (2) heading target theta = unwrap(atan2(ydot, xdot)) and P^T theta.
-    //     Slot r < F: sample lane + 32 r.  Leftover slot (n % 32 samples): split
-    //     mode gives each sample a group of g lanes that share its obstacles.
+    // (2) pass A over every sample (lane + 32 r), CH slots at a time: x, y,
+    //     xdot, ydot, xddot, yddot from c; theta = atan2(ydot, xdot) with the
+    //     unwrap test against the previous sample done in registers; the
+    //     acceleration block (_speedups.pyx:179-198), which needs no psi, and the
+    //     contractions P^T theta and Pddot^T g_acc.
+    double Gx[NB], Gy[NB], pt[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) Gx[i] = Gy[i] = pt[i] = 0.0;
+    double sqo = 0.0, sqa = 0.0, sqn = 0.0;
     {
-      int r = 0;
-#pragma unroll 1
-      for (; r + 1 < sl.F; r += 2) {  // two full slots per pass
-        const int k0 = lane + 32 * r, k1 = k0 + 32;
-        double xd0 = 0.0, yd0 = 0.0, xd1 = 0.0, yd1 = 0.0;
+      bool wrap = false;
+      double prev_last = 0.0;  // theta of sample 32 r - 1: lane 31 of the previous slot
+#pragma unroll
+      for (int r0 = 0; r0 < NKM; r0 += CH) {
+        int k[CH];
+        bool v[CH];
+        double xx[CH], yy[CH], xd[CH], yd[CH], xdd[CH], ydd[CH];
+#pragma unroll
+        for (int s = 0; s < CH; ++s) {
+          k[s] = lane + 32 * (r0 + s < NKM ? r0 + s : 0);
+          v[s] = r0 + s < NKM && k[s] < n;
+          xx[s] = yy[s] = xd[s] = yd[s] = xdd[s] = ydd[s] = 0.0;
+        }
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
-          const double pd0 = sPd[i * npad + k0], pd1 = sPd[i * npad + k1];
           const double2 c = cxy[i];
-          xd0 = fma(pd0, c.x, xd0);
-          yd0 = fma(pd0, c.y, yd0);
-          xd1 = fma(pd1, c.x, xd1);
-          yd1 = fma(pd1, c.y, yd1);
-        }
-        ws.th[k0] = atan2_nb(yd0, xd0);
-        ws.th[k1] = atan2_nb(yd1, xd1);
-        ws.xd[k0] = xd0;
-        ws.yd[k0] = yd0;
-        ws.xd[k1] = xd1;
-        ws.yd[k1] = yd1;
-      }
-#pragma unroll 1
-      for (; r < nslots; ++r) {
-        const Slot S = slot(r, lane, sl);
-        if (S.valid && S.leader) {
-          double xd = 0.0, yd = 0.0;
 #pragma unroll
-          for (int i = 0; i < NB; ++i) {
-            const double pd = sPd[i * npad + S.k];
-            const double2 c = cxy[i];
-            xd = fma(pd, c.x, xd);
-            yd = fma(pd, c.y, yd);
+          for (int s = 0; s < CH; ++s) {
+            if (r0 + s >= NKM) continue;
+            const double p = sP[i * npad + k[s]], pd = sPd[i * npad + k[s]],
+                         pdd = sPdd[i * npad + k[s]];
+            xx[s] = fma(p, c.x, xx[s]);
+            yy[s] = fma(p, c.y, yy[s]);
+            xd[s] = fma(pd, c.x, xd[s]);
+            yd[s] = fma(pd, c.y, yd[s]);
+            xdd[s] = fma(pdd, c.x, xdd[s]);
+            ydd[s] = fma(pdd, c.y, ydd[s]);
           }
-          ws.th[S.k] = atan2_nb(yd, xd);
-          ws.xd[S.k] = xd;
-          ws.yd[S.k] = yd;
+        }
+        double th[CH], gax[CH], gay[CH];
+#pragma unroll
+        for (int s = 0; s < CH; ++s) {
+          if (r0 + s >= NKM) continue;
+          th[s] = atan2_nb(yd[s], xd[s]);
+          double prev = __shfl_up_sync(BMPC_FULL, th[s], 1);
+          const double last = __shfl_sync(BMPC_FULL, th[s], 31);
+          if (lane == 0) prev = prev_last;
+          prev_last = last;
+          if (v[s] && k[s] > 0 && !(fabs(th[s] - prev) < CUDART_PI)) wrap = true;
+          if (v[s]) {
+            ws.th[k[s]] = th[s];
+            ws.xd[k[s]] = xd[s];
+            ws.yd[k[s]] = yd[s];
+            if constexpr (kStoreXY) {
+              ws.x[k[s]] = xx[s];
+              ws.y[k[s]] = yy[s];
+            }
+          }
+          // acceleration block (_speedups.pyx:179-198)
+          const double m2 = fma(xdd[s], xdd[s], ydd[s] * ydd[s]);
+          const double mi = rsqrt_nb(m2);
+          const double caa = m2 > 0.0 ? xdd[s] * mi : 1.0, saa = ydd[s] * mi;
+          const double mag = m2 * mi;
+          const double da = mag < A.a_max ? mag : A.a_max;
+          gax[s] = v[s] ? da * caa : 0.0;
+          gay[s] = v[s] ? da * saa : 0.0;
+          if (v[s]) {
+            const double rax = xdd[s] - gax[s], ray = ydd[s] - gay[s];
+            sqa = fma(rax, rax, fma(ray, ray, sqa));
+          } else {
+            th[s] = 0.0;
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+#pragma unroll
+          for (int s = 0; s < CH; ++s) {
+            if (r0 + s >= NKM) continue;
+            const double p = sP[i * npad + k[s]], pdd = sPdd[i * npad + k[s]];
+            pt[i] = fma(p, th[s], pt[i]);
+            Gx[i] = fma(pdd, gax[s], Gx[i]);
+            Gy[i] = fma(pdd, gay[s], Gy[i]);
+          }
         }
       }
-    }
-    __syncwarp();
-    bool wrap = false;
-#pragma unroll 1
-    for (int r = 0; r < nslots; ++r) {
-      const Slot S = slot(r, lane, sl);
-      if (S.valid && S.leader && S.k > 0) {
-        const double dd = ws.th[S.k] - ws.th[S.k - 1];
-        if (!(fabs(dd) < CUDART_PI)) wrap = true;
+      BMPC_PROF(2);
+      if (__any_sync(BMPC_FULL, wrap)) {  // rare: exact numpy unwrap, then P^T theta again
+        __syncwarp();
+        if (lane == 0) np_unwrap_serial(ws.th, n);
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < NB; ++i) pt[i] = 0.0;
+#pragma unroll
+        for (int r = 0; r < NKM; ++r) {
+          const int k = lane + 32 * r;
+          if (k < n) {
+            const double t = ws.th[k];
+#pragma unroll
+            for (int i = 0; i < NB; ++i) pt[i] = fma(sP[i * npad + k], t, pt[i]);
+          }
+        }
       }
-    }
-    if (__any_sync(BMPC_FULL, wrap)) {
-      if (lane == 0) np_unwrap_serial(ws.th, n);
-      __syncwarp();
     }
     double pth;
     {
-      double pt[NB];
-#pragma unroll
-      for (int i = 0; i < NB; ++i) pt[i] = 0.0;
-#pragma unroll 1
-      for (int r = 0; r < nslots; ++r) {
-        const Slot S = slot(r, lane, sl);
-        if (S.valid && S.leader) {
-          const double th = ws.th[S.k];
-#pragma unroll
-          for (int i = 0; i < NB; ++i) pt[i] = fma(sP[i * npad + S.k], th, pt[i]);
-        }
-      }
 #pragma unroll
       for (int i = 0; i < NB; ++i) ws.red[lane * kRedStride + i] = pt[i];
       __syncwarp();
@@ -643,6 +729,7 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
       __syncwarp();
     }
 
+    BMPC_PROF(3);
     // (3) psi QP
     {
       if (!yax && owner) ws.bc[li] = rho * pth + lamp;
@@ -662,15 +749,91 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
       __syncwarp();
       if (!yax && owner) cpown = ws.cp[li];
     }
-
-    // (4) fused tail + on-the-fly contractions
-    double Gx[NB], Gy[NB];
+    // lambda_psi step P^T (psi - theta) = (P^T P) c_psi - P^T theta (solver.py:494)
+    double Lp = 0.0;
+    if (!yax && owner) {
+      const double* mr = sMp + li * C.kms;
+      double s4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int i = 0; i < NB; ++i) { Gx[i] = Gy[i] = 0.0; }
-    double sqo = 0.0, sqa = 0.0, sqn = 0.0;
-    TailArgs T{sP, sPd, sPdd, cxy, ws.cp, xi, ws.th, ws.xd, ws.yd, n, m, a, b, inv_ab,
-               A.a_max, A.v_min, A.v_max, (last && (A.flags & BMPC_F_V)) ? A.v_out : nullptr,
-               (size_t)L, inst};
+      for (int j = 0; j < NB; ++j) s4[j & 3] = fma(mr[j], ws.cp[j], s4[j & 3]);
+      Lp = ((s4[0] + s4[1]) + (s4[2] + s4[3])) - pth;
+    }
+
+    BMPC_PROF(4);
+    // (4) pass B: psi = P c_psi and the non-holonomic block (_speedups.pyx:200-216),
+    //     contracted onto Pdot.
+#pragma unroll
+    for (int r0 = 0; r0 < NKM; r0 += CH) {
+      int k[CH];
+      bool v[CH];
+      double ps[CH];
+#pragma unroll
+      for (int s = 0; s < CH; ++s) {
+        k[s] = lane + 32 * (r0 + s < NKM ? r0 + s : 0);
+        v[s] = r0 + s < NKM && k[s] < n;
+        ps[s] = 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        const double cpi = ws.cp[i];
+#pragma unroll
+        for (int s = 0; s < CH; ++s)
+          if (r0 + s < NKM) ps[s] = fma(sP[i * npad + k[s]], cpi, ps[s]);
+      }
+      // branch-free sin/cos for every slot first, so the slots interleave; the
+      // full-range fallback (huge / non-finite headings) is one rare branch
+      double sps[CH], cps[CH];
+      bool big = false;
+#pragma unroll
+      for (int s = 0; s < CH; ++s) {
+        sps[s] = 0.0;
+        cps[s] = 1.0;
+        if (r0 + s >= NKM) continue;
+        sincos_nb(ps[s], &sps[s], &cps[s]);
+        big |= !(fabs(ps[s]) < 1.0e5);
+      }
+      if (big) {
+#pragma unroll
+        for (int s = 0; s < CH; ++s)
+          if (r0 + s < NKM && !(fabs(ps[s]) < 1.0e5)) sincos(ps[s], &sps[s], &cps[s]);
+      }
+      double gnx[CH], gny[CH], vv[CH];
+#pragma unroll
+      for (int s = 0; s < CH; ++s) {
+        gnx[s] = gny[s] = vv[s] = 0.0;
+        if (r0 + s >= NKM) continue;
+        const double xd = v[s] ? ws.xd[k[s]] : 0.0, yd = v[s] ? ws.yd[k[s]] : 0.0;
+        const double s2 = fma(xd, xd, yd * yd);
+        double u = s2 * rsqrt_nb(s2);
+        u = u < A.v_min ? A.v_min : (u > A.v_max ? A.v_max : u);
+        vv[s] = u;
+        gnx[s] = v[s] ? u * cps[s] : 0.0;
+        gny[s] = v[s] ? u * sps[s] : 0.0;
+        const double rnx = xd - gnx[s], rny = yd - gny[s];
+        const double q = fma(rnx, rnx, fma(rny, rny, sqn));
+        sqn = v[s] ? q : sqn;
+      }
+      if (last && (A.flags & BMPC_F_V)) {
+#pragma unroll
+        for (int s = 0; s < CH; ++s)
+          if (v[s]) A.v_out[(size_t)k[s] * L + inst] = vv[s];
+      }
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+#pragma unroll
+        for (int s = 0; s < CH; ++s) {
+          if (r0 + s >= NKM) continue;
+          const double pd = sPd[i * npad + k[s]];
+          Gx[i] = fma(pd, gnx[s], Gx[i]);
+          Gy[i] = fma(pd, gny[s], Gy[i]);
+        }
+      }
+    }
+
+    BMPC_PROF(12);
+    // (5) obstacle block, samples dealt as in slot(): full slots two at a time,
+    //     the n % 32 leftover samples split over lane groups.
+    TailArgs T{sP, cxy, xi, kStoreXY ? ws.x : nullptr, kStoreXY ? ws.y : nullptr, n, m, a, b, inv_ab};
     int r = 0;
     if (kPairSlots<NB>) {
       // two full sample slots per pass: twice the independent work in flight,
@@ -678,18 +841,19 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
 #pragma unroll 1
       for (; r + 1 < sl.F; r += 2) {
         const int ks[2] = {lane + 32 * r, lane + 32 * (r + 1)};
-        tail_block<2, NB, npad, F32>(T, ks, 0, 1, 0, true, true, Gx, Gy, sqo, sqa, sqn);
+        obstacle_block<2, NB, npad, F32>(T, ks, 0, 1, 0, true, true, Gx, Gy, sqo);
       }
     }
 #pragma unroll 1
     for (; r < nslots; ++r) {
       const Slot S = slot(r, lane, sl);
       const int ks[1] = {S.k};
-      tail_block<1, NB, npad, F32>(T, ks, S.j0, S.js, (r == sl.F) ? sl.g : 1, S.valid, S.leader, Gx, Gy,
-                              sqo, sqa, sqn);
+      obstacle_block<1, NB, npad, F32>(T, ks, S.j0, S.js, (r == sl.F) ? sl.g : 1, S.valid, S.leader,
+                                       Gx, Gy, sqo);
     }
-    // warp contractions over the samples -> owner lanes (shared-memory transpose,
-    // fixed summation order)
+    BMPC_PROF(5);
+    // G = F_axis^T g: shared-memory transpose of the lane partials, fixed
+    // summation order; residual sums by xor butterflies (identical on all lanes)
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
       ws.red[lane * kRedStride + i] = Gx[i];
@@ -697,50 +861,31 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
     }
     __syncwarp();
     G = owner ? column_sum(ws.red, lane) : 0.0;
+    sqo = warp_sum(sqo);
+    sqa = warp_sum(sqa);
+    sqn = warp_sum(sqn);
     __syncwarp();
+    BMPC_PROF(6);
     // lambda step F_axis^T r = F_axis^T (F_axis c - g) = (F_axis^T F_axis) c - G:
     // the residual vectors never need their own contraction
-    double R = 0.0;
     if (owner) {
       const double* mr = sM + li * C.kms;
       double s4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int j = 0; j < NB; ++j) s4[j & 3] = fma(mr[j], ws.cxy[2 * j + (yax ? 1 : 0)], s4[j & 3]);
-      R = ((s4[0] + s4[1]) + (s4[2] + s4[3])) - G;
+      const double R = ((s4[0] + s4[1]) + (s4[2] + s4[3])) - G;
+      lam -= rho * R;
     }
-    {
-      double Lp[NB];
-#pragma unroll
-      for (int i = 0; i < NB; ++i) Lp[i] = 0.0;
-#pragma unroll 1
-      for (int r = 0; r < nslots; ++r) {
-        const Slot S = slot(r, lane, sl);
-        if (S.valid && S.leader) {
-          const double dpt = ws.th[S.k];
-#pragma unroll
-          for (int i = 0; i < NB; ++i) Lp[i] = fma(sP[i * npad + S.k], dpt, Lp[i]);
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < NB; ++i) ws.red[lane * kRedStride + i] = Lp[i];
-    }
-    ws.red[lane * kRedStride + 16] = sqo;
-    ws.red[lane * kRedStride + 17] = sqa;
-    ws.red[lane * kRedStride + 18] = sqn;
-    __syncwarp();
-    const double q3 = ((!yax && owner) || (lane >= 16 && lane < 19)) ? column_sum(ws.red, lane) : 0.0;
-    __syncwarp();
-    if (owner) lam -= rho * R;
-    if (!yax && owner) lamp -= rho * q3;
+    if (!yax && owner) lamp -= rho * Lp;
     if (lane >= 16 && lane < 19) {
-      const double res = sqrt(q3);
+      const double res = sqrt(lane == 16 ? sqo : (lane == 17 ? sqa : sqn));
       if (A.flags & BMPC_F_HISTORY)
         A.hist[((size_t)(A.hist_offset + t) * 3 + (lane - 16)) * L + inst] = res;
       if (last && A.res_final) A.res_final[(size_t)(lane - 16) * L + inst] = res;
       if (last) ws.res[60 + lane - 16] = res;  // for the fused scoring below
     }
     have_sol = true;
-    __syncwarp();
+    BMPC_PROF(7);
   }
 
   // ------------------------------------------------- fused planner scoring ----
@@ -773,6 +918,7 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
       F.flags[inst] = f;
     }
   }
+  BMPC_PROF(8);
 
   // ------------------------------------------------------------- outputs ----
   if (owner) {
@@ -802,6 +948,8 @@ __global__ void __launch_bounds__(256) am_solve_kernel(const bmpc_dev_consts C,
     }
     if (lane < RP) cr[5 * NB + 2 * RX + lane] = ws.solp[lane];
   }
+  BMPC_PROF(9);
+  BMPC_PROF_FLUSH
 }
 
 }  // namespace bmpc

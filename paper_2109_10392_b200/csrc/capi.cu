@@ -136,7 +136,7 @@ int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pd
   const int npad = n <= 64 ? 64 : (n <= 128 ? 128 : (n <= 224 ? 224 : 256));
   const int kxs = rx | 1, kps = rp | 1, kms = nb | 1;
   const size_t nPT = (size_t)3 * nb * npad, nKx = (size_t)rx * kxs, nKp = (size_t)rp * kps;
-  std::vector<double> h(nPT + 2 * nKx + 2 * nKp + (size_t)nb * kms + npad, 0.0);
+  std::vector<double> h(nPT + 2 * nKx + 2 * nKp + 2 * (size_t)nb * kms + npad, 0.0);
   const double* mats[3] = {P, Pdot, Pddot};
   for (int q = 0; q < 3; ++q)
     for (int i = 0; i < nb; ++i)
@@ -151,6 +151,14 @@ int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pd
       for (int j = 0; j < dims[q]; ++j) h[o + (size_t)i * strides[q] + j] = blocks[q][(size_t)i * dims[q] + j];
     o += (size_t)dims[q] * strides[q];
   }
+  // P^T P right after M (the lambda_psi identity), accumulated in extended precision
+  for (int i = 0; i < nb; ++i)
+    for (int j = 0; j < nb; ++j) {
+      long double acc = 0.0L;
+      for (int k = 0; k < n; ++k) acc += (long double)P[(size_t)k * nb + i] * P[(size_t)k * nb + j];
+      h[o + (size_t)i * kms + j] = (double)acc;
+    }
+  o += (size_t)nb * kms;
   for (int k = 0; k < n; ++k) h[o + k] = tau[k];
   bmpc_ctx* c = new bmpc_ctx();
   cudaError_t e = cudaMalloc(&c->dmem, h.size() * sizeof(double));
