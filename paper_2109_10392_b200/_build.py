@@ -44,7 +44,7 @@ def _stale(out: Path, deps: list[Path]) -> bool:
 
 def build(force: bool = False, verbose: bool = False, variant: str | None = None) -> Path:
     variant = variant if variant is not None else os.environ.get("BMPC_VARIANT", "")
-    vflags = VARIANTS[variant] if variant else []
+    vflags = (VARIANTS.get(variant, []) + os.environ.get("BMPC_VARIANT_FLAGS", "").split()) if variant else []
     lib = LIB.with_name(f"libbatchmpc_b200_{variant}.so") if variant else LIB
     objdir = OBJDIR.with_name(f"obj_{variant}") if variant else OBJDIR
     LIBDIR.mkdir(parents=True, exist_ok=True)

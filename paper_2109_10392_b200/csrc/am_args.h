@@ -21,6 +21,8 @@ typedef struct {
   const double* Kpf;  // [nb+4][kps] inverse of the heading KKT matrix
   const double* Kpa;  // [nb+4][kps] the heading KKT matrix
   const double* M;    // [2][nb][kms] F_axis^T F_axis, then P^T P (multiplier step identities)
+  int const_doubles;  // size of the whole constant image starting at PT (even; the
+                      // kernel's shared-memory layout, copied in one bulk transfer)
 } bmpc_dev_consts;
 
 enum { BMPC_INIT_COLD = 0, BMPC_INIT_WARM = 1, BMPC_INIT_RESUME = 2 };

@@ -74,6 +74,35 @@ __shared__ long long s_prof_t[8];
 #define BMPC_PROF_FLUSH
 #endif
 
+// mbarrier + 1-D bulk asynchronous copy (TMA engine) helpers.
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, unsigned bytes,
+                                              unsigned long long* bar) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+      "l"(src), "r"(bytes), "r"(b)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(unsigned long long* bar, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT%=;\n}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
 struct WarpScratch {
   double* bc;    // 64: KKT right-hand sides (x at 0, y at 32)
   double* sol;   // 64: [c; mu] of the xy QP, kept across sweeps (x at 0, y at 32)
@@ -384,7 +413,13 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
 }
 
 template <int NB, int NKM, bool F32>
-__global__ void __launch_bounds__(256, 1) am_solve_kernel(const bmpc_dev_consts C,
+#ifndef BMPC_MINB
+#define BMPC_MINB 1
+#endif
+#ifndef BMPC_MAXT
+#define BMPC_MAXT 256
+#endif
+__global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bmpc_dev_consts C,
                                                        const bmpc_solve_args A) {
   extern __shared__ __align__(16) double sm[];
   const int W = blockDim.x >> 5;
@@ -398,7 +433,7 @@ __global__ void __launch_bounds__(256, 1) am_solve_kernel(const bmpc_dev_consts 
   constexpr int RX = NB + 6, RP = NB + 4;
 
   constexpr bool kStoreXY = bmpc_stores_xy(npad);  // else the obstacle block re-evaluates x, y
-  constexpr int CH = NKM < 4 ? NKM : 4;              // sample slots per pass A / B chunk
+  constexpr int CH = NKM < 2 ? NKM : 2;              // sample slots per pass A / B chunk
   double* sPT = sm;                          // P^T, Pdot^T, Pddot^T
   double* sKxf = sPT + 3 * NB * npad;
   double* sKxa = sKxf + RX * C.kxs;
@@ -416,18 +451,22 @@ __global__ void __launch_bounds__(256, 1) am_solve_kernel(const bmpc_dev_consts 
   const SlotLayout sl = slot_layout(n);
   const int nslots = sl.F + (sl.R > 0 ? 1 : 0);
 
-  for (int t = threadIdx.x; t < 3 * NB * npad; t += blockDim.x) sPT[t] = C.PT[t];
-  for (int t = threadIdx.x; t < RX * C.kxs; t += blockDim.x) {
-    sKxf[t] = C.Kxf[t];
-    sKxa[t] = C.Kxa[t];
+  // The constant block (basis, KKT pairs, M, P^T P, tau) is one contiguous
+  // image in global memory laid out exactly like shared memory: one thread
+  // streams it in with bulk asynchronous copies (TMA, cp.async.bulk) that
+  // complete on an mbarrier, instead of every warp issuing the loads.
+  __shared__ __align__(8) unsigned long long s_cbar;
+  if (threadIdx.x == 0) {
+    const unsigned bytes = (unsigned)C.const_doubles * 8u;
+    mbar_init(&s_cbar, 1);
+    mbar_arrive_expect_tx(&s_cbar, bytes);
+    constexpr unsigned kChunk = 16384;
+    for (unsigned o = 0; o < bytes; o += kChunk)
+      bulk_copy_g2s(reinterpret_cast<char*>(sm) + o, reinterpret_cast<const char*>(C.PT) + o,
+                    bytes - o < kChunk ? bytes - o : kChunk, &s_cbar);
   }
-  for (int t = threadIdx.x; t < RP * C.kps; t += blockDim.x) {
-    sKpf[t] = C.Kpf[t];
-    sKpa[t] = C.Kpa[t];
-  }
-  for (int t = threadIdx.x; t < 2 * NB * C.kms; t += blockDim.x) sM[t] = C.M[t];  // M, then P^T P
-  for (int t = threadIdx.x; t < npad; t += blockDim.x) sTau[t] = C.tau[t];
-  __syncthreads();
+  __syncthreads();  // the initialised barrier is visible to every thread
+  mbar_wait_parity(&s_cbar, 0);
 
   const int inst = blockIdx.x * W + warp;
   if (inst >= L) return;  // no block-wide barriers below this point
@@ -629,7 +668,7 @@ __global__ void __launch_bounds__(256, 1) am_solve_kernel(const bmpc_dev_consts 
     {
       bool wrap = false;
       double prev_last = 0.0;  // theta of sample 32 r - 1: lane 31 of the previous slot
-#pragma unroll
+#pragma unroll 1  // chunks stay rolled: instruction-cache footprint
       for (int r0 = 0; r0 < NKM; r0 += CH) {
         int k[CH];
         bool v[CH];
@@ -762,7 +801,7 @@ __global__ void __launch_bounds__(256, 1) am_solve_kernel(const bmpc_dev_consts 
     BMPC_PROF(4);
     // (4) pass B: psi = P c_psi and the non-holonomic block (_speedups.pyx:200-216),
     //     contracted onto Pdot.
-#pragma unroll
+#pragma unroll 1  // chunks stay rolled: instruction-cache footprint
     for (int r0 = 0; r0 < NKM; r0 += CH) {
       int k[CH];
       bool v[CH];

@@ -136,7 +136,10 @@ int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pd
   const int npad = n <= 64 ? 64 : (n <= 128 ? 128 : (n <= 224 ? 224 : 256));
   const int kxs = rx | 1, kps = rp | 1, kms = nb | 1;
   const size_t nPT = (size_t)3 * nb * npad, nKx = (size_t)rx * kxs, nKp = (size_t)rp * kps;
-  std::vector<double> h(nPT + 2 * nKx + 2 * nKp + 2 * (size_t)nb * kms + npad, 0.0);
+  // the kernel's shared-memory image: M and P^T P padded to an even count so
+  // tau (and the total) stay 16-byte aligned for the bulk copy
+  const size_t nM = ((size_t)2 * nb * kms + 1) & ~(size_t)1;
+  std::vector<double> h(nPT + 2 * nKx + 2 * nKp + nM + npad, 0.0);
   const double* mats[3] = {P, Pdot, Pddot};
   for (int q = 0; q < 3; ++q)
     for (int i = 0; i < nb; ++i)
@@ -158,7 +161,7 @@ int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pd
       for (int k = 0; k < n; ++k) acc += (long double)P[(size_t)k * nb + i] * P[(size_t)k * nb + j];
       h[o + (size_t)i * kms + j] = (double)acc;
     }
-  o += (size_t)nb * kms;
+  o = offs[4] + nM;
   for (int k = 0; k < n; ++k) h[o + k] = tau[k];
   bmpc_ctx* c = new bmpc_ctx();
   cudaError_t e = cudaMalloc(&c->dmem, h.size() * sizeof(double));
@@ -190,6 +193,7 @@ int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pd
   c->C.Kpa = c->dmem + offs[3];
   c->C.M = c->dmem + offs[4];
   c->C.tau = c->dmem + o;
+  c->C.const_doubles = (int)h.size();
   *out = c;
   return BMPC_OK;
 }
