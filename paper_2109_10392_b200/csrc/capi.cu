@@ -5,6 +5,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -73,6 +74,10 @@ struct bmpc_ctx {
   double* dmem = nullptr;  // one allocation for every constant
   int sms = 148;
   int smem_optin = 227 * 1024;
+  // pinned staging for bmpc_plan_host's results (grown on demand)
+  std::mutex stage_mu;
+  void* stage = nullptr;
+  size_t stage_bytes = 0;
 };
 
 static thread_local std::string g_err;
@@ -201,6 +206,7 @@ int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pd
 int bmpc_ctx_destroy(bmpc_ctx* ctx) {
   if (!ctx) return BMPC_OK;
   cudaFree(ctx->dmem);
+  if (ctx->stage) cudaFreeHost(ctx->stage);
   delete ctx;
   return BMPC_OK;
 }
@@ -500,46 +506,64 @@ int bmpc_plan_host(bmpc_ctx* ctx, const bmpc_problem* hp, const bmpc_solve_opts*
   if (is_warm(o)) return fail(BMPC_EINVAL, "bmpc_plan_host: warm starts use the device API");
   cudaStream_t st = S_(stream);
   const int n = ctx->C.n, nb = ctx->C.nb;
-  const size_t L = (size_t)hp->S * hp->l, mn = (size_t)hp->m * n;
+  const size_t L = (size_t)hp->S * hp->l, mn = (size_t)hp->m * n, S = (size_t)hp->S;
+  const bool score = spec && hs;
+  // One device arena: inputs, then the results in the order they come back.
+  // Results are contiguous so one copy brings them to the pinned staging
+  // buffer; every region is a multiple of 8 bytes.
+  const size_t hist = (size_t)o->max_iter * 3 * L;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { const size_t at = off; off += (bytes + 15) & ~(size_t)15; return at; };
+  const size_t o_xix = take(S * mn * 8), o_xiy = take(S * mn * 8), o_bxy = take(12 * L * 8),
+               o_bps = take(4 * L * 8), o_hist = take(hist * 8), o_lam = take(3 * nb * L * 8),
+               o_v = take(o->want_v && ho->v ? n * L * 8 : 0);
+  const size_t o_res0 = off;  // results block
+  const size_t o_coef = take(3 * nb * L * 8), o_rf = take(3 * L * 8);
+  const size_t o_meta = take(score ? L * 8 : 0), o_mr = take(score ? L * 8 : 0),
+               o_hm = take(score ? L * 8 : 0), o_best = take(score ? 4 * S * 8 : 0),
+               o_fl = take(score ? L : 0);
+  const size_t res_bytes = off - o_res0;
   DevBuf B(st);
-  bmpc_problem dp = *hp;
-  double* xix = B.alloc<double>(hp->S * mn);
-  double* xiy = B.alloc<double>(hp->S * mn);
-  double* bxy = B.alloc<double>(12 * L);
-  double* bps = B.alloc<double>(4 * L);
-  if (!xix || !xiy || !bxy || !bps) return fail(BMPC_ECUDA, "device allocation failed");
-  CK(cudaMemcpyAsync(xix, hp->xi_x, hp->S * mn * 8, cudaMemcpyHostToDevice, st), "h2d");
-  CK(cudaMemcpyAsync(xiy, hp->xi_y, hp->S * mn * 8, cudaMemcpyHostToDevice, st), "h2d");
+  char* arena = B.alloc<char>(off);
+  if (!arena) return fail(BMPC_ECUDA, "device allocation failed");
+  double* xix = (double*)(arena + o_xix);
+  double* xiy = (double*)(arena + o_xiy);
+  double* bxy = (double*)(arena + o_bxy);
+  double* bps = (double*)(arena + o_bps);
+  CK(cudaMemcpyAsync(xix, hp->xi_x, S * mn * 8, cudaMemcpyHostToDevice, st), "h2d");
+  CK(cudaMemcpyAsync(xiy, hp->xi_y, S * mn * 8, cudaMemcpyHostToDevice, st), "h2d");
   CK(cudaMemcpyAsync(bxy, hp->b_xy, 12 * L * 8, cudaMemcpyHostToDevice, st), "h2d");
   CK(cudaMemcpyAsync(bps, hp->b_psi, 4 * L * 8, cudaMemcpyHostToDevice, st), "h2d");
+  bmpc_problem dp = *hp;
   dp.xi_x = xix;
   dp.xi_y = xiy;
   dp.b_xy = bxy;
   dp.b_psi = bps;
   bmpc_solve_out dout;
   memset(&dout, 0, sizeof(dout));
-  double* coef = B.alloc<double>(6 * nb * L);
+  double* coef = (double*)(arena + o_coef);
+  double* lam = (double*)(arena + o_lam);
   dout.c_x = coef;
   dout.c_y = coef + nb * L;
   dout.c_psi = coef + 2 * nb * L;
-  dout.l_x = coef + 3 * nb * L;
-  dout.l_y = coef + 4 * nb * L;
-  dout.l_psi = coef + 5 * nb * L;
-  dout.history = B.alloc<double>((size_t)o->max_iter * 3 * L);
-  dout.res_final = B.alloc<double>(3 * L);
-  dout.v = (o->want_v && ho->v) ? B.alloc<double>(n * L) : nullptr;
-  if (!coef || !dout.history || !dout.res_final) return fail(BMPC_ECUDA, "device allocation failed");
+  dout.l_x = lam;
+  dout.l_y = lam + nb * L;
+  dout.l_psi = lam + 2 * nb * L;
+  dout.history = (double*)(arena + o_hist);
+  dout.res_final = (double*)(arena + o_rf);
+  dout.v = (o->want_v && ho->v) ? (double*)(arena + o_v) : nullptr;
   bmpc_score_out ds;
   memset(&ds, 0, sizeof(ds));
-  if (spec && hs) {  // solve with the fused scoring epilogue, then the per-scene argmin
-    ds.meta_cost = B.alloc<double>(L);
-    ds.min_ratio = B.alloc<double>(L);
-    ds.heading_max = B.alloc<double>(L);
-    ds.flags = B.alloc<unsigned char>(L);
-    ds.best_index = B.alloc<long long>(hp->S);
-    ds.argmin_all = B.alloc<long long>(hp->S);
-    ds.argmin_hc = B.alloc<long long>(hp->S);
-    ds.n_feasible = B.alloc<long long>(hp->S);
+  if (score) {  // solve with the fused scoring epilogue, then the per-scene argmin
+    ds.meta_cost = (double*)(arena + o_meta);
+    ds.min_ratio = (double*)(arena + o_mr);
+    ds.heading_max = (double*)(arena + o_hm);
+    ds.flags = (unsigned char*)(arena + o_fl);
+    long long* idx = (long long*)(arena + o_best);
+    ds.best_index = idx;
+    ds.argmin_all = idx + S;
+    ds.argmin_hc = idx + 2 * S;
+    ds.n_feasible = idx + 3 * S;
     rc = bmpc_plan(ctx, &dp, o, &dout, spec, &ds, stream);
   } else {
     rc = bmpc_solve(ctx, &dp, o, &dout, stream);
@@ -547,26 +571,41 @@ int bmpc_plan_host(bmpc_ctx* ctx, const bmpc_problem* hp, const bmpc_solve_opts*
   if (rc) return rc;
   ho->iterations = dout.iterations;
   ho->converged = dout.converged;
+  // rarely requested extras straight to the caller's memory
   struct Cp { void* h; const void* d; size_t bytes; };
-  const Cp cps[] = {
-      {ho->c_x, dout.c_x, nb * L * 8}, {ho->c_y, dout.c_y, nb * L * 8},
-      {ho->c_psi, dout.c_psi, nb * L * 8}, {ho->l_x, dout.l_x, nb * L * 8},
-      {ho->l_y, dout.l_y, nb * L * 8}, {ho->l_psi, dout.l_psi, nb * L * 8},
-      {ho->v, dout.v, n * L * 8},
+  const Cp extra[] = {
+      {ho->l_x, dout.l_x, nb * L * 8}, {ho->l_y, dout.l_y, nb * L * 8},
+      {ho->l_psi, dout.l_psi, nb * L * 8}, {ho->v, dout.v, n * L * 8},
       {ho->history, dout.history, (size_t)dout.iterations * 3 * L * 8},
-      {ho->res_final, dout.res_final, 3 * L * 8},
-      {hs ? hs->meta_cost : nullptr, ds.meta_cost, L * 8},
-      {hs ? hs->min_ratio : nullptr, ds.min_ratio, L * 8},
-      {hs ? hs->heading_max : nullptr, ds.heading_max, L * 8},
-      {hs ? hs->flags : nullptr, ds.flags, L},
-      {hs ? hs->best_index : nullptr, ds.best_index, (size_t)hp->S * 8},
-      {hs ? hs->argmin_all : nullptr, ds.argmin_all, (size_t)hp->S * 8},
-      {hs ? hs->argmin_hc : nullptr, ds.argmin_hc, (size_t)hp->S * 8},
-      {hs ? hs->n_feasible : nullptr, ds.n_feasible, (size_t)hp->S * 8},
   };
-  for (const Cp& c : cps)
+  for (const Cp& c : extra)
     if (c.h && c.d && c.bytes) CK(cudaMemcpyAsync(c.h, c.d, c.bytes, cudaMemcpyDeviceToHost, st), "d2h");
+  // the results block in one copy through the pinned staging buffer
+  std::lock_guard<std::mutex> lk(ctx->stage_mu);
+  if (ctx->stage_bytes < res_bytes) {
+    if (ctx->stage) cudaFreeHost(ctx->stage);
+    ctx->stage = nullptr;
+    ctx->stage_bytes = 0;
+    CK(cudaHostAlloc(&ctx->stage, res_bytes, cudaHostAllocDefault), "pinned staging");
+    ctx->stage_bytes = res_bytes;
+  }
+  CK(cudaMemcpyAsync(ctx->stage, arena + o_res0, res_bytes, cudaMemcpyDeviceToHost, st), "d2h");
   CK(cudaStreamSynchronize(st), "sync");
+  const char* hb = (const char*)ctx->stage - o_res0;  // arena offset -> staging
+  const Cp res[] = {
+      {ho->c_x, hb + o_coef, nb * L * 8}, {ho->c_y, hb + o_coef + nb * L * 8, nb * L * 8},
+      {ho->c_psi, hb + o_coef + 2 * nb * L * 8, nb * L * 8}, {ho->res_final, hb + o_rf, 3 * L * 8},
+      {score ? hs->meta_cost : nullptr, hb + o_meta, L * 8},
+      {score ? hs->min_ratio : nullptr, hb + o_mr, L * 8},
+      {score ? hs->heading_max : nullptr, hb + o_hm, L * 8},
+      {score ? hs->flags : nullptr, hb + o_fl, L},
+      {score ? hs->best_index : nullptr, hb + o_best, S * 8},
+      {score ? hs->argmin_all : nullptr, hb + o_best + S * 8, S * 8},
+      {score ? hs->argmin_hc : nullptr, hb + o_best + 2 * S * 8, S * 8},
+      {score ? hs->n_feasible : nullptr, hb + o_best + 3 * S * 8, S * 8},
+  };
+  for (const Cp& c : res)
+    if (c.h && c.bytes) memcpy(c.h, c.d, c.bytes);
   return BMPC_OK;
 }
 

@@ -516,9 +516,9 @@ def plan_batch(solver: BatchSolver, scenes, max_iter: int = 100, tol: float = 0.
     res = np.empty((3, L))
     out = nat.SolveOut(coef[0].ctypes.data, coef[1].ctypes.data, coef[2].ctypes.data, None, None,
                        None, None, None, res.ctypes.data, 0, 0)
-    meta, mr, hm = np.empty(L), np.empty(L), np.empty(L)
+    meta, mr, hm = np.empty((3, L))
     flags = np.empty(L, dtype=np.uint8)
-    best, amin, ahc, nf = (np.empty(S, dtype=np.int64) for _ in range(4))
+    best, amin, ahc, nf = np.empty((4, S), dtype=np.int64)
     so = nat.ScoreOut(meta.ctypes.data, mr.ctypes.data, hm.ctypes.data, flags.ctypes.data,
                       best.ctypes.data, amin.ctypes.data, ahc.ctypes.data, nf.ctypes.data)
     nat.check(nat.load().bmpc_plan_host(ctx, ctypes.byref(prob), ctypes.byref(opts), ctypes.byref(out),
