@@ -334,8 +334,17 @@ int bmpc_sweeps(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opts* o, 
   return rc;
 }
 
+// Work enqueued right after the sweeps (the per-scene argmin of bmpc_plan):
+// issued before the early-stop check synchronises, and again after a re-run.
+struct PostSolve {
+  const bmpc_problem* p;
+  const bmpc_score_out* so;
+};
+static int post_solve(const PostSolve* ps, cudaStream_t st);
+
 static int solve_impl(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opts* o,
-                      bmpc_solve_out* out, const bmpc_fused_score* fsc, void* stream);
+                      bmpc_solve_out* out, const bmpc_fused_score* fsc, void* stream,
+                      const PostSolve* post = nullptr);
 
 int bmpc_solve(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opts* o,
                bmpc_solve_out* out, void* stream) {
@@ -374,16 +383,22 @@ int bmpc_plan(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opts* o, bm
   if (!so || !so->meta_cost || !so->min_ratio || !so->heading_max || !so->flags)
     return fail(BMPC_EINVAL, "bmpc_plan: per-instance score outputs required");
   const bmpc_fused_score f = fused_from(spec, so);
-  if ((rc = solve_impl(ctx, p, o, out, &f, stream))) return rc;
+  const PostSolve post{p, so};
+  return solve_impl(ctx, p, o, out, &f, stream, &post);
+}
+
+static int post_solve(const PostSolve* ps, cudaStream_t st) {
+  const bmpc_score_out* so = ps->so;
   if (so->best_index && so->argmin_all && so->argmin_hc && so->n_feasible)
-    CK(bmpc::op_argmin(p->S, p->l, so->meta_cost, so->flags, so->best_index, so->argmin_all,
-                       so->argmin_hc, so->n_feasible, S_(stream)),
+    CK(bmpc::op_argmin(ps->p->S, ps->p->l, so->meta_cost, so->flags, so->best_index, so->argmin_all,
+                       so->argmin_hc, so->n_feasible, st),
        "argmin");
   return BMPC_OK;
 }
 
 static int solve_impl(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opts* o,
-                      bmpc_solve_out* out, const bmpc_fused_score* fsc, void* stream) {
+                      bmpc_solve_out* out, const bmpc_fused_score* fsc, void* stream,
+                      const PostSolve* post) {
   int rc = check_problem(ctx, p);
   if (rc) return rc;
   if (!o || !out) return fail(BMPC_EINVAL, "null opts/out");
@@ -409,18 +424,25 @@ static int solve_impl(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opt
     // residual is <= tol; when it is not the last one, re-run exactly that many
     // sweeps (the instances are independent and deterministic, so the re-run
     // reproduces the same iterates).
-    int t = 1 << 30;
+    // The follow-up work is enqueued before the check synchronises, so the
+    // device never idles on the host round trip; it is redone after a re-run.
+    int t = 0;
     CK(cudaMallocAsync(&tstar, sizeof(int), st), "cudaMallocAsync");
-    CK(cudaMemcpyAsync(tstar, &t, sizeof(int), cudaMemcpyHostToDevice, st), "memcpy");
+    CK(cudaMemsetAsync(tstar, 0x7f, sizeof(int), st), "memset");  // "none" = 0x7f7f7f7f
     CK(bmpc::op_first_converged(o->max_iter, L, out->history, o->tol, tstar, st), "first_converged");
     CK(cudaMemcpyAsync(&t, tstar, sizeof(int), cudaMemcpyDeviceToHost, st), "memcpy");
+    if (post && (rc = post_solve(post, st))) return rc;
     CK(cudaStreamSynchronize(st), "sync");
     if (t < o->max_iter) {
       converged = 1;
       iters = t + 1;
-      if (iters < o->max_iter)
+      if (iters < o->max_iter) {
         rc = launch_sweeps(ctx, p, xi2, o, iters, mode, 0, nullptr, 0, out, st, fsc);
+        if (!rc && post) rc = post_solve(post, st);
+      }
     }
+  } else if (!rc && post) {
+    rc = post_solve(post, st);
   }
   if (xi2) cudaFreeAsync(xi2, st);
   if (tstar) cudaFreeAsync(tstar, st);
