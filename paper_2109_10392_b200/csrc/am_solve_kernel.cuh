@@ -1,29 +1,29 @@
 #pragma once
-// am_solve.cu -- persistent fused alternating-minimization kernel (sm_100a, fp64).
+// am_solve_kernel.cuh -- persistent fused alternating-minimization kernel
+// (sm_100a, fp64).
 //
 // One warp owns one trajectory instance for the whole solve; all AM sweeps run
 // inside a single launch and every iterate stays on chip (registers + a few
-// hundred bytes of per-warp shared memory).  Per sweep (reference
+// KB of per-warp shared memory).  Per sweep (reference
 // /root/reference/pkg/src/batchmpc/solver.py:458-500):
 //
-//   1. xy QP     [c; mu] = K_axis^-1 [rho*G + lambda ; b], one refinement step
+//   1. xy QP     [c; mu] = K_axis^-1 [rho*G + lambda ; b], refined against K
 //                (solver.py:302-312, :164-168)
-//   2. sampling  xdot, ydot = Pdot c ; theta = unwrap(atan2(ydot, xdot)) (:474-477)
-//   3. psi QP    c_psi = K_psi^-1 [rho*P^T theta + lambda_psi ; b_psi], refined (:322-328)
-//   4. tail      closed forms for d, d_a, v; residual blocks; next targets
-//                (kernels/_speedups.pyx:114-218), contracted on the fly:
-//                G = F_axis^T g = P^T sum_j g_obs,j + Pddot^T g_acc + Pdot^T g_nh
-//                R = F_axis^T r (same split), lambda -= rho*R (:491-494)
+//   2. pass A    x, y, xdot, ydot, xddot, yddot = [P; Pdot; Pddot] c;
+//                theta = unwrap(atan2(ydot, xdot)) (:474-477); acceleration
+//                block (kernels/_speedups.pyx:179-198); P^T theta, Pddot^T g_a
+//   3. psi QP    c_psi = K_psi^-1 [rho*P^T theta + lambda_psi ; b_psi], refined
+//                (:322-328); lambda_psi step via (P^T P) c_psi - P^T theta
+//   4. pass B    psi = P c_psi, non-holonomic block (_speedups.pyx:200-216), Pdot^T g_n
+//   5. obstacles exact form of _speedups.pyx:150-176 (outside: g_j = x, r_j = 0),
+//                P^T sum_j g_j
+//   6. G = F_axis^T g reduction; lambda_xy -= rho ((F_axis^T F_axis) c - G) (:491-494)
 //
 // Lanes split the horizon samples k (k = lane + 32*r); lane i owns coefficient i
 // of the x axis (and of psi), lane 16+i coefficient i of the y axis.  The
-// contractions over k are warp reduce-scatters with a fixed summation tree, so
-// an instance's arithmetic never depends on the batch size, its column index
-// or the GPU shard it lands on.
-//
-// The obstacle block uses the minimal formulation of SURVEY.md finding 8:
-// obstacle-sum-first projections and rsqrt-and-multiply in place of sqrt and
-// three divisions (parity measured at <=1e-10 relative on stable columns).
+// contractions over k go through a shared-memory transpose with a fixed
+// summation order, so an instance's arithmetic never depends on the batch
+// size, its column index or the GPU shard it lands on.
 #include <cuda_runtime.h>
 #include <stdio.h>
 
@@ -242,12 +242,10 @@ struct TailArgs {
   double a, b, inv_ab;
 };
 
-// fp32 mode obstacle term.  In exact arithmetic the reference's closed forms
-// give r = w - a d (cos, sin) = 0 and g = x whenever the sample is outside the
-// ellipse (d = r/(ab) > 1), and d = 1 inside; so only inside terms carry a
-// residual, r = w - (a cos, b sin), and g = x - r always.  Evaluating that
-// form in fp32 (w rounded from the fp64 difference) keeps far and virtual
-// obstacles (+1e4 m) exact instead of rounding |w| ~ 1e4 m in fp32.
+// fp32 mode inside term (the outside test runs in fp64 in both modes): with
+// d = 1 the residual is r = w - (a cos, b sin) and g = x - r, evaluated in fp32
+// from w rounded off the fp64 difference, so far and virtual obstacles (+1e4 m)
+// never see |w| rounded in fp32.
 __device__ __forceinline__ void obstacle_term_f32(double x, double y, double2 q, float a, float b,
                                                   float ab2, float& srx, float& sry, float& sq) {
   const float wx = (float)(x - q.x), wy = (float)(y - q.y);
@@ -298,7 +296,7 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
     }
     BMPC_PROF_NS(10);
     const int qstep = js * T.n;
-    constexpr int U = (F32 || NS == 1) ? 4 : 2;  // obstacles in flight per sample
+    constexpr int U = NS == 1 ? 4 : 2;  // obstacles in flight per sample
     const double2* qp[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) qp[s] = T.xi + j0 * T.n + k[s];
@@ -332,13 +330,9 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
 #pragma unroll
           for (int u = 0; u < U; ++u) qn[s][u] = __ldg(qp[s] + (U + u) * qstep);
       }
-      if constexpr (F32) {
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-#pragma unroll
-          for (int s = 0; s < NS; ++s)
-            obstacle_term_f32(x[s], y[s], q[s][u], af, bf, ab2, srx[s], sry[s], sqf[s]);
-      } else {
+      {
+        // outside test in fp64 for both modes; the rare inside terms in the
+        // mode's precision
         bool in[NS][U], any = false;
 #pragma unroll
         for (int u = 0; u < U; ++u)
@@ -352,8 +346,12 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
           for (int u = 0; u < U; ++u)
 #pragma unroll
             for (int s = 0; s < NS; ++s)
-              if (in[s][u])
-                obstacle_inside_term(x[s], y[s], q[s][u], T.a, T.b, gsx[s], gsy[s], sq[s], cin[s]);
+              if (in[s][u]) {
+                if constexpr (F32)
+                  obstacle_term_f32(x[s], y[s], q[s][u], af, bf, ab2, srx[s], sry[s], sqf[s]);
+                else
+                  obstacle_inside_term(x[s], y[s], q[s][u], T.a, T.b, gsx[s], gsy[s], sq[s], cin[s]);
+              }
         }
       }
 #pragma unroll
@@ -363,10 +361,12 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
         const double2 q = __ldg(qp[s]);
-        if constexpr (F32)
-          obstacle_term_f32(x[s], y[s], q, af, bf, ab2, srx[s], sry[s], sqf[s]);
-        else if (obstacle_inside(x[s], y[s], q, T.a, T.b, abd2))
-          obstacle_inside_term(x[s], y[s], q, T.a, T.b, gsx[s], gsy[s], sq[s], cin[s]);
+        if (obstacle_inside(x[s], y[s], q, T.a, T.b, abd2)) {
+          if constexpr (F32)
+            obstacle_term_f32(x[s], y[s], q, af, bf, ab2, srx[s], sry[s], sqf[s]);
+          else
+            obstacle_inside_term(x[s], y[s], q, T.a, T.b, gsx[s], gsy[s], sq[s], cin[s]);
+        }
         qp[s] += qstep;
       }
     }
