@@ -544,22 +544,19 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
         if (cold) {
           const double xl = __dadd_rn(x0, __dmul_rn(sTau[k], __dsub_rn(xf, x0)));
           const double yl = __dadd_rn(y0, __dmul_rn(sTau[k], __dsub_rn(yf, y0)));
-#pragma unroll 2
+          // obstacle_update (_speedups.pyx:12-39) on the straight line, in the
+          // exact form of the sweep's obstacle block: outside terms give
+          // g_j = x, inside ones q + (a cos, b sin)
+          const double abd2 = (a * b) * (a * b);
+          double cin = 0.0, sq0 = 0.0;
+#pragma unroll 4
           for (int j = 0; j < m; ++j) {
             const double2 q = __ldg(xi + j * n + k);
-            const double wx = xl - q.x, wy = yl - q.y;
-            // the reference's trig form (obstacle_update, _speedups.pyx:12-39) with
-            // the branch-free <=2-ulp atan2/sincos (alpha is in [-pi, pi])
-            const double al = atan2_nb(a * wy, b * wx);
-            double sa, ca;
-            sincos_nb(al, &sa, &ca);
-            const double num = __dadd_rn(__dmul_rn(__dmul_rn(a, ca), wx), __dmul_rn(__dmul_rn(b, sa), wy));
-            const double den = __dadd_rn(__dmul_rn(a * ca, a * ca), __dmul_rn(b * sa, b * sa));
-            double d = div_nb(num, den);  // den >= b^2 > 0
-            d = d < 1.0 ? 1.0 : d;
-            gsx += q.x + __dmul_rn(a * d, ca);
-            gsy += q.y + __dmul_rn(b * d, sa);
+            if (obstacle_inside(xl, yl, q, a, b, abd2))
+              obstacle_inside_term(xl, yl, q, a, b, gsx, gsy, sq0, cin);
           }
+          gsx = fma((double)m - cin, xl, gsx);
+          gsy = fma((double)m - cin, yl, gsy);
           gnx = speed0;  // v cos(psi) with psi = P c_psi = 0, alpha_a = d_a = 0
         } else {
           double ps = 0.0;
@@ -570,7 +567,8 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
             const size_t row = (size_t)(j * n + k) * L + inst;
             const double al = A.w_alpha[row], d = A.w_d[row];
             double sa, ca;
-            sincos(al, &sa, &ca);
+            sincos_nb(al, &sa, &ca);  // alpha in [-pi, pi]; full range only if needed
+            if (!(fabs(al) < 1.0e5)) sincos(al, &sa, &ca);
             gsx += q.x + __dmul_rn(a * d, ca);
             gsy += q.y + __dmul_rn(b * d, sa);
           }
