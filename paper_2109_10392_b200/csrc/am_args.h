@@ -20,7 +20,7 @@ typedef struct {
   const double* Kxa;  // [nb+6][kxs] the per-axis KKT matrix (refinement residual)
   const double* Kpf;  // [nb+4][kps] inverse of the heading KKT matrix
   const double* Kpa;  // [nb+4][kps] the heading KKT matrix
-  const double* M;    // [2][nb][kms] F_axis^T F_axis, then P^T P (multiplier step identities)
+  const double* M;    // [4][nb][kms] F_axis^T F_axis, P^T P, Pddot^T Pddot, Pdot^T Pdot
   int const_doubles;  // size of the whole constant image starting at PT (even; the
                       // kernel's shared-memory layout, copied in one bulk transfer)
 } bmpc_dev_consts;
@@ -98,7 +98,13 @@ typedef struct {
 // Per-warp shared scratch of the persistent kernel (csrc/am_solve_kernel.cuh):
 // 288 doubles of KKT vectors, the per-sample arrays (theta, xdot, ydot and,
 // for npad <= 128, x and y), and the 32 x 33 transpose buffer.
-BMPC_HD constexpr bool bmpc_stores_xy(int npad) { return npad <= 128; }
+#ifndef BMPC_XY_NPAD_MAX
+#define BMPC_XY_NPAD_MAX 128
+#endif
+#ifndef BMPC_MAX_WARPS
+#define BMPC_MAX_WARPS 8  // warps (instances) per CTA; the kernel's launch bound is 32x this
+#endif
+BMPC_HD constexpr bool bmpc_stores_xy(int npad) { return npad <= BMPC_XY_NPAD_MAX; }
 BMPC_HD constexpr int bmpc_sample_arrays(int npad) { return bmpc_stores_xy(npad) ? 5 : 3; }
 BMPC_HD constexpr int bmpc_warp_scratch_doubles(int npad) {
   return 288 + bmpc_sample_arrays(npad) * npad + 32 * 33;

@@ -38,8 +38,8 @@ namespace bmpc {
 // device counter.  Compiled out of the product library.
 #ifdef BMPC_PHASE_PROF
 static __device__ unsigned long long g_phase_cycles[16];
-__shared__ unsigned long long s_prof[8][16];
-__shared__ long long s_prof_t[8];
+__shared__ unsigned long long s_prof[BMPC_MAX_WARPS][16];
+__shared__ long long s_prof_t[BMPC_MAX_WARPS];
 #define BMPC_PROF_DECL                                               \
   if ((threadIdx.x & 31) == 0) {                                     \
     for (int _i = 0; _i < 16; ++_i) s_prof[threadIdx.x >> 5][_i] = 0; \
@@ -212,6 +212,23 @@ __device__ __forceinline__ bool obstacle_inside(double x, double y, double2 q, d
   const double px = b * (x - q.x), py = a * (y - q.y);
   return !(fma(px, px, py * py) >= ab2);
 }
+// Inside term of the sweep's obstacle block: residual r_j = w - (a cos, b sin)
+// (g_j - x = -r_j), accumulated with its square.
+__device__ __forceinline__ void obstacle_inside_res(double x, double y, double2 q, double a,
+                                                    double b, double& srx, double& sry,
+                                                    double& sq, double& cin) {
+  const double wx = x - q.x, wy = y - q.y;
+  const double px = b * wx, py = a * wy;
+  const double r2 = fma(px, px, py * py);
+  const double ri = rsqrt_nb(r2);
+  const double ca = r2 > 0.0 ? px * ri : 1.0, sa = py * ri;  // r = 0 -> (1, 0)
+  const double rx = wx - a * ca, ry = wy - b * sa;
+  sq = fma(rx, rx, fma(ry, ry, sq));
+  srx += rx;
+  sry += ry;
+  cin += 1.0;
+}
+
 __device__ __forceinline__ void obstacle_inside_term(double x, double y, double2 q, double a,
                                                      double b, double& gix, double& giy,
                                                      double& sq, double& cin) {
@@ -247,7 +264,9 @@ struct TailArgs {
 // from w rounded off the fp64 difference, so far and virtual obstacles (+1e4 m)
 // never see |w| rounded in fp32.
 __device__ __forceinline__ void obstacle_term_f32(double x, double y, double2 q, float a, float b,
-                                                  float ab2, float& srx, float& sry, float& sq) {
+                                                  float ab2, float& srx, float& sry, float& sq,
+                                                  double& cin) {
+  cin += 1.0;
   const float wx = (float)(x - q.x), wy = (float)(y - q.y);
   const float px = b * wx, py = a * wy;
   const float r2 = fmaf(px, px, py * py);
@@ -272,9 +291,10 @@ template <int NS, int NB, int NPAD, bool F32>
 __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)[NS], int j0, int js,
                                                int group, bool valid, bool leader,
                                                double (&Gx)[NB], double (&Gy)[NB], double& sqo) {
-  double x[NS], y[NS], gsx[NS], gsy[NS], sq[NS];
+  double x[NS], y[NS], gsx[NS], gsy[NS], sq[NS];  // gsx, gsy: sum of inside residuals
+  double cin[NS];                                   // inside terms per sample
 #pragma unroll
-  for (int s = 0; s < NS; ++s) x[s] = y[s] = gsx[s] = gsy[s] = sq[s] = 0.0;
+  for (int s = 0; s < NS; ++s) x[s] = y[s] = gsx[s] = gsy[s] = sq[s] = cin[s] = 0.0;
   if (valid) {
     if (T.xs) {
 #pragma unroll
@@ -305,9 +325,6 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
     for (int s = 0; s < NS; ++s) srx[s] = sry[s] = sqf[s] = 0.f;
     const float af = (float)T.a, bf = (float)T.b, ab2 = (float)(T.a * T.b * T.a * T.b);
     const double abd2 = (T.a * T.b) * (T.a * T.b);
-    double cin[NS];  // fp64 mode: inside terms per sample
-#pragma unroll
-    for (int s = 0; s < NS; ++s) cin[s] = 0.0;
     int j = j0;
     // software pipeline: the next group's predictions are in flight while the
     // current group computes (xi comes from L2 once it outgrows L1, e.g. c4)
@@ -348,9 +365,9 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
             for (int s = 0; s < NS; ++s)
               if (in[s][u]) {
                 if constexpr (F32)
-                  obstacle_term_f32(x[s], y[s], q[s][u], af, bf, ab2, srx[s], sry[s], sqf[s]);
+                  obstacle_term_f32(x[s], y[s], q[s][u], af, bf, ab2, srx[s], sry[s], sqf[s], cin[s]);
                 else
-                  obstacle_inside_term(x[s], y[s], q[s][u], T.a, T.b, gsx[s], gsy[s], sq[s], cin[s]);
+                  obstacle_inside_res(x[s], y[s], q[s][u], T.a, T.b, gsx[s], gsy[s], sq[s], cin[s]);
               }
         }
       }
@@ -363,28 +380,18 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
         const double2 q = __ldg(qp[s]);
         if (obstacle_inside(x[s], y[s], q, T.a, T.b, abd2)) {
           if constexpr (F32)
-            obstacle_term_f32(x[s], y[s], q, af, bf, ab2, srx[s], sry[s], sqf[s]);
+            obstacle_term_f32(x[s], y[s], q, af, bf, ab2, srx[s], sry[s], sqf[s], cin[s]);
           else
-            obstacle_inside_term(x[s], y[s], q, T.a, T.b, gsx[s], gsy[s], sq[s], cin[s]);
+            obstacle_inside_res(x[s], y[s], q, T.a, T.b, gsx[s], gsy[s], sq[s], cin[s]);
         }
         qp[s] += qstep;
       }
     }
-    // terms this lane evaluated per sample (obstacles j0, j0 + js, ...)
-    const double cnt = j0 < T.m ? (double)((T.m - j0 + js - 1) / js) : 0.0;
-    if constexpr (!F32) {
-      // outside terms contribute g_j = x each
+    if constexpr (F32) {
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
-        gsx[s] = fma(cnt - cin[s], x[s], gsx[s]);
-        gsy[s] = fma(cnt - cin[s], y[s], gsy[s]);
-      }
-    } else {
-      // g_j = x - r_j exactly, so sum_j g_j = (#obstacles) x - sum_j r_j
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        gsx[s] = fma(cnt, x[s], -(double)srx[s]);
-        gsy[s] = fma(cnt, y[s], -(double)sry[s]);
+        gsx[s] = (double)srx[s];
+        gsy[s] = (double)sry[s];
         sq[s] = (double)sqf[s];
       }
     }
@@ -395,18 +402,30 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
       gsx[0] += __shfl_xor_sync(BMPC_FULL, gsx[0], o);
       gsy[0] += __shfl_xor_sync(BMPC_FULL, gsy[0], o);
       sq[0] += __shfl_xor_sync(BMPC_FULL, sq[0], o);
+      cin[0] += __shfl_xor_sync(BMPC_FULL, cin[0], o);
     }
   }
-  if (!(valid && leader)) return;
+  // P^T sum_j g_j = m (P^T P) c - P^T sum_inside r_j: only samples with an inside
+  // term contribute here (the m (P^T P) c part is added once per sweep); the
+  // contraction runs only when some lane of the warp has one
+  const bool own = valid && leader;
+  bool any = false;
 #pragma unroll
-  for (int s = 0; s < NS; ++s) sqo += sq[s];
+  for (int s = 0; s < NS; ++s) {
+    sqo += own ? sq[s] : 0.0;
+    any |= own && cin[s] > 0.0;
+    gsx[s] = own ? -gsx[s] : 0.0;
+    gsy[s] = own ? -gsy[s] : 0.0;
+  }
+  if (__any_sync(BMPC_FULL, any)) {
 #pragma unroll
-  for (int i = 0; i < NB; ++i) {
+    for (int i = 0; i < NB; ++i) {
 #pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      const double p = T.P[i * NPAD + k[s]];
-      Gx[i] = fma(p, gsx[s], Gx[i]);
-      Gy[i] = fma(p, gsy[s], Gy[i]);
+      for (int s = 0; s < NS; ++s) {
+        const double p = T.P[i * NPAD + k[s]];
+        Gx[i] = fma(p, gsx[s], Gx[i]);
+        Gy[i] = fma(p, gsy[s], Gy[i]);
+      }
     }
   }
   BMPC_PROF_NS(13);
@@ -417,7 +436,7 @@ template <int NB, int NKM, bool F32>
 #define BMPC_MINB 1
 #endif
 #ifndef BMPC_MAXT
-#define BMPC_MAXT 256
+#define BMPC_MAXT (32 * BMPC_MAX_WARPS)
 #endif
 __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bmpc_dev_consts C,
                                                        const bmpc_solve_args A) {
@@ -439,9 +458,11 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
   double* sKxa = sKxf + RX * C.kxs;
   double* sKpf = sKxa + RX * C.kxs;
   double* sKpa = sKpf + RP * C.kps;
-  double* sM = sKpa + RP * C.kps;   // F_axis^T F_axis (lambda identity)
-  double* sMp = sM + NB * C.kms;    // P^T P (lambda_psi identity)
-  double* sTau = sM + ((2 * NB * C.kms + 1) & ~1);  // keep the double2 scratch 16-byte aligned
+  double* sM = sKpa + RP * C.kps;   // F_axis^T F_axis = m P^T P + Pddot^T Pddot + Pdot^T Pdot
+  double* sMp = sM + NB * C.kms;    // P^T P
+  double* sMdd = sMp + NB * C.kms;  // Pddot^T Pddot
+  double* sMd = sMdd + NB * C.kms;  // Pdot^T Pdot
+  double* sTau = sM + ((4 * NB * C.kms + 1) & ~1);  // keep the double2 scratch 16-byte aligned
   double* wbase = sTau + npad + warp * bmpc_warp_scratch_doubles(npad);
   double* arr = wbase + kWarpScratch;
   WarpScratch ws{wbase,       wbase + 64,   wbase + 128, wbase + 192, wbase + 224, wbase + 256,
@@ -656,16 +677,18 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
 
     // (2) pass A over every sample (lane + 32 r), CH slots at a time: x, y,
     //     xdot, ydot, xddot, yddot from c; theta = atan2(ydot, xdot) with the
-    //     unwrap test against the previous sample done in registers; the
-    //     acceleration block (_speedups.pyx:179-198), which needs no psi, and the
-    //     contractions P^T theta and Pddot^T g_acc.
-    double Gx[NB], Gy[NB], pt[NB];
+    //     unwrap test against the previous sample done in registers; P^T theta.
+    //     Acceleration block (_speedups.pyx:179-198) in exact form: unclipped
+    //     samples give g_acc = (xddot, yddot) and r = 0, so Pddot^T g_acc =
+    //     (Pddot^T Pddot) c plus a sparse correction from the clipped samples.
+    double Gx[NB], Gy[NB], pt[NB];  // Gx, Gy: lane partials of F_axis^T g beyond the Gram terms
 #pragma unroll
     for (int i = 0; i < NB; ++i) Gx[i] = Gy[i] = pt[i] = 0.0;
     double sqo = 0.0, sqa = 0.0, sqn = 0.0;
     {
       bool wrap = false;
       double prev_last = 0.0;  // theta of sample 32 r - 1: lane 31 of the previous slot
+      const double amax2 = A.a_max * A.a_max;
 #pragma unroll 1  // chunks stay rolled: instruction-cache footprint
       for (int r0 = 0; r0 < NKM; r0 += CH) {
         int k[CH];
@@ -693,9 +716,12 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
             ydd[s] = fma(pdd, c.y, ydd[s]);
           }
         }
-        double th[CH], gax[CH], gay[CH];
+        double th[CH];
+        bool clip[CH], anyclip = false;
 #pragma unroll
         for (int s = 0; s < CH; ++s) {
+          th[s] = 0.0;
+          clip[s] = false;
           if (r0 + s >= NKM) continue;
           th[s] = atan2_nb(yd[s], xd[s]);
           double prev = __shfl_up_sync(BMPC_FULL, th[s], 1);
@@ -711,31 +737,43 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
               ws.x[k[s]] = xx[s];
               ws.y[k[s]] = yy[s];
             }
-          }
-          // acceleration block (_speedups.pyx:179-198)
-          const double m2 = fma(xdd[s], xdd[s], ydd[s] * ydd[s]);
-          const double mi = rsqrt_nb(m2);
-          const double caa = m2 > 0.0 ? xdd[s] * mi : 1.0, saa = ydd[s] * mi;
-          const double mag = m2 * mi;
-          const double da = mag < A.a_max ? mag : A.a_max;
-          gax[s] = v[s] ? da * caa : 0.0;
-          gay[s] = v[s] ? da * saa : 0.0;
-          if (v[s]) {
-            const double rax = xdd[s] - gax[s], ray = ydd[s] - gay[s];
-            sqa = fma(rax, rax, fma(ray, ray, sqa));
           } else {
             th[s] = 0.0;
           }
+          // |acc| > a_max (NaN tests unclipped: g = acc propagates it)
+          clip[s] = v[s] && fma(xdd[s], xdd[s], ydd[s] * ydd[s]) > amax2;
+          anyclip |= clip[s];
         }
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
 #pragma unroll
           for (int s = 0; s < CH; ++s) {
             if (r0 + s >= NKM) continue;
-            const double p = sP[i * npad + k[s]], pdd = sPdd[i * npad + k[s]];
-            pt[i] = fma(p, th[s], pt[i]);
-            Gx[i] = fma(pdd, gax[s], Gx[i]);
-            Gy[i] = fma(pdd, gay[s], Gy[i]);
+            pt[i] = fma(sP[i * npad + k[s]], th[s], pt[i]);
+          }
+        }
+        if (__any_sync(BMPC_FULL, anyclip)) {  // clipped samples: g = a_max (cos, sin)
+          double ex[CH], ey[CH];  // g_acc - acc
+#pragma unroll
+          for (int s = 0; s < CH; ++s) {
+            ex[s] = ey[s] = 0.0;
+            if (r0 + s >= NKM) continue;
+            const double m2 = fma(xdd[s], xdd[s], ydd[s] * ydd[s]);
+            const double mi = rsqrt_nb(m2);
+            const double dx = A.a_max * (xdd[s] * mi) - xdd[s], dy = A.a_max * (ydd[s] * mi) - ydd[s];
+            ex[s] = clip[s] ? dx : 0.0;
+            ey[s] = clip[s] ? dy : 0.0;
+            sqa = fma(ex[s], ex[s], fma(ey[s], ey[s], sqa));
+          }
+#pragma unroll
+          for (int i = 0; i < NB; ++i) {
+#pragma unroll
+            for (int s = 0; s < CH; ++s) {
+              if (r0 + s >= NKM) continue;
+              const double pdd = sPdd[i * npad + k[s]];
+              Gx[i] = fma(pdd, ex[s], Gx[i]);
+              Gy[i] = fma(pdd, ey[s], Gy[i]);
+            }
           }
         }
       }
@@ -765,9 +803,32 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
       pth = owner ? column_sum(ws.red, li) : 0.0;  // lanes i and 16+i both get sum_k P_ki theta_k
       __syncwarp();
     }
-
     BMPC_PROF(3);
-    // (3) psi QP
+
+    // (3) obstacle block (exact form, independent of psi), samples dealt as in
+    //     slot(): full slots two at a time, the n % 32 leftover samples split
+    //     over lane groups.
+    {
+      TailArgs T{sP, cxy, xi, kStoreXY ? ws.x : nullptr, kStoreXY ? ws.y : nullptr, n, m, a, b, inv_ab};
+      int r = 0;
+      if (kPairSlots<NB>) {
+#pragma unroll 1
+        for (; r + 1 < sl.F; r += 2) {
+          const int ks[2] = {lane + 32 * r, lane + 32 * (r + 1)};
+          obstacle_block<2, NB, npad, F32>(T, ks, 0, 1, 0, true, true, Gx, Gy, sqo);
+        }
+      }
+#pragma unroll 1
+      for (; r < nslots; ++r) {
+        const Slot S = slot(r, lane, sl);
+        const int ks[1] = {S.k};
+        obstacle_block<1, NB, npad, F32>(T, ks, S.j0, S.js, (r == sl.F) ? sl.g : 1, S.valid,
+                                         S.leader, Gx, Gy, sqo);
+      }
+    }
+    BMPC_PROF(5);
+
+    // (4) psi QP
     {
       if (!yax && owner) ws.bc[li] = rho * pth + lamp;
       if (yax && li < 4) ws.bc[NB + li] = bps;
@@ -795,9 +856,9 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
       for (int j = 0; j < NB; ++j) s4[j & 3] = fma(mr[j], ws.cp[j], s4[j & 3]);
       Lp = ((s4[0] + s4[1]) + (s4[2] + s4[3])) - pth;
     }
-
     BMPC_PROF(4);
-    // (4) pass B: psi = P c_psi and the non-holonomic block (_speedups.pyx:200-216),
+
+    // (5) pass B: psi = P c_psi and the non-holonomic block (_speedups.pyx:200-216),
     //     contracted onto Pdot.
 #pragma unroll 1  // chunks stay rolled: instruction-cache footprint
     for (int r0 = 0; r0 < NKM; r0 += CH) {
@@ -866,52 +927,41 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
         }
       }
     }
-
     BMPC_PROF(12);
-    // (5) obstacle block, samples dealt as in slot(): full slots two at a time,
-    //     the n % 32 leftover samples split over lane groups.
-    TailArgs T{sP, cxy, xi, kStoreXY ? ws.x : nullptr, kStoreXY ? ws.y : nullptr, n, m, a, b, inv_ab};
-    int r = 0;
-    if (kPairSlots<NB>) {
-      // two full sample slots per pass: twice the independent work in flight,
-      // same accumulation order as one slot at a time
-#pragma unroll 1
-      for (; r + 1 < sl.F; r += 2) {
-        const int ks[2] = {lane + 32 * r, lane + 32 * (r + 1)};
-        obstacle_block<2, NB, npad, F32>(T, ks, 0, 1, 0, true, true, Gx, Gy, sqo);
-      }
-    }
-#pragma unroll 1
-    for (; r < nslots; ++r) {
-      const Slot S = slot(r, lane, sl);
-      const int ks[1] = {S.k};
-      obstacle_block<1, NB, npad, F32>(T, ks, S.j0, S.js, (r == sl.F) ? sl.g : 1, S.valid, S.leader,
-                                       Gx, Gy, sqo);
-    }
-    BMPC_PROF(5);
-    // G = F_axis^T g: shared-memory transpose of the lane partials, fixed
-    // summation order; residual sums by xor butterflies (identical on all lanes)
+
+    // (6) G = F_axis^T g = m (P^T P) c + (Pddot^T Pddot) c + the lane partials
+    //     (Pdot^T g_nh and the exact-form corrections):
+    //     the dense sample part through the shared-memory transpose (fixed
+    //     summation order), residual sums by xor butterflies (identical on all
+    //     lanes).  lambda step F_axis^T (F_axis c - g) = (F_axis^T F_axis) c - G
+    //     = (Pdot^T Pdot) c - lane partials.
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
       ws.red[lane * kRedStride + i] = Gx[i];
       ws.red[lane * kRedStride + 16 + i] = Gy[i];
     }
     __syncwarp();
-    G = owner ? column_sum(ws.red, lane) : 0.0;
+    const double gn = owner ? column_sum(ws.red, lane) : 0.0;
     sqo = warp_sum(sqo);
     sqa = warp_sum(sqa);
     sqn = warp_sum(sqn);
     __syncwarp();
     BMPC_PROF(6);
-    // lambda step F_axis^T r = F_axis^T (F_axis c - g) = (F_axis^T F_axis) c - G:
-    // the residual vectors never need their own contraction
     if (owner) {
-      const double* mr = sM + li * C.kms;
-      double s4[4] = {0.0, 0.0, 0.0, 0.0};
+      const double* m1 = sMp + li * C.kms;
+      const double* m2 = sMdd + li * C.kms;
+      const double* m3 = sMd + li * C.kms;
+      double a1[2] = {0.0, 0.0}, a2[2] = {0.0, 0.0}, a3[2] = {0.0, 0.0};
 #pragma unroll
-      for (int j = 0; j < NB; ++j) s4[j & 3] = fma(mr[j], ws.cxy[2 * j + (yax ? 1 : 0)], s4[j & 3]);
-      const double R = ((s4[0] + s4[1]) + (s4[2] + s4[3])) - G;
-      lam -= rho * R;
+      for (int j = 0; j < NB; ++j) {
+        const double cj = ws.cxy[2 * j + (yax ? 1 : 0)];
+        a1[j & 1] = fma(m1[j], cj, a1[j & 1]);
+        a2[j & 1] = fma(m2[j], cj, a2[j & 1]);
+        a3[j & 1] = fma(m3[j], cj, a3[j & 1]);
+      }
+      const double rest = gn;
+      G = fma((double)m, a1[0] + a1[1], a2[0] + a2[1]) + rest;
+      lam -= rho * ((a3[0] + a3[1]) - rest);
     }
     if (!yax && owner) lamp -= rho * Lp;
     if (lane >= 16 && lane < 19) {

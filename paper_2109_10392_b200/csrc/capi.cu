@@ -143,7 +143,7 @@ int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pd
   const size_t nPT = (size_t)3 * nb * npad, nKx = (size_t)rx * kxs, nKp = (size_t)rp * kps;
   // the kernel's shared-memory image: M and P^T P padded to an even count so
   // tau (and the total) stay 16-byte aligned for the bulk copy
-  const size_t nM = ((size_t)2 * nb * kms + 1) & ~(size_t)1;
+  const size_t nM = ((size_t)4 * nb * kms + 1) & ~(size_t)1;
   std::vector<double> h(nPT + 2 * nKx + 2 * nKp + nM + npad, 0.0);
   const double* mats[3] = {P, Pdot, Pddot};
   for (int q = 0; q < 3; ++q)
@@ -159,13 +159,17 @@ int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pd
       for (int j = 0; j < dims[q]; ++j) h[o + (size_t)i * strides[q] + j] = blocks[q][(size_t)i * dims[q] + j];
     o += (size_t)dims[q] * strides[q];
   }
-  // P^T P right after M (the lambda_psi identity), accumulated in extended precision
-  for (int i = 0; i < nb; ++i)
-    for (int j = 0; j < nb; ++j) {
-      long double acc = 0.0L;
-      for (int k = 0; k < n; ++k) acc += (long double)P[(size_t)k * nb + i] * P[(size_t)k * nb + j];
-      h[o + (size_t)i * kms + j] = (double)acc;
-    }
+  // P^T P, Pddot^T Pddot, Pdot^T Pdot right after M (the exact-form sweep and
+  // multiplier identities), accumulated in extended precision
+  const double* grams[3] = {P, Pddot, Pdot};
+  for (int q = 0; q < 3; ++q)
+    for (int i = 0; i < nb; ++i)
+      for (int j = 0; j < nb; ++j) {
+        long double acc = 0.0L;
+        for (int k = 0; k < n; ++k)
+          acc += (long double)grams[q][(size_t)k * nb + i] * grams[q][(size_t)k * nb + j];
+        h[o + ((size_t)q * nb + i) * kms + j] = (double)acc;
+      }
   o = offs[4] + nM;
   for (int k = 0; k < n; ++k) h[o + k] = tau[k];
   bmpc_ctx* c = new bmpc_ctx();
@@ -238,7 +242,7 @@ static int check_problem(const bmpc_ctx* ctx, const bmpc_problem* p) {
 static int auto_warps(const bmpc_ctx* ctx, int L, int req) {
   int w = req > 0 ? req : (L + ctx->sms - 1) / ctx->sms;
   if (w < 1) w = 1;
-  if (w > 8) w = 8;
+  if (w > BMPC_MAX_WARPS) w = BMPC_MAX_WARPS;
   while (w > 1 && bmpc::am_solve_smem_bytes(ctx->C.nb, ctx->C.npad, ctx->C.kxs, ctx->C.kps, w) >
                       (size_t)ctx->smem_optin)
     --w;
