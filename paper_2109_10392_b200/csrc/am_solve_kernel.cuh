@@ -104,8 +104,8 @@ __device__ __forceinline__ void mbar_wait_parity(unsigned long long* bar, unsign
 }
 
 struct WarpScratch {
-  double* bc;    // 64: KKT right-hand sides (x at 0, y at 32)
-  double* sol;   // 64: [c; mu] of the xy QP, kept across sweeps (x at 0, y at 32)
+  double* bc;    // 64: KKT right-hand sides (x at 0, y at kYOff)
+  double* sol;   // 64: [c; mu] of the xy QP, kept across sweeps (x at 0, y at kYOff)
   double* res;   // 64: refinement residual rhs - K * sol
   double* cxy;   // 32: (c_x[i], c_y[i]) pairs
   double* cp;    // 16: c_psi
@@ -118,6 +118,12 @@ struct WarpScratch {
   double* red;   // 32 x kRedStride: transpose buffer of the sample contractions
 };
 constexpr int kWarpScratch = 288;
+// y-axis offset of the xy KKT vectors in bc/sol/res: odd, so the x-row and
+// y-row lanes' broadcast reads of element j hit different banks
+#ifndef BMPC_YOFF
+#define BMPC_YOFF 33
+#endif
+constexpr int kYOff = BMPC_YOFF;
 constexpr int kRedStride = 33;
 constexpr int kRedSize = 32 * kRedStride;
 
@@ -316,7 +322,7 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
     }
     BMPC_PROF_NS(10);
     const int qstep = js * T.n;
-    constexpr int U = NS == 1 ? 4 : 2;  // obstacles in flight per sample
+    constexpr int U = NS == 1 ? 4 : 2;  // obstacles in flight per sample (NS * U terms)
     const double2* qp[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) qp[s] = T.xi + j0 * T.n + k[s];
@@ -525,7 +531,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int q = lane + 32 * h;
-      if (q < 2 * RX) ws.sol[(q >= RX ? 32 : 0) + q - (q >= RX ? RX : 0)] = cr[5 * NB + q];
+      if (q < 2 * RX) ws.sol[(q >= RX ? kYOff : 0) + q - (q >= RX ? RX : 0)] = cr[5 * NB + q];
     }
     if (lane < RP) ws.solp[lane] = cr[5 * NB + 2 * RX + lane];
     __syncwarp();
@@ -633,7 +639,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
     //     the previous sweep's [c; mu] instead -- the same accuracy
     //     for one matrix pass less.
     {
-      double* rb = ws.bc + (yax ? 32 : 0);
+      double* rb = ws.bc + (yax ? kYOff : 0);
       if (owner) rb[li] = rho * G + lam;
       if (li < 6) rb[NB + li] = bnd;
       __syncwarp();
@@ -643,7 +649,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
           const int q = lane + 32 * h;
           if (q < 2 * RX) {
             const int ax = q >= RX ? 1 : 0, row = q - ax * RX;
-            ws.sol[ax * 32 + row] = kkt_row_dot<RX>(sKxf + row * C.kxs, ws.bc + ax * 32);
+            ws.sol[ax * kYOff + row] = kkt_row_dot<RX>(sKxf + row * C.kxs, ws.bc + ax * kYOff);
           }
         }
         __syncwarp();
@@ -653,8 +659,8 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
         const int q = lane + 32 * h;
         if (q < 2 * RX) {
           const int ax = q >= RX ? 1 : 0, row = q - ax * RX;
-          ws.res[ax * 32 + row] =
-              ws.bc[ax * 32 + row] - kkt_row_dot<RX>(sKxa + row * C.kxs, ws.sol + ax * 32);
+          ws.res[ax * kYOff + row] =
+              ws.bc[ax * kYOff + row] - kkt_row_dot<RX>(sKxa + row * C.kxs, ws.sol + ax * kYOff);
         }
       }
       __syncwarp();
@@ -664,8 +670,8 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
         if (q < 2 * RX) {  // each lane rewrites only its own rows of sol
           const int ax = q >= RX ? 1 : 0, row = q - ax * RX;
           const double s =
-              ws.sol[ax * 32 + row] + kkt_row_dot<RX>(sKxf + row * C.kxs, ws.res + ax * 32);
-          ws.sol[ax * 32 + row] = s;
+              ws.sol[ax * kYOff + row] + kkt_row_dot<RX>(sKxf + row * C.kxs, ws.res + ax * kYOff);
+          ws.sol[ax * kYOff + row] = s;
           if (row < NB) ws.cxy[2 * row + ax] = s;
         }
       }
@@ -1031,7 +1037,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int q = lane + 32 * h;
-      if (q < 2 * RX) cr[5 * NB + q] = ws.sol[(q >= RX ? 32 : 0) + q - (q >= RX ? RX : 0)];
+      if (q < 2 * RX) cr[5 * NB + q] = ws.sol[(q >= RX ? kYOff : 0) + q - (q >= RX ? RX : 0)];
     }
     if (lane < RP) cr[5 * NB + 2 * RX + lane] = ws.solp[lane];
   }
