@@ -643,36 +643,40 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
       if (owner) rb[li] = rho * G + lam;
       if (li < 6) rb[NB + li] = bnd;
       __syncwarp();
+      // rows q = lane and lane + 32 of the stacked (x, y) system: both dot
+      // products are evaluated unconditionally (clamped rows) so they
+      // interleave; only valid rows are stored
+      const int q0 = lane < 2 * RX ? lane : 2 * RX - 1, q1 = lane + 32 < 2 * RX ? lane + 32 : 2 * RX - 1;
+      const int ax0 = q0 >= RX ? 1 : 0, row0 = q0 - ax0 * RX;
+      const int ax1 = q1 >= RX ? 1 : 0, row1 = q1 - ax1 * RX;
+      const int o0 = ax0 * kYOff + row0, o1 = ax1 * kYOff + row1;
+      const bool w0 = lane < 2 * RX, w1 = lane + 32 < 2 * RX;
       if (!have_sol) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int q = lane + 32 * h;
-          if (q < 2 * RX) {
-            const int ax = q >= RX ? 1 : 0, row = q - ax * RX;
-            ws.sol[ax * kYOff + row] = kkt_row_dot<RX>(sKxf + row * C.kxs, ws.bc + ax * kYOff);
-          }
-        }
+        const double d0 = kkt_row_dot<RX>(sKxf + row0 * C.kxs, ws.bc + ax0 * kYOff);
+        const double d1 = kkt_row_dot<RX>(sKxf + row1 * C.kxs, ws.bc + ax1 * kYOff);
+        if (w0) ws.sol[o0] = d0;
+        if (w1) ws.sol[o1] = d1;
         __syncwarp();
       }
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int q = lane + 32 * h;
-        if (q < 2 * RX) {
-          const int ax = q >= RX ? 1 : 0, row = q - ax * RX;
-          ws.res[ax * kYOff + row] =
-              ws.bc[ax * kYOff + row] - kkt_row_dot<RX>(sKxa + row * C.kxs, ws.sol + ax * kYOff);
-        }
+      {
+        const double d0 = kkt_row_dot<RX>(sKxa + row0 * C.kxs, ws.sol + ax0 * kYOff);
+        const double d1 = kkt_row_dot<RX>(sKxa + row1 * C.kxs, ws.sol + ax1 * kYOff);
+        const double r0 = ws.bc[o0] - d0, r1 = ws.bc[o1] - d1;
+        if (w0) ws.res[o0] = r0;
+        if (w1) ws.res[o1] = r1;
       }
       __syncwarp();
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int q = lane + 32 * h;
-        if (q < 2 * RX) {  // each lane rewrites only its own rows of sol
-          const int ax = q >= RX ? 1 : 0, row = q - ax * RX;
-          const double s =
-              ws.sol[ax * kYOff + row] + kkt_row_dot<RX>(sKxf + row * C.kxs, ws.res + ax * kYOff);
-          ws.sol[ax * kYOff + row] = s;
-          if (row < NB) ws.cxy[2 * row + ax] = s;
+      {  // each lane rewrites only its own rows of sol
+        const double d0 = kkt_row_dot<RX>(sKxf + row0 * C.kxs, ws.res + ax0 * kYOff);
+        const double d1 = kkt_row_dot<RX>(sKxf + row1 * C.kxs, ws.res + ax1 * kYOff);
+        const double s0 = ws.sol[o0] + d0, s1 = ws.sol[o1] + d1;
+        if (w0) {
+          ws.sol[o0] = s0;
+          if (row0 < NB) ws.cxy[2 * row0 + ax0] = s0;
+        }
+        if (w1) {
+          ws.sol[o1] = s1;
+          if (row1 < NB) ws.cxy[2 * row1 + ax1] = s1;
         }
       }
       __syncwarp();
