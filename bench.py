@@ -194,13 +194,20 @@ def run_ours(args, rank, world, local_rank):
     sc = D.alloc_score(L, prob.S, dev)
     prec = 1 if args.precision == "fp32" else 0
     opts = nat.SolveOpts(max_iter=iters, tol=0.0, precision=prec)
+    # the device API without host synchronisation: the early-stop decision stays
+    # on the device and {iterations, converged} land in status_dev
+    status_dev = torch.zeros(2, dtype=torch.int32, device=dev)
+    opts_async = nat.SolveOpts(max_iter=iters, tol=0.0, precision=prec, status_dev=status_dev.data_ptr())
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    launches_per_step = 4  # pack_xi, am_solve (+ fused scoring), first_converged, argmin
+    # pack_xi, am_solve (+ fused scoring), first_clear, rerun_plan, am_solve (early-stop
+    # re-run: exits at once when there is none), argmin
+    launches_per_step = 6
 
     def step():
-        # one persistent launch (all sweeps + fused scoring epilogue) + per-scene argmin
+        # the residual history is not requested (plan_batch does not return it)
         out = D.solution_struct(sol)
-        nat.check(lib.bmpc_plan(ctx, ctypes.byref(pstruct), ctypes.byref(opts), ctypes.byref(out),
+        out.history = None
+        nat.check(lib.bmpc_plan(ctx, ctypes.byref(pstruct), ctypes.byref(opts_async), ctypes.byref(out),
                                 ctypes.byref(sspec), ctypes.byref(D.score_struct(sc)), sp))
         return out
 

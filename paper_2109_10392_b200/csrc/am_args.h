@@ -62,6 +62,11 @@ typedef struct {
   double* hist;         // [rows][3][L]
   double* res_final;    // [3][L]
   bmpc_fused_score score;  // used with BMPC_F_SCORE
+  // global early stop (solver.py:437-439): notconv[hist_offset + t] is set to 1
+  // by every instance whose worst residual after sweep t is not <= tol
+  double tol;
+  int* notconv;
+  const int* iters_dev;  // non-NULL: sweep count read on the device (0 = nothing to do)
 } bmpc_solve_args;
 
 // Doubles of carried state per instance: lambda_x, lambda_y, lambda_psi, G_x,

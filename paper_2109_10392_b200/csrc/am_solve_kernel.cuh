@@ -447,6 +447,9 @@ template <int NB, int NKM, bool F32>
 __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bmpc_dev_consts C,
                                                        const bmpc_solve_args A) {
   extern __shared__ __align__(16) double sm[];
+  // device-decided sweep count (the early-stop re-run): 0 = nothing to do
+  const int iters = A.iters_dev ? *A.iters_dev : A.iters;
+  if (iters <= 0) return;
   const int W = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -631,8 +634,8 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
   BMPC_PROF(0);
 
   // ----------------------------------------------------------- AM sweeps ----
-  for (int t = 0; t < A.iters; ++t) {
-    const bool last = t == A.iters - 1;
+  for (int t = 0; t < iters; ++t) {
+    const bool last = t == iters - 1;
     // (1) xy QP: [c; mu] = K^-1 [rho*G + lambda ; b] with one refinement step,
     //     the 2*(nb+6) rows of both axes spread over the lanes (two per lane max).
     //     The first sweep refines the plain inverse apply; later sweeps refine
@@ -974,8 +977,15 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
       lam -= rho * ((a3[0] + a3[1]) - rest);
     }
     if (!yax && owner) lamp -= rho * Lp;
+    const double res = sqrt(lane == 16 ? sqo : (lane == 17 ? sqa : sqn));  // lanes 16..18
+    if (A.notconv) {  // global early stop: flag this sweep unless every residual <= tol
+      const bool nc = __any_sync(BMPC_FULL, lane >= 16 && lane < 19 && !(res <= A.tol));
+      if (lane == 0 && nc) {
+        int* f = A.notconv + A.hist_offset + t;
+        if (*(volatile int*)f == 0) *f = 1;
+      }
+    }
     if (lane >= 16 && lane < 19) {
-      const double res = sqrt(lane == 16 ? sqo : (lane == 17 ? sqa : sqn));
       if (A.flags & BMPC_F_HISTORY)
         A.hist[((size_t)(A.hist_offset + t) * 3 + (lane - 16)) * L + inst] = res;
       if (last && A.res_final) A.res_final[(size_t)(lane - 16) * L + inst] = res;
@@ -988,7 +998,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
   // ------------------------------------------------- fused planner scoring ----
   // sample_plan + filter_candidates + meta_cost of this instance straight from
   // the on-chip coefficients (planner.py:210-245, :412-423; csrc/score.cuh).
-  if ((A.flags & BMPC_F_SCORE) && A.iters > 0) {
+  if (A.flags & BMPC_F_SCORE) {
     const bmpc_fused_score& F = A.score;
     const ScoreParams sp{n, m, F.kind, a, b, F.v_cruise, F.v_max, F.y_rl, F.w1, F.w2,
                          F.heading_limit, F.residual_tol, F.ratio_min};

@@ -50,8 +50,9 @@ cudaError_t op_argmin(int S, int l, const double* meta, const uint8_t* flags, lo
                       long long* best_all, long long* best_hc, long long* nfeas, cudaStream_t st);
 cudaError_t op_pack_xi(long long total, const double* xi_x, const double* xi_y, double* out,
                        cudaStream_t st);
-cudaError_t op_first_converged(int iters, long long L, const double* hist, double tol, int* tstar,
-                               cudaStream_t st);
+cudaError_t op_first_clear(int iters, const int* notconv, int* tstar, cudaStream_t st);
+cudaError_t op_rerun_plan(int max_iter, const int* tstar, int* rerun, int* status, int* status2,
+                          cudaStream_t st);
 cudaError_t dfma_peak_tflops(int reps, double* tflops, cudaStream_t st);
 cudaError_t op_math_check(int fn, long long n, const double* a, const double* b, double* out,
                           double* out2, cudaStream_t st);
@@ -253,7 +254,8 @@ static int auto_warps(const bmpc_ctx* ctx, int L, int req) {
 static int launch_sweeps(bmpc_ctx* ctx, const bmpc_problem* p, const double* xi2,
                          const bmpc_solve_opts* o, int iters, int init_mode, int hist_offset,
                          double* carry, int write_carry, bmpc_solve_out* out, cudaStream_t st,
-                         const bmpc_fused_score* fsc = nullptr) {
+                         const bmpc_fused_score* fsc = nullptr, int* notconv = nullptr,
+                         const int* iters_dev = nullptr) {
   const int L = p->S * p->l;
   bmpc_solve_args A;
   memset(&A, 0, sizeof(A));
@@ -294,6 +296,9 @@ static int launch_sweeps(bmpc_ctx* ctx, const bmpc_problem* p, const double* xi2
   A.v_out = out->v;
   A.hist = out->history;
   A.res_final = out->res_final;
+  A.tol = o->tol;
+  A.notconv = notconv;
+  A.iters_dev = iters_dev;
   if (fsc) {
     A.flags |= BMPC_F_SCORE;
     A.score = *fsc;
@@ -408,50 +413,58 @@ static int solve_impl(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opt
   if (!o || !out) return fail(BMPC_EINVAL, "null opts/out");
   if (o->precision != 0 && o->precision != 1) return fail(BMPC_EINVAL, "precision must be 0 (fp64) or 1 (fp32 obstacle block)");
   if (o->max_iter < 1) return fail(BMPC_EINVAL, "max_iter must be >= 1");
-  if (!out->history || !out->res_final)
-    return fail(BMPC_EINVAL, "history and res_final outputs are required");
+  if (!out->res_final) return fail(BMPC_EINVAL, "the res_final output is required");
   if ((rc = check_warm(o, p))) return rc;
   cudaStream_t st = S_(stream);
   const int L = p->S * p->l;
   const long long tot = (long long)p->S * p->m * ctx->C.n;
   double* xi2 = nullptr;
-  int* tstar = nullptr;
+  // scratch ints: [0] first converged sweep, [1, max_iter] not-converged flags
+  // per sweep, [max_iter + 1] re-run sweep count, [max_iter + 2, + 3] status
+  int* scr = nullptr;
   if (tot > 0) {
     CK(cudaMallocAsync(&xi2, tot * 2 * sizeof(double), st), "cudaMallocAsync");
     CK(bmpc::op_pack_xi(tot, p->xi_x, p->xi_y, xi2, st), "pack_xi");
   }
   const int mode = is_warm(o) ? BMPC_INIT_WARM : BMPC_INIT_COLD;
-  rc = launch_sweeps(ctx, p, xi2, o, o->max_iter, mode, 0, nullptr, 0, out, st, fsc);
-  int iters = o->max_iter, converged = 0;
-  if (!rc && L > 0) {
-    // Global early stop (solver.py:437-439): find the first sweep whose worst
-    // residual is <= tol; when it is not the last one, re-run exactly that many
-    // sweeps (the instances are independent and deterministic, so the re-run
-    // reproduces the same iterates).
-    // The follow-up work is enqueued before the check synchronises, so the
-    // device never idles on the host round trip; it is redone after a re-run.
-    int t = 0;
-    CK(cudaMallocAsync(&tstar, sizeof(int), st), "cudaMallocAsync");
-    CK(cudaMemsetAsync(tstar, 0x7f, sizeof(int), st), "memset");  // "none" = 0x7f7f7f7f
-    CK(bmpc::op_first_converged(o->max_iter, L, out->history, o->tol, tstar, st), "first_converged");
-    CK(cudaMemcpyAsync(&t, tstar, sizeof(int), cudaMemcpyDeviceToHost, st), "memcpy");
-    if (post && (rc = post_solve(post, st))) return rc;
-    CK(cudaStreamSynchronize(st), "sync");
-    if (t < o->max_iter) {
-      converged = 1;
-      iters = t + 1;
-      if (iters < o->max_iter) {
-        rc = launch_sweeps(ctx, p, xi2, o, iters, mode, 0, nullptr, 0, out, st, fsc);
-        if (!rc && post) rc = post_solve(post, st);
-      }
-    }
-  } else if (!rc && post) {
-    rc = post_solve(post, st);
+  const int M = o->max_iter;
+  int status[2] = {M, 0};
+  if (L > 0) {
+    CK(cudaMallocAsync(&scr, (size_t)(M + 4) * sizeof(int), st), "cudaMallocAsync");
+    CK(cudaMemsetAsync(scr, 0x7f, sizeof(int), st), "memset");  // "none" = 0x7f7f7f7f
+    CK(cudaMemsetAsync(scr + 1, 0, (size_t)M * sizeof(int), st), "memset");
   }
+  rc = launch_sweeps(ctx, p, xi2, o, M, mode, 0, nullptr, 0, out, st, fsc, scr ? scr + 1 : nullptr);
+  if (!rc && L > 0) {
+    // Global early stop (solver.py:437-439): the first sweep whose worst
+    // residual over every instance is <= tol.  When it is not the last one the
+    // solve re-runs exactly that many sweeps (instances are independent and
+    // deterministic, so the re-run reproduces the same iterates).  The decision
+    // and the re-run launch stay on the device -- the second launch exits at
+    // once when there is nothing to redo -- so nothing waits on the host.
+    CK(bmpc::op_first_clear(M, scr + 1, scr, st), "first_clear");
+    CK(bmpc::op_rerun_plan(M, scr, scr + M + 1, scr + M + 2, o->status_dev, st), "rerun_plan");
+    rc = launch_sweeps(ctx, p, xi2, o, M, mode, 0, nullptr, 0, out, st, fsc, scr + 1, scr + M + 1);
+  }
+  if (!rc && post) rc = post_solve(post, st);
+  if (!rc && L > 0 && !o->status_dev)
+    CK(cudaMemcpyAsync(status, scr + M + 2, sizeof(status), cudaMemcpyDeviceToHost, st), "memcpy");
   if (xi2) cudaFreeAsync(xi2, st);
-  if (tstar) cudaFreeAsync(tstar, st);
+  if (scr) cudaFreeAsync(scr, st);
   if (rc) return rc;
   CK(cudaGetLastError(), "bmpc_solve");
+  if (o->status_dev) {
+    if (L == 0) {  // nothing ran: report max_iter sweeps, not converged
+      const int h[2] = {M, 0};
+      CK(cudaMemcpyAsync(o->status_dev, h, sizeof(h), cudaMemcpyHostToDevice, st), "memcpy");
+      CK(cudaStreamSynchronize(st), "sync");
+    }
+    out->iterations = -1;
+    out->converged = -1;
+    return BMPC_OK;
+  }
+  CK(cudaStreamSynchronize(st), "sync");
+  const int iters = status[0], converged = status[1];
   out->iterations = iters;
   out->converged = converged;
   return BMPC_OK;
@@ -541,13 +554,14 @@ int bmpc_plan_host(bmpc_ctx* ctx, const bmpc_problem* hp, const bmpc_solve_opts*
   size_t off = 0;
   auto take = [&](size_t bytes) { const size_t at = off; off += (bytes + 15) & ~(size_t)15; return at; };
   const size_t o_xix = take(S * mn * 8), o_xiy = take(S * mn * 8), o_bxy = take(12 * L * 8),
-               o_bps = take(4 * L * 8), o_hist = take(hist * 8), o_lam = take(3 * nb * L * 8),
+               o_bps = take(4 * L * 8), o_hist = take(ho->history ? hist * 8 : 0),
+               o_lam = take(3 * nb * L * 8),
                o_v = take(o->want_v && ho->v ? n * L * 8 : 0);
   const size_t o_res0 = off;  // results block
   const size_t o_coef = take(3 * nb * L * 8), o_rf = take(3 * L * 8);
   const size_t o_meta = take(score ? L * 8 : 0), o_mr = take(score ? L * 8 : 0),
                o_hm = take(score ? L * 8 : 0), o_best = take(score ? 4 * S * 8 : 0),
-               o_fl = take(score ? L : 0);
+               o_fl = take(score ? L : 0), o_stat = take(2 * sizeof(int));
   const size_t res_bytes = off - o_res0;
   DevBuf B(st);
   char* arena = B.alloc<char>(off);
@@ -575,9 +589,14 @@ int bmpc_plan_host(bmpc_ctx* ctx, const bmpc_problem* hp, const bmpc_solve_opts*
   dout.l_x = lam;
   dout.l_y = lam + nb * L;
   dout.l_psi = lam + 2 * nb * L;
-  dout.history = (double*)(arena + o_hist);
+  dout.history = ho->history ? (double*)(arena + o_hist) : nullptr;  // written only on request
   dout.res_final = (double*)(arena + o_rf);
   dout.v = (o->want_v && ho->v) ? (double*)(arena + o_v) : nullptr;
+  // no synchronisation inside the solve: its {iterations, converged} come back
+  // with the results block
+  bmpc_solve_opts o2 = *o;
+  o2.status_dev = (int*)(arena + o_stat);
+  o = &o2;
   bmpc_score_out ds;
   memset(&ds, 0, sizeof(ds));
   if (score) {  // solve with the fused scoring epilogue, then the per-scene argmin
@@ -595,14 +614,12 @@ int bmpc_plan_host(bmpc_ctx* ctx, const bmpc_problem* hp, const bmpc_solve_opts*
     rc = bmpc_solve(ctx, &dp, o, &dout, stream);
   }
   if (rc) return rc;
-  ho->iterations = dout.iterations;
-  ho->converged = dout.converged;
   // rarely requested extras straight to the caller's memory
   struct Cp { void* h; const void* d; size_t bytes; };
   const Cp extra[] = {
       {ho->l_x, dout.l_x, nb * L * 8}, {ho->l_y, dout.l_y, nb * L * 8},
       {ho->l_psi, dout.l_psi, nb * L * 8}, {ho->v, dout.v, n * L * 8},
-      {ho->history, dout.history, (size_t)dout.iterations * 3 * L * 8},
+      {ho->history, dout.history, (size_t)o->max_iter * 3 * L * 8},  // rows past iterations: stale
   };
   for (const Cp& c : extra)
     if (c.h && c.d && c.bytes) CK(cudaMemcpyAsync(c.h, c.d, c.bytes, cudaMemcpyDeviceToHost, st), "d2h");
@@ -618,6 +635,9 @@ int bmpc_plan_host(bmpc_ctx* ctx, const bmpc_problem* hp, const bmpc_solve_opts*
   CK(cudaMemcpyAsync(ctx->stage, arena + o_res0, res_bytes, cudaMemcpyDeviceToHost, st), "d2h");
   CK(cudaStreamSynchronize(st), "sync");
   const char* hb = (const char*)ctx->stage - o_res0;  // arena offset -> staging
+  const int* stat = (const int*)(hb + o_stat);
+  ho->iterations = stat[0];
+  ho->converged = stat[1];
   const Cp res[] = {
       {ho->c_x, hb + o_coef, nb * L * 8}, {ho->c_y, hb + o_coef + nb * L * 8, nb * L * 8},
       {ho->c_psi, hb + o_coef + 2 * nb * L * 8, nb * L * 8}, {ho->res_final, hb + o_rf, 3 * L * 8},

@@ -383,31 +383,14 @@ __global__ void k_pack_xi(long long total, const double* __restrict__ xi_x,
 
 // First iteration t whose worst residual over all instances is <= tol
 // (solver.py:437-439); rows >= iters leave *tstar untouched.
-__global__ void k_first_converged(int iters, long long L, const double* __restrict__ hist,
-                                  double tol, int* tstar) {
-  const int t = blockIdx.x;
-  if (t >= iters) return;
-  double mx = -INFINITY;
-  bool nan = false;
-  const double* row = hist + (size_t)t * 3 * L;
-  for (long long e = threadIdx.x; e < 3 * L; e += blockDim.x) {
-    const double v = row[e];
-    if (v != v) nan = true;
-    mx = fmax(mx, v);
-  }
-  mx = warp_max(mx);
-  nan = __any_sync(BMPC_FULL, nan);
-  __shared__ double sm[32];
-  __shared__ int sn[32];
-  if ((threadIdx.x & 31) == 0) { sm[threadIdx.x >> 5] = mx; sn[threadIdx.x >> 5] = nan; }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double m = -INFINITY;
-    bool anynan = false;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { m = fmax(m, sm[w]); anynan |= sn[w] != 0; }
-    // numpy max propagates NaN, and NaN <= tol is False
-    if (!anynan && m <= tol) atomicMin(tstar, t);
-  }
+// First sweep no instance flagged as not converged (the persistent kernel
+// raises notconv[t] for any worst residual that is not <= tol, NaN included).
+__global__ void k_first_clear(int iters, const int* __restrict__ notconv, int* tstar) {
+  int best = 0x7f7f7f7f;
+  for (int t = threadIdx.x; t < iters; t += blockDim.x)
+    if (notconv[t] == 0) best = min(best, t);
+  for (int o = 16; o >= 1; o >>= 1) best = min(best, __shfl_xor_sync(BMPC_FULL, best, o));
+  if ((threadIdx.x & 31) == 0 && best < 0x7f7f7f7f) atomicMin(tstar, best);
 }
 
 // ---------------------------------------------------------------- launchers --
@@ -495,9 +478,29 @@ cudaError_t op_pack_xi(long long total, const double* xi_x, const double* xi_y, 
     k_pack_xi<<<nblk(total), kTB, 0, st>>>(total, xi_x, xi_y, reinterpret_cast<double2*>(out));
   return cudaGetLastError();
 }
-cudaError_t op_first_converged(int iters, long long L, const double* hist, double tol, int* tstar,
-                               cudaStream_t st) {
-  if (iters > 0) k_first_converged<<<iters, 256, 0, st>>>(iters, L, hist, tol, tstar);
+// Device-side early-stop decision: the re-run sweep count (0 = none) and the
+// {iterations, converged} status of the solve.
+__global__ void k_rerun_plan(int max_iter, const int* tstar, int* rerun, int* status, int* status2) {
+  const int t = *tstar;
+  const bool conv = t < max_iter;
+  const int iters = conv ? t + 1 : max_iter;
+  *rerun = (conv && iters < max_iter) ? iters : 0;
+  status[0] = iters;
+  status[1] = conv ? 1 : 0;
+  if (status2) {
+    status2[0] = iters;
+    status2[1] = conv ? 1 : 0;
+  }
+}
+
+cudaError_t op_rerun_plan(int max_iter, const int* tstar, int* rerun, int* status, int* status2,
+                          cudaStream_t st) {
+  k_rerun_plan<<<1, 1, 0, st>>>(max_iter, tstar, rerun, status, status2);
+  return cudaGetLastError();
+}
+
+cudaError_t op_first_clear(int iters, const int* notconv, int* tstar, cudaStream_t st) {
+  if (iters > 0) k_first_clear<<<1, 256, 0, st>>>(iters, notconv, tstar);
   return cudaGetLastError();
 }
 

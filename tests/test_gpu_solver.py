@@ -314,3 +314,56 @@ def test_fused_scoring_equals_standalone(cuda):
     for k in ("meta_cost", "min_ratio", "heading_max", "flags", "best_index", "argmin_all",
               "argmin_hc", "n_feasible"):
         assert cuda.equal(getattr(fused, k), getattr(alone, k)), k
+
+
+@pytest.mark.parametrize("tol_mode", ["none", "early"])
+def test_async_plan_matches_sync(cuda, tol_mode):
+    """bmpc_plan with status_dev (no host synchronisation; the early-stop re-run
+    decided on the device) == the synchronous call, bit for bit, and the
+    device status carries {iterations, converged}."""
+    import ctypes
+
+    from paper_2109_10392_b200 import _native as nat
+    from paper_2109_10392_b200 import device as D
+    from paper_2109_10392_b200.planner import FilterLimits, MetaCostSpec, _spec_struct
+
+    z = golden("c0")
+    solver = _solver(z)
+    S = _Scenes(z)
+    prob = D.DeviceProblem.from_host(int(z["n"]), S.xi_x, S.xi_y, S.b_xy, S.b_psi, S.l, S.a, S.b,
+                                     S.v_min, S.v_max, S.a_max)
+    spec = _spec_struct(MetaCostSpec("cruise", v_cruise=20.0), FilterLimits())
+    lib, ctx = nat.load(), solver._context()
+    sp = ctypes.c_void_p(D.stream_ptr())
+    dev = prob.b_xy.device
+    tol = 0.0
+    if tol_mode == "early":  # a tolerance first met at sweep 25 of 60
+        sol = D.alloc_solution(solver.basis.n_b, solver.basis.grid.n, prob.L, 60, False, dev)
+        nat.check(lib.bmpc_solve(ctx, ctypes.byref(prob.c_struct()), ctypes.byref(nat.SolveOpts(max_iter=60)),
+                                 ctypes.byref(D.solution_struct(sol)), sp))
+        worst = sol.history.amax(dim=(1, 2)).cpu().numpy()
+        tol = float(worst[24]) * (1 + 1e-9)
+    results = []
+    for use_async in (False, True):
+        sol = D.alloc_solution(solver.basis.n_b, solver.basis.grid.n, prob.L, 60, False, dev)
+        sc = D.alloc_score(prob.L, prob.S, dev)
+        status = cuda.full((2,), -5, dtype=cuda.int32, device=dev)
+        opts = nat.SolveOpts(max_iter=60, tol=tol, status_dev=status.data_ptr() if use_async else None)
+        out = D.solution_struct(sol)
+        nat.check(lib.bmpc_plan(ctx, ctypes.byref(prob.c_struct()), ctypes.byref(opts), ctypes.byref(out),
+                                ctypes.byref(spec), ctypes.byref(D.score_struct(sc)), sp))
+        cuda.cuda.synchronize()
+        it, conv = (out.iterations, out.converged) if not use_async else tuple(status.cpu().tolist())
+        if use_async:
+            assert out.iterations == -1
+        results.append((it, conv, sol, sc))
+    (i0, c0, s0, k0), (i1, c1, s1, k1) = results
+    assert (i0, c0) == (i1, c1)
+    if tol_mode == "early":
+        assert i0 == int(np.argmax(worst <= tol)) + 1 and c0 == 1
+    else:
+        assert (i0, c0) == (60, 0)
+    for k in ("c_x", "c_y", "c_psi", "res_final"):
+        assert cuda.equal(getattr(s0, k), getattr(s1, k)), k
+    for k in ("meta_cost", "flags", "best_index", "argmin_all", "argmin_hc"):
+        assert cuda.equal(getattr(k0, k), getattr(k1, k)), k
