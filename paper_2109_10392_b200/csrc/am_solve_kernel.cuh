@@ -27,6 +27,8 @@
 #include <cuda_runtime.h>
 #include <stdio.h>
 
+#include <type_traits>
+
 #include "am_args.h"
 #include "common.cuh"
 #include "score.cuh"
@@ -702,23 +704,24 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
       bool wrap = false;
       double prev_last = 0.0;  // theta of sample 32 r - 1: lane 31 of the previous slot
       const double amax2 = A.a_max * A.a_max;
-#pragma unroll 1  // chunks stay rolled: instruction-cache footprint
-      for (int r0 = 0; r0 < NKM; r0 += CH) {
-        int k[CH];
-        bool v[CH];
-        double xx[CH], yy[CH], xd[CH], yd[CH], xdd[CH], ydd[CH];
+      // full chunks of CH slots (every slot valid at compile time), then the
+      // NKM % CH remainder; chunks stay rolled for the instruction cache
+      auto chunk_a = [&](auto nsc, const int r0) {
+        constexpr int NSC = decltype(nsc)::value;
+        int k[NSC];
+        bool v[NSC];
+        double xx[NSC], yy[NSC], xd[NSC], yd[NSC], xdd[NSC], ydd[NSC];
 #pragma unroll
-        for (int s = 0; s < CH; ++s) {
-          k[s] = lane + 32 * (r0 + s < NKM ? r0 + s : 0);
-          v[s] = r0 + s < NKM && k[s] < n;
+        for (int s = 0; s < NSC; ++s) {
+          k[s] = lane + 32 * (r0 + s);
+          v[s] = k[s] < n;
           xx[s] = yy[s] = xd[s] = yd[s] = xdd[s] = ydd[s] = 0.0;
         }
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
           const double2 c = cxy[i];
 #pragma unroll
-          for (int s = 0; s < CH; ++s) {
-            if (r0 + s >= NKM) continue;
+          for (int s = 0; s < NSC; ++s) {
             const double p = sP[i * npad + k[s]], pd = sPd[i * npad + k[s]],
                          pdd = sPdd[i * npad + k[s]];
             xx[s] = fma(p, c.x, xx[s]);
@@ -729,13 +732,12 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
             ydd[s] = fma(pdd, c.y, ydd[s]);
           }
         }
-        double th[CH];
-        bool clip[CH], anyclip = false;
+        double th[NSC];
+        bool clip[NSC], anyclip = false;
 #pragma unroll
-        for (int s = 0; s < CH; ++s) {
+        for (int s = 0; s < NSC; ++s) {
           th[s] = 0.0;
           clip[s] = false;
-          if (r0 + s >= NKM) continue;
           th[s] = atan2_nb(yd[s], xd[s]);
           double prev = __shfl_up_sync(BMPC_FULL, th[s], 1);
           const double last = __shfl_sync(BMPC_FULL, th[s], 31);
@@ -760,17 +762,15 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
 #pragma unroll
-          for (int s = 0; s < CH; ++s) {
-            if (r0 + s >= NKM) continue;
+          for (int s = 0; s < NSC; ++s) {
             pt[i] = fma(sP[i * npad + k[s]], th[s], pt[i]);
           }
         }
         if (__any_sync(BMPC_FULL, anyclip)) {  // clipped samples: g = a_max (cos, sin)
-          double ex[CH], ey[CH];  // g_acc - acc
+          double ex[NSC], ey[NSC];  // g_acc - acc
 #pragma unroll
-          for (int s = 0; s < CH; ++s) {
+          for (int s = 0; s < NSC; ++s) {
             ex[s] = ey[s] = 0.0;
-            if (r0 + s >= NKM) continue;
             const double m2 = fma(xdd[s], xdd[s], ydd[s] * ydd[s]);
             const double mi = rsqrt_nb(m2);
             const double dx = A.a_max * (xdd[s] * mi) - xdd[s], dy = A.a_max * (ydd[s] * mi) - ydd[s];
@@ -781,15 +781,17 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
 #pragma unroll
           for (int i = 0; i < NB; ++i) {
 #pragma unroll
-            for (int s = 0; s < CH; ++s) {
-              if (r0 + s >= NKM) continue;
-              const double pdd = sPdd[i * npad + k[s]];
+            for (int s = 0; s < NSC; ++s) {
+                const double pdd = sPdd[i * npad + k[s]];
               Gx[i] = fma(pdd, ex[s], Gx[i]);
               Gy[i] = fma(pdd, ey[s], Gy[i]);
             }
           }
         }
-      }
+      };
+#pragma unroll 1
+      for (int r0 = 0; r0 + CH <= NKM; r0 += CH) chunk_a(std::integral_constant<int, CH>{}, r0);
+      if constexpr (NKM % CH != 0) chunk_a(std::integral_constant<int, NKM % CH>{}, NKM - NKM % CH);
       BMPC_PROF(2);
       if (__any_sync(BMPC_FULL, wrap)) {  // rare: exact numpy unwrap, then P^T theta again
         __syncwarp();
@@ -873,46 +875,46 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
 
     // (5) pass B: psi = P c_psi and the non-holonomic block (_speedups.pyx:200-216),
     //     contracted onto Pdot.
-#pragma unroll 1  // chunks stay rolled: instruction-cache footprint
-    for (int r0 = 0; r0 < NKM; r0 += CH) {
-      int k[CH];
-      bool v[CH];
-      double ps[CH];
+    // full chunks of CH slots (every slot valid at compile time), then the
+    // NKM % CH remainder; chunks stay rolled for the instruction cache
+    auto chunk_b = [&](auto nsc, const int r0) {
+      constexpr int NSC = decltype(nsc)::value;
+      int k[NSC];
+      bool v[NSC];
+      double ps[NSC];
 #pragma unroll
-      for (int s = 0; s < CH; ++s) {
-        k[s] = lane + 32 * (r0 + s < NKM ? r0 + s : 0);
-        v[s] = r0 + s < NKM && k[s] < n;
+      for (int s = 0; s < NSC; ++s) {
+        k[s] = lane + 32 * (r0 + s);
+        v[s] = k[s] < n;
         ps[s] = 0.0;
       }
 #pragma unroll
       for (int i = 0; i < NB; ++i) {
         const double cpi = ws.cp[i];
 #pragma unroll
-        for (int s = 0; s < CH; ++s)
-          if (r0 + s < NKM) ps[s] = fma(sP[i * npad + k[s]], cpi, ps[s]);
+        for (int s = 0; s < NSC; ++s)
+          ps[s] = fma(sP[i * npad + k[s]], cpi, ps[s]);
       }
       // branch-free sin/cos for every slot first, so the slots interleave; the
       // full-range fallback (huge / non-finite headings) is one rare branch
-      double sps[CH], cps[CH];
+      double sps[NSC], cps[NSC];
       bool big = false;
 #pragma unroll
-      for (int s = 0; s < CH; ++s) {
+      for (int s = 0; s < NSC; ++s) {
         sps[s] = 0.0;
         cps[s] = 1.0;
-        if (r0 + s >= NKM) continue;
         sincos_nb(ps[s], &sps[s], &cps[s]);
         big |= !(fabs(ps[s]) < 1.0e5);
       }
       if (big) {
 #pragma unroll
-        for (int s = 0; s < CH; ++s)
-          if (r0 + s < NKM && !(fabs(ps[s]) < 1.0e5)) sincos(ps[s], &sps[s], &cps[s]);
+        for (int s = 0; s < NSC; ++s)
+          if (!(fabs(ps[s]) < 1.0e5)) sincos(ps[s], &sps[s], &cps[s]);
       }
-      double gnx[CH], gny[CH], vv[CH];
+      double gnx[NSC], gny[NSC], vv[NSC];
 #pragma unroll
-      for (int s = 0; s < CH; ++s) {
+      for (int s = 0; s < NSC; ++s) {
         gnx[s] = gny[s] = vv[s] = 0.0;
-        if (r0 + s >= NKM) continue;
         const double xd = v[s] ? ws.xd[k[s]] : 0.0, yd = v[s] ? ws.yd[k[s]] : 0.0;
         const double s2 = fma(xd, xd, yd * yd);
         double u = s2 * rsqrt_nb(s2);
@@ -926,20 +928,22 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
       }
       if (last && (A.flags & BMPC_F_V)) {
 #pragma unroll
-        for (int s = 0; s < CH; ++s)
+        for (int s = 0; s < NSC; ++s)
           if (v[s]) A.v_out[(size_t)k[s] * L + inst] = vv[s];
       }
 #pragma unroll
       for (int i = 0; i < NB; ++i) {
 #pragma unroll
-        for (int s = 0; s < CH; ++s) {
-          if (r0 + s >= NKM) continue;
+        for (int s = 0; s < NSC; ++s) {
           const double pd = sPd[i * npad + k[s]];
           Gx[i] = fma(pd, gnx[s], Gx[i]);
           Gy[i] = fma(pd, gny[s], Gy[i]);
         }
       }
-    }
+    };
+#pragma unroll 1
+    for (int r0 = 0; r0 + CH <= NKM; r0 += CH) chunk_b(std::integral_constant<int, CH>{}, r0);
+    if constexpr (NKM % CH != 0) chunk_b(std::integral_constant<int, NKM % CH>{}, NKM - NKM % CH);
     BMPC_PROF(12);
 
     // (6) G = F_axis^T g = m (P^T P) c + (Pddot^T Pddot) c + the lane partials
