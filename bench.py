@@ -104,6 +104,13 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows), "source": "nvml"}
 
 
+def _coll_device(dev):
+    """Device of the bench's scalar collectives: the GPU under NCCL, host under gloo."""
+    import torch.distributed as dist
+
+    return dev if dist.get_backend() == "nccl" else "cpu"
+
+
 # ------------------------------------------------------------- workloads ----
 def make_step_workload(cfg_name: str, world: int, rank: int):
     from paper_2109_10392_b200.scenes import CONFIGS, make_workload
@@ -172,6 +179,7 @@ def run_ours(args, rank, world, local_rank):
     from paper_2109_10392_b200 import make_solver
     from paper_2109_10392_b200.planner import FilterLimits, MetaCostSpec, _spec_struct, plan_batch
 
+    local_rank = local_rank % max(1, torch.cuda.device_count())  # see main(): gloo smoke test
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     cfg, W, offset = make_step_workload(args.config, world, rank)
@@ -244,7 +252,7 @@ def run_ours(args, rank, world, local_rank):
 
         rec = local_winner(sc.meta_cost.cpu().numpy(), sc.flags.cpu().numpy() == 7, offset)
         best_local, _ = allgather_winner(rec)
-        tt = torch.tensor([t_local], dtype=torch.float64, device=dev)
+        tt = torch.tensor([t_local], dtype=torch.float64, device=_coll_device(dev))
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         t_max = float(tt.item())
     else:
@@ -291,7 +299,7 @@ def run_ours(args, rank, world, local_rank):
         best_e2e = res.best_index[0]
     e2e_local = sum(e2e_ms)
     if world > 1:
-        tt = torch.tensor([e2e_local], dtype=torch.float64, device=dev)
+        tt = torch.tensor([e2e_local], dtype=torch.float64, device=_coll_device(dev))
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         e2e_local = float(tt.item())
     e2e_value = total_problems / (e2e_local / 1e3)
@@ -414,8 +422,16 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        # one process per GPU over NCCL; BMPC_DIST_BACKEND=gloo lets a single-GPU
+        # box smoke-test the multi-rank plumbing (ranks then share the device and
+        # the tiny collectives run on host tensors)
+        backend = os.environ.get("BMPC_DIST_BACKEND", "nccl")
+        dev_index = local_rank % max(1, torch.cuda.device_count())
+        torch.cuda.set_device(dev_index)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group(backend)
     if args.impl == "reference":
         run_reference(args, rank, world)
     else:
