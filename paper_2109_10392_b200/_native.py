@@ -87,6 +87,7 @@ EXPORTS = {
     "bmpc_plan": ([c_void_p, POINTER(Problem), POINTER(SolveOpts), POINTER(SolveOut),
                    POINTER(ScoreSpec), POINTER(ScoreOut), c_void_p], c_int),
     "bmpc_sample": ([c_void_p, c_int] + [c_void_p] * 12 + [c_void_p], c_int),
+    "bmpc_assemble": ([c_void_p, c_int, c_int, c_int, c_int] + [c_void_p] * 9 + [c_void_p], c_int),
     "bmpc_op_obstacle_update": ([c_int, c_int, c_int] + [c_void_p] * 4 + [c_double, c_double]
                                 + [c_void_p] * 2 + [c_void_p], c_int),
     "bmpc_op_accel_update": ([c_int, c_int, c_void_p, c_void_p, c_double, c_void_p, c_void_p, c_void_p], c_int),

@@ -51,6 +51,9 @@ cudaError_t op_argmin(int S, int l, const double* meta, const uint8_t* flags, lo
 cudaError_t op_pack_xi(long long total, const double* xi_x, const double* xi_y, double* out,
                        cudaStream_t st);
 cudaError_t op_first_clear(int iters, const int* notconv, int* tstar, cudaStream_t st);
+cudaError_t op_assemble(int S, int V, int m, int n, int l, const double* veh, const int* nveh,
+                        const double* ego, const double* goals, const double* rel, double* xi_x,
+                        double* xi_y, double* b_xy, double* b_psi, cudaStream_t st);
 cudaError_t op_rerun_plan(int max_iter, const int* tstar, int* rerun, int* status, int* status2,
                           cudaStream_t st);
 cudaError_t dfma_peak_tflops(int reps, double* tflops, cudaStream_t st);
@@ -523,6 +526,21 @@ int bmpc_score(bmpc_ctx* ctx, const bmpc_problem* p, const double* c_x, const do
                        out->argmin_hc, out->n_feasible, st),
        "argmin");
   if (xi2) cudaFreeAsync(xi2, st);
+  return BMPC_OK;
+}
+
+int bmpc_assemble(bmpc_ctx* ctx, int S, int V, int m, int l, const double* veh, const int* nveh,
+                  const double* ego, const double* goals, const double* rel, double* xi_x,
+                  double* xi_y, double* b_xy, double* b_psi, void* stream) {
+  if (!ctx || S < 0 || V < 0 || m < 0 || l < 0) return fail(BMPC_EINVAL, "bmpc_assemble: bad size");
+  if ((S > 0 && (!ego || !nveh || (V > 0 && !veh))) || (m > 0 && (!rel || !xi_x || !xi_y)) ||
+      (l > 0 && (!goals || !b_xy || !b_psi)))
+    return fail(BMPC_EINVAL, "bmpc_assemble: null argument");
+  if ((size_t)(V + 4 * m) * sizeof(double) > 48 * 1024)
+    return fail(BMPC_EINVAL, "bmpc_assemble: V + 4m too large (shared-memory staging)");
+  CK(bmpc::op_assemble(S, V, m, ctx->C.n, l, veh, nveh, ego, goals, rel, xi_x, xi_y, b_xy, b_psi,
+                       S_(stream)),
+     "assemble");
   return BMPC_OK;
 }
 

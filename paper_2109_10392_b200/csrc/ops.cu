@@ -532,3 +532,76 @@ cudaError_t op_math_check(int fn, long long n, const double* a, const double* b,
   return cudaGetLastError();
 }
 }  // namespace bmpc
+
+// ------------------------------------------------------- scene assembly --
+// Device-side build_batch for S stacked scenes (planner.py:336-360,
+// traffic.py:199-233): select_nearest (stable sort by squared distance, pad
+// with virtual vehicles at ego + 1e4), predict_constant_velocity
+// (x + vx * (t_k - t_0)) and boundary_vectors.  Same roundings as the
+// reference's Python/numpy (this unit is compiled with -fmad=false).
+namespace bmpc {
+__global__ void k_assemble_xi(int S, int V, int m, int n, const double* __restrict__ veh,
+                              const int* __restrict__ nveh, const double* __restrict__ ego,
+                              const double* __restrict__ rel, double* xi_x, double* xi_y) {
+  extern __shared__ double sh[];
+  double* d = sh;                        // V squared distances
+  double* pick = sh + V;                 // m x 4 picked states
+  const int s = blockIdx.x;
+  const int nv = min(nveh[s], V);
+  const double ex = ego[s * 8 + 0], ey = ego[s * 8 + 3];
+  const double* vs = veh + (size_t)s * V * 4;
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+    const double dx = __dadd_rn(vs[i * 4 + 0], -ex), dy = __dadd_rn(vs[i * 4 + 1], -ey);
+    d[i] = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+  }
+  for (int j = threadIdx.x; j < m; j += blockDim.x) {  // virtual padding
+    pick[j * 4 + 0] = __dadd_rn(ex, 1.0e4);
+    pick[j * 4 + 1] = __dadd_rn(ey, 1.0e4);
+    pick[j * 4 + 2] = 0.0;
+    pick[j * 4 + 3] = 0.0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) {  // stable rank = sorted position
+    const double di = d[i];
+    int r = 0;
+    for (int j = 0; j < nv; ++j) r += (d[j] < di) || (d[j] == di && j < i);
+    if (r < m)
+      for (int q = 0; q < 4; ++q) pick[r * 4 + q] = vs[i * 4 + q];
+  }
+  __syncthreads();
+  const size_t base = (size_t)s * m * n;
+  for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
+    const int j = e / n, k = e - j * n;
+    xi_x[base + e] = __dadd_rn(pick[j * 4 + 0], __dmul_rn(pick[j * 4 + 2], rel[k]));
+    xi_y[base + e] = __dadd_rn(pick[j * 4 + 1], __dmul_rn(pick[j * 4 + 3], rel[k]));
+  }
+}
+
+__global__ void k_assemble_b(int S, int l, const double* __restrict__ ego,
+                             const double* __restrict__ goals, double* b_xy, double* b_psi) {
+  const long long L = (long long)S * l;
+  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= L) return;
+  const double* e = ego + (c / l) * 8;
+  const double* g = goals + c * 6;
+  const double col[12] = {e[0], e[1], e[2], g[0], g[1], g[2], e[3], e[4], e[5], g[3], g[4], g[5]};
+#pragma unroll
+  for (int r = 0; r < 12; ++r) b_xy[r * L + c] = col[r];
+  b_psi[0 * L + c] = e[6];
+  b_psi[1 * L + c] = e[7];
+  b_psi[2 * L + c] = 0.0;
+  b_psi[3 * L + c] = 0.0;
+}
+
+cudaError_t op_assemble(int S, int V, int m, int n, int l, const double* veh, const int* nveh,
+                        const double* ego, const double* goals, const double* rel, double* xi_x,
+                        double* xi_y, double* b_xy, double* b_psi, cudaStream_t st) {
+  if (S > 0 && m > 0) {
+    const size_t smem = (size_t)(V + 4 * m) * sizeof(double);
+    k_assemble_xi<<<S, 256, smem, st>>>(S, V, m, n, veh, nveh, ego, rel, xi_x, xi_y);
+  }
+  const long long L = (long long)S * l;
+  if (L > 0) k_assemble_b<<<nblk(L), kTB, 0, st>>>(S, l, ego, goals, b_xy, b_psi);
+  return cudaGetLastError();
+}
+}  // namespace bmpc

@@ -141,3 +141,47 @@ def peak_fp64_tflops(reps: int = 5) -> float:
     nat.check(nat.load().bmpc_dfma_peak(reps, ctypes.byref(out), ctypes.c_void_p(stream_ptr())),
               "dfma_peak")
     return out.value
+
+
+def assemble_scenes(solver, egos, vehicles, goals, m: int, a: float, b: float, v_min: float,
+                    v_max: float, a_max: float, device=None, stream=None) -> DeviceProblem:
+    """build_batch for S scenes on the device (`bmpc_assemble`): the m nearest
+    vehicles of each scene, their constant-velocity predictions and the
+    boundary vectors of its goals (planner.py:336-360, traffic.py:199-233).
+
+    egos: S EgoState; vehicles: S lists of VehicleState; goals: S lists of
+    Goal (the same count l each).  Host data is packed into small state
+    arrays -- (S, V, 4) vehicles, (S, 8) egos, (S*l, 6) goals -- instead of the
+    (S, m*n) prediction tables, which are built on the device."""
+    torch = _torch()
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    S = len(egos)
+    if len(vehicles) != S or len(goals) != S:
+        raise ValueError("one vehicle list and one goal list per ego state")
+    l = len(goals[0]) if S else 0
+    if any(len(g) != l for g in goals):
+        raise ValueError("every scene needs the same number of goals")
+    V = max([len(v) for v in vehicles] + [1])
+    veh = np.zeros((S, V, 4))
+    nveh = np.array([len(v) for v in vehicles], dtype=np.int32)
+    for s, vs in enumerate(vehicles):
+        for i, v in enumerate(vs):
+            veh[s, i] = (v.x, v.y, v.vx, v.vy)
+    ego = np.array([[e.x, e.vx, e.ax, e.y, e.vy, e.ay, e.psi, e.psidot] for e in egos],
+                   dtype=np.float64).reshape(S, 8)
+    gl = np.array([[g.x, g.vx, g.ax, g.y, g.vy, g.ay] for gs in goals for g in gs],
+                  dtype=np.float64).reshape(S * l, 6)
+    times = np.asarray(solver.basis.grid.times, dtype=np.float64)
+    rel = times - times[0]
+    n = times.shape[0]
+    up = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev)  # noqa: E731
+    d_veh, d_nveh, d_ego, d_goals, d_rel = up(veh), up(nveh), up(ego), up(gl), up(rel)
+    f64 = lambda *shape: torch.empty(*shape, dtype=torch.float64, device=dev)  # noqa: E731
+    xi_x, xi_y = f64(S, m * n), f64(S, m * n)
+    b_xy, b_psi = f64(12, S * l), f64(4, S * l)
+    nat.check(nat.load().bmpc_assemble(solver._context(), S, V, m, l, ptr(d_veh), ptr(d_nveh),
+                                       ptr(d_ego), ptr(d_goals), ptr(d_rel), ptr(xi_x), ptr(xi_y),
+                                       ptr(b_xy), ptr(b_psi), ctypes.c_void_p(stream_ptr(stream))),
+              "assemble")
+    return DeviceProblem(m=m, l=l, S=S, xi_x=xi_x, xi_y=xi_y, b_xy=b_xy, b_psi=b_psi, a=float(a),
+                         b=float(b), v_min=float(v_min), v_max=float(v_max), a_max=float(a_max))
