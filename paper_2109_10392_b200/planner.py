@@ -530,3 +530,44 @@ def plan_batch(solver: BatchSolver, scenes, max_iter: int = 100, tol: float = 0.
                       best_index=[int(b) if b >= 0 else None for b in best], argmin_all=amin,
                       argmin_hc=ahc, n_feasible=nf, iterations=out.iterations,
                       converged=bool(out.converged))
+
+
+def plan_states(solver: BatchSolver, egos, vehicles, goals, cfg: "PlannerConfig | None" = None,
+                max_iter: int | None = None, tol: float = 0.0, spec: MetaCostSpec | None = None,
+                limits: FilterLimits | None = None, precision: str = "fp64",
+                stream=None) -> PlanResult:
+    """Plan S scenes straight from their ego / vehicle / goal states: the scene
+    assembly (select_nearest, constant-velocity prediction, boundary vectors)
+    runs on the device (`bmpc_assemble`), then solve + fused scoring + argmin
+    (`bmpc_plan`).  Only the small state arrays cross the host link -- not the
+    (S, m*n) prediction tables the host build_batch path uploads.
+    """
+    from . import device as D
+
+    cfg = cfg or PlannerConfig()
+    limits = limits or FilterLimits()
+    spec = spec or MetaCostSpec("cruise", v_cruise=20.0)
+    max_iter = int(max_iter if max_iter is not None else cfg.max_iter)
+    prob = D.assemble_scenes(solver, egos, vehicles, goals, cfg.m, cfg.a, cfg.b, cfg.v_min,
+                             cfg.v_max, cfg.a_max, stream=stream)
+    dev = prob.b_xy.device
+    nb, n = solver.basis.n_b, solver.basis.grid.n
+    sol = D.alloc_solution(nb, n, prob.L, max_iter, False, dev)
+    sc = D.alloc_score(prob.L, prob.S, dev)
+    out = D.solution_struct(sol)
+    out.history = None
+    opts = nat.SolveOpts(max_iter=max_iter, tol=float(tol), precision=_precision_code(precision))
+    nat.check(nat.load().bmpc_plan(solver._context(), ctypes.byref(prob.c_struct()), ctypes.byref(opts),
+                                   ctypes.byref(out), ctypes.byref(_spec_struct(spec, limits)),
+                                   ctypes.byref(D.score_struct(sc)), ctypes.c_void_p(D.stream_ptr(stream))),
+              "plan_states")
+    solver.kkt.n_solves += 2 * out.iterations
+    h = lambda t: t.cpu().numpy()  # noqa: E731
+    best = h(sc.best_index)
+    return PlanResult(c_x=h(sol.c_x), c_y=h(sol.c_y), c_psi=h(sol.c_psi), res_final=h(sol.res_final),
+                      meta_cost=h(sc.meta_cost), min_ratio=h(sc.min_ratio),
+                      heading_max=h(sc.heading_max), flags=h(sc.flags),
+                      best_index=[int(x) if x >= 0 else None for x in best],
+                      argmin_all=h(sc.argmin_all), argmin_hc=h(sc.argmin_hc),
+                      n_feasible=h(sc.n_feasible), iterations=out.iterations,
+                      converged=bool(out.converged))

@@ -50,3 +50,44 @@ def test_assemble_matches_host(cuda):
                 prob.b_xy[:, c].cpu().numpy(),
                 [e.x, e.vx, e.ax, g.x, g.vx, g.ax, e.y, e.vy, e.ay, g.y, g.vy, g.ay])
             np.testing.assert_array_equal(prob.b_psi[:, c].cpu().numpy(), [e.psi, e.psidot, 0.0, 0.0])
+
+
+def test_plan_states_equals_host_path(cuda):
+    """plan_states (device assembly) == plan_batch over the host-assembled
+    scenes, bit for bit."""
+    from paper_2109_10392_b200 import make_solver
+    from paper_2109_10392_b200.planner import (EgoState, FilterLimits, MetaCostSpec, PlannerConfig,
+                                               plan_batch, plan_states, sample_goals_uniform)
+    from paper_2109_10392_b200.traffic import VehicleState, predict_constant_velocity, select_nearest
+
+    rng = np.random.default_rng(3)
+    cfg = PlannerConfig(m=10, t_f=5.0, v_max=35.0, b=2.4)
+    solver = make_solver(cfg.n, cfg.t_f, cfg.degree, cfg.m)
+    egos, vehs, goals = [], [], []
+    for s in range(3):
+        ego = EgoState(x=0.0, y=float(rng.choice([-5.25, -1.75, 1.75, 5.25])), vx=float(rng.uniform(15, 25)))
+        vs = [VehicleState(id=i, x=float(rng.uniform(-30, 120)), y=float(rng.choice([-5.25, -1.75, 1.75, 5.25])),
+                           vx=float(rng.uniform(10, 25)), vy=0.0, lane=0) for i in range(14)]
+        egos.append(ego)
+        vehs.append(vs)
+        goals.append(sample_goals_uniform(rng, ego, 64, cfg.t_f))
+    spec, limits = MetaCostSpec("cruise", v_cruise=20.0), FilterLimits()
+    dev = plan_states(solver, egos, vehs, goals, cfg, max_iter=40, tol=0.0, spec=spec, limits=limits)
+
+    class Scenes:
+        pass
+
+    sc = Scenes()
+    xs, ys = zip(*(predict_constant_velocity(select_nearest(v, e.x, e.y, cfg.m), solver.basis.grid.times)
+                   for e, v in zip(egos, vehs)))
+    sc.xi_x, sc.xi_y = np.stack(xs), np.stack(ys)
+    cols = [(e, g) for e, gs in zip(egos, goals) for g in gs]
+    sc.b_xy = np.array([[e.x, e.vx, e.ax, g.x, g.vx, g.ax, e.y, e.vy, e.ay, g.y, g.vy, g.ay]
+                        for e, g in cols]).T.copy()
+    sc.b_psi = np.array([[e.psi, e.psidot, 0.0, 0.0] for e, _ in cols]).T.copy()
+    sc.l, sc.S = 64, 3
+    sc.a, sc.b, sc.v_min, sc.v_max, sc.a_max = cfg.a, cfg.b, cfg.v_min, cfg.v_max, cfg.a_max
+    host = plan_batch(solver, sc, max_iter=40, tol=0.0, spec=spec, limits=limits)
+    for k in ("c_x", "c_y", "c_psi", "res_final", "meta_cost", "flags", "argmin_all", "argmin_hc"):
+        np.testing.assert_array_equal(getattr(dev, k), getattr(host, k), err_msg=k)
+    assert dev.best_index == host.best_index and dev.iterations == host.iterations == 40
