@@ -56,6 +56,7 @@ typedef struct {
   // warm start (BMPC_INIT_WARM), reference AmState layouts (rows, L)
   const double *w_alpha, *w_d, *w_alpha_a, *w_d_a, *w_v, *w_cpsi;
   const double *w_lx, *w_ly, *w_lp;   // may be NULL (zero multipliers)
+  const unsigned char* w_mask;        // may be NULL (every instance warm); 0 = cold
   double* carry;        // [L][5*nb]: lambda_x, lambda_y, lambda_psi, G_x, G_y
   double *c_x, *c_y, *c_psi, *l_x, *l_y, *l_psi;  // (nb, L)
   double* v_out;        // (n, L)

@@ -547,7 +547,9 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
     double ax[16], ay[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) { ax[i] = 0.0; ay[i] = 0.0; }
-    const bool cold = A.init_mode == BMPC_INIT_COLD;
+    // warm starts may cover only some instances (the planner's eligible
+    // columns, planner.py:362-410); the rest start cold
+    const bool cold = A.init_mode == BMPC_INIT_COLD || (A.w_mask && !A.w_mask[inst]);
     double x0 = 0, xf = 0, y0 = 0, yf = 0, speed0 = 0;
     if (cold) {
       // straight start->goal line (solver.py:226-252)

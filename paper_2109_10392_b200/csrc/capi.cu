@@ -285,6 +285,7 @@ static int launch_sweeps(bmpc_ctx* ctx, const bmpc_problem* p, const double* xi2
   A.w_d_a = o->w_d_a;
   A.w_v = o->w_v;
   A.w_cpsi = o->w_c_psi;
+  A.w_mask = o->w_mask;
   const bool keep = o->keep_multipliers != 0;
   A.w_lx = keep ? o->w_l_x : nullptr;
   A.w_ly = keep ? o->w_l_y : nullptr;

@@ -22,7 +22,7 @@ import numpy as np
 
 from . import _native as nat
 from .basis import BoundarySpec, build_basis, build_constant_matrices, build_time_grid
-from .solver import AmState, BatchSolver, ProblemBatch, Residuals, _precision_code
+from .solver import AmState, BatchSolver, ProblemBatch, Residuals, SolveInfo, _precision_code
 from .traffic import VehicleState, predict_constant_velocity, select_nearest
 
 
@@ -337,7 +337,8 @@ class Planner:
         self.basis = build_basis(grid, cfg.degree)
         self.mats = build_constant_matrices(self.basis, cfg.m, BoundarySpec())
         self.solver = BatchSolver(self.basis, self.mats, cfg.rho_xy)
-        self._prev_state = None
+        self._prev = None        # (device solution, residuals) of the last cycle
+        self._shift_dev = None
         self._prev_steering = 0.0
         # exact time-shift map in coefficient space (planner.py:326-334): the
         # basis evaluated one control period later, projected back
@@ -365,65 +366,82 @@ class Planner:
         return ProblemBatch(l=len(goals), xi_x=xi_x, xi_y=xi_y, a=c.a, b=c.b, v_min=c.v_min,
                             v_max=c.v_max, a_max=c.a_max, b_xy=b_xy, b_psi=b_psi, rho_xy=c.rho_xy)
 
+    def _warm_device(self, prob, batch: ProblemBatch):
+        """Warm start of the next solve, built and kept on the device
+        (planner.py:362-410): the previous solution's near-converged columns
+        (worst residual <= warm_residual_cap) shifted one cycle by the exact
+        coefficient map, their closed-form alpha/d/alpha_a/d_a/v on the
+        shifted trajectories, multipliers carried.  Returns (warm dict,
+        eligibility mask) -- the kernel starts the other columns cold -- or
+        (None, None)."""
+        import torch
+
+        from . import kernels
+        from .device import DeviceSolution
+
+        if self._prev is None:
+            return None, None
+        prev, prev_res = self._prev
+        if prev.c_x.shape[1] != batch.l:
+            return None, None
+        eligible = prev_res.max_per_instance() <= self.cfg.warm_residual_cap
+        if not eligible.any():
+            return None, None
+        dev = prev.c_x.device
+        if self._shift_dev is None:
+            self._shift_dev = torch.from_numpy(np.ascontiguousarray(self._shift_map)).to(dev)
+        S = self._shift_dev
+        cx, cy, cp = (S @ t for t in (prev.c_x, prev.c_y, prev.c_psi))
+        smp = self.solver.sample_device(
+            DeviceSolution(cx, cy, cp, None, None, None, None, None, None, 0, False),
+            which=("x", "y", "xdot", "ydot", "xddot", "yddot"))
+        alpha, d = kernels.obstacle_update(smp["x"], smp["y"], prob.xi_x[0], prob.xi_y[0],
+                                           batch.a, batch.b)
+        alpha_a, d_a = kernels.accel_update(smp["xddot"], smp["yddot"], batch.a_max)
+        v = kernels.v_update(smp["xdot"], smp["ydot"], batch.v_min, batch.v_max)
+        warm = dict(alpha=alpha, d=d, alpha_a=alpha_a, d_a=d_a, v=v, c_psi=cp, c_x=cx, c_y=cy,
+                    lambda_x=prev.l_x, lambda_y=prev.l_y, lambda_psi=prev.l_psi)
+        mask = torch.from_numpy(eligible.astype(np.uint8)).to(dev)
+        return warm, mask
+
+    def _warm_state(self, batch: ProblemBatch) -> AmState | None:
+        """The reference-shaped warm AmState (host arrays): cold state with the
+        eligible columns replaced by the device warm start."""
+        warm, mask = self._warm_device(self.solver.device_problem(batch), batch)
+        if warm is None:
+            return None
+        state = self.solver.init_state(batch)
+        idx = np.where(mask.cpu().numpy() != 0)[0]
+        for k in ("c_x", "c_y", "c_psi", "v", "alpha", "d", "alpha_a", "d_a", "lambda_x", "lambda_y",
+                  "lambda_psi"):
+            getattr(state, k)[:, idx] = warm[k].cpu().numpy()[:, idx]
+        return state
+
     def sample_plan(self, state: AmState, goals: list, residuals: Residuals,
                     batch: ProblemBatch | None = None) -> RankedPlan:
         """x, y, psi, psidot, v = |(xdot, ydot)| (unclipped), xddot, yddot
         (planner.py:412-423), sampled on the device."""
         import torch
 
-        from .device import DeviceSolution
-
         dev = torch.device("cuda", torch.cuda.current_device())
         up = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)  # noqa: E731
-        cx, cy, cp = up(state.c_x), up(state.c_y), up(state.c_psi)
-        res = up(np.stack([residuals.r_obs, residuals.r_acc, residuals.r_nonhol]))
+        return self._sample_plan_device(up(state.c_x), up(state.c_y), up(state.c_psi), goals,
+                                        residuals, batch)
+
+    def _sample_plan_device(self, cx, cy, cp, goals: list, residuals: Residuals,
+                            batch: ProblemBatch | None = None) -> RankedPlan:
+        import torch
+
+        from .device import DeviceSolution
+
+        dev = cx.device
+        res = torch.from_numpy(np.stack([residuals.r_obs, residuals.r_acc, residuals.r_nonhol])).to(dev)
         sol = DeviceSolution(cx, cy, cp, None, None, None, None, res, None, 0, False)
         smp = self.solver.sample_device(sol, which=("x", "y", "psi", "psidot", "v", "xddot", "yddot"))
         h = {k: v.cpu().numpy() for k, v in smp.items()}
         return RankedPlan(goals=goals, x=h["x"], y=h["y"], psi=h["psi"], psidot=h["psidot"], v=h["v"],
                           xddot=h["xddot"], yddot=h["yddot"], residuals=residuals,
                           _dev=dict(solver=self.solver, c_x=cx, c_y=cy, c_psi=cp, res=res, batch=batch))
-
-    def _warm_state(self, batch: ProblemBatch) -> AmState | None:
-        """Cold state with the near-converged previous instances shifted one
-        cycle, multipliers carried (planner.py:362-410); the shift and the
-        closed forms run on the device."""
-        import torch
-
-        from . import kernels
-        from .device import DeviceSolution
-
-        if self._prev_state is None:
-            return None
-        prev, prev_res = self._prev_state
-        if prev.c_x.shape[1] != batch.l:
-            return None
-        eligible = prev_res.max_per_instance() <= self.cfg.warm_residual_cap
-        if not eligible.any():
-            return None
-        idx = np.where(eligible)[0]
-        state = self.solver.init_state(batch)
-        dev = torch.device("cuda", torch.cuda.current_device())
-        up = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)  # noqa: E731
-        S = up(self._shift_map)
-        cx, cy, cp = (S @ up(getattr(prev, k)[:, idx]) for k in ("c_x", "c_y", "c_psi"))
-        smp = self.solver.sample_device(
-            DeviceSolution(cx.contiguous(), cy.contiguous(), cp.contiguous(), None, None, None, None,
-                           None, None, 0, False), which=("x", "y", "xdot", "ydot", "xddot", "yddot"))
-        c = self.cfg
-        v = kernels.v_update(smp["xdot"], smp["ydot"], batch.v_min, batch.v_max)
-        alpha, d = kernels.obstacle_update(smp["x"], smp["y"], up(batch.xi_x), up(batch.xi_y),
-                                           batch.a, batch.b)
-        alpha_a, d_a = kernels.accel_update(smp["xddot"], smp["yddot"], batch.a_max)
-        h = lambda t: t.cpu().numpy()  # noqa: E731
-        state.c_x[:, idx], state.c_y[:, idx], state.c_psi[:, idx] = h(cx), h(cy), h(cp)
-        state.v[:, idx] = h(v)
-        state.alpha[:, idx], state.d[:, idx] = h(alpha), h(d)
-        state.alpha_a[:, idx], state.d_a[:, idx] = h(alpha_a), h(d_a)
-        for k in ("lambda_x", "lambda_y", "lambda_psi"):
-            getattr(state, k)[:, idx] = getattr(prev, k)[:, idx]
-        del c
-        return state
 
     def fallback_command(self, ego: EgoState) -> ControlCommand:
         """Hold steering, bleed speed toward v_min over the horizon (planner.py:425-430)."""
@@ -438,15 +456,19 @@ class Planner:
         c = self.cfg
         goals = sample_goals(ego, self.lanes, self.meta, c.l, c.t_f)
         batch = self.build_batch(ego, vehicles, goals)
-        warm = self._warm_state(batch) if c.warm_start else None
+        prob = self.solver.device_problem(batch)
+        warm, mask = self._warm_device(prob, batch) if c.warm_start else (None, None)
         start = time.perf_counter()
-        state, info = self.solver.solve(batch, max_iter=c.max_iter, tol=c.tol, warm=warm,
-                                        keep_multipliers=True)
+        sol = self.solver.solve_device(prob, max_iter=c.max_iter, tol=c.tol, warm=warm,
+                                       keep_multipliers=True, want_v=False, warm_mask=mask)
+        hist = sol.history[: sol.iterations].cpu().numpy()
         solve_time = time.perf_counter() - start
-        plan = self.sample_plan(state, goals, info.residual_history[-1], batch)
+        history = [Residuals(r_obs=h[0].copy(), r_acc=h[1].copy(), r_nonhol=h[2].copy()) for h in hist]
+        info = SolveInfo(residual_history=history, iterations=sol.iterations, converged=sol.converged)
+        plan = self._sample_plan_device(sol.c_x, sol.c_y, sol.c_psi, goals, history[-1], batch)
         filter_candidates(plan, batch, c.limits)
         rank(plan, self.meta)
-        self._prev_state = (state, plan.residuals)
+        self._prev = (sol, plan.residuals)
         if plan.best_index is None:
             command, fallback = self.fallback_command(ego), True
         else:

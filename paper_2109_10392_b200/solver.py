@@ -293,11 +293,13 @@ class BatchSolver:
 
     def solve_device(self, prob, max_iter: int = 150, tol: float = 1e-3, warm: dict | None = None,
                      keep_multipliers: bool = False, want_v: bool = True, warps_per_block: int = 0,
-                     precision: str = "fp64"):
+                     precision: str = "fp64", warm_mask=None):
         """Solve a DeviceProblem (one or many scenes) with every buffer in HBM.
 
-        ``warm`` maps AmState field names to device tensors.  Returns a
-        device.DeviceSolution; blocks only to learn the sweep count.
+        ``warm`` maps AmState field names to device tensors; ``warm_mask`` (L
+        uint8 device tensor, optional) limits the warm start to the instances
+        it marks, the others start cold.  Returns a device.DeviceSolution;
+        blocks only to learn the sweep count.
         """
         import torch
 
@@ -317,6 +319,8 @@ class BatchSolver:
                              ("w_d_a", "d_a"), ("w_v", "v"), ("w_c_psi", "c_psi"),
                              ("w_l_x", "lambda_x"), ("w_l_y", "lambda_y"), ("w_l_psi", "lambda_psi")):
                 setattr(opts, fld, warm[key].data_ptr())
+            if warm_mask is not None:
+                opts.w_mask = warm_mask.data_ptr()
         out = D.solution_struct(sol)
         nat.check(nat.load().bmpc_solve(ctx, ctypes.byref(prob.c_struct()), ctypes.byref(opts),
                                         ctypes.byref(out), ctypes.c_void_p(D.stream_ptr())), "solve")
