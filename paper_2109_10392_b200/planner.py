@@ -349,12 +349,15 @@ class Planner:
         self._shift_map = np.linalg.pinv(self.basis.P) @ bernstein(u, cfg.degree)
 
     def boundary_vectors(self, ego: EgoState, goals: list[Goal]) -> tuple[np.ndarray, np.ndarray]:
+        """Per-instance boundary right-hand sides (planner.py:336-347), column i
+        = [ego x, vx, ax, goal x, vx, ax, ego y, vy, ay, goal y, vy, ay]."""
         l = len(goals)
+        g = np.array([(q.x, q.vx, q.ax, q.y, q.vy, q.ay) for q in goals], dtype=np.float64).reshape(l, 6)
         b_xy = np.empty((12, l))
-        b_psi = np.empty((4, l))
-        for i, g in enumerate(goals):
-            b_xy[:, i] = [ego.x, ego.vx, ego.ax, g.x, g.vx, g.ax, ego.y, ego.vy, ego.ay, g.y, g.vy, g.ay]
-            b_psi[:, i] = [ego.psi, ego.psidot, 0.0, 0.0]
+        b_xy[[0, 1, 2, 6, 7, 8]] = np.array([ego.x, ego.vx, ego.ax, ego.y, ego.vy, ego.ay])[:, None]
+        b_xy[[3, 4, 5, 9, 10, 11]] = g.T
+        b_psi = np.zeros((4, l))
+        b_psi[0], b_psi[1] = ego.psi, ego.psidot
         return b_xy, b_psi
 
     def build_batch(self, ego: EgoState, vehicles: list[VehicleState], goals: list[Goal]
