@@ -264,7 +264,7 @@ struct TailArgs {
   const double2* xi;
   const double *xs, *ys;  // sampled positions (pass A) or nullptr: recompute from c
   int n, m;
-  double a, b, inv_ab;
+  double a, b;
 };
 
 // fp32 mode inside term (the outside test runs in fp64 in both modes): with
@@ -289,12 +289,14 @@ __device__ __forceinline__ void obstacle_term_f32(double x, double y, double2 q,
   sry += ry;
 }
 
-// Obstacle block of the fused tail (kernels/_speedups.pyx:150-176) for NS
-// samples of one lane: sum_j g_obs,j contracted onto P on the fly, and the
-// squared residual.  Obstacles j0, j0+js, ...; `group` > 1 marks a split slot
-// whose obstacle partials are summed over `group` consecutive lanes
-// (warp-uniform) before the group leader contracts them.  The acceleration
-// and non-holonomic blocks run in passes A and B of the sweep.
+// Obstacle block (kernels/_speedups.pyx:150-176) in exact form for NS samples
+// of one lane: every term takes the outside test; the inside terms' residuals
+// r_j give the correction -P^T sum_inside r_j to P^T sum_j g_j = m (P^T P) c
+// (the Gram part is added once per sweep) and the squared residual.
+// Obstacles j0, j0+js, ...; `group` > 1 marks a split slot whose partials are
+// summed over `group` consecutive lanes (warp-uniform) before the group leader
+// contributes them.  The acceleration and non-holonomic blocks run in passes
+// A and B of the sweep.
 template <int NS, int NB, int NPAD, bool F32>
 __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)[NS], int j0, int js,
                                                int group, bool valid, bool leader,
@@ -510,7 +512,6 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
       reinterpret_cast<const double2*>(A.xi) + (size_t)(inst / A.l) * A.m * n;
   const int m = A.m;
   const double a = A.a, b = A.b, rho = C.rho;
-  const double inv_ab = 1.0 / (a * b);
 
   const int li = lane & 15;
   const bool yax = lane >= 16;
@@ -826,7 +827,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
     //     slot(): full slots two at a time, the n % 32 leftover samples split
     //     over lane groups.
     {
-      TailArgs T{sP, cxy, xi, kStoreXY ? ws.x : nullptr, kStoreXY ? ws.y : nullptr, n, m, a, b, inv_ab};
+      TailArgs T{sP, cxy, xi, kStoreXY ? ws.x : nullptr, kStoreXY ? ws.y : nullptr, n, m, a, b};
       int r = 0;
       if (kPairSlots<NB>) {
 #pragma unroll 1
