@@ -1,0 +1,78 @@
+"""Parity across the kernel's instantiation space: horizon lengths that hit
+every padding (64/128/224/256 samples) and every leftover-slot layout (split
+groups of 2..16 lanes, one lane per sample, none), Bernstein orders 6..16,
+obstacle counts 1..40 (inside-heavy scenes included) -- against the oracle on
+the same inputs, 1e-8 relative on columns the oracle's own 1-ulp screen marks
+stable, identical scoring indices.  The oracle is the pinned CPU restatement
+of the reference (tests/test_oracle.py)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [  # (n, t_f, degree, m, l, sweeps)
+    (40, 4.0, 6, 2, 24, 30),     # npad 64, R=8 -> split groups of 4
+    (64, 5.0, 6, 5, 20, 30),     # npad 64, no leftover
+    (100, 5.0, 10, 1, 16, 40),   # a single obstacle
+    (110, 6.0, 8, 12, 24, 30),   # npad 128, R=14 -> groups of 2
+    (127, 5.0, 12, 7, 16, 30),   # R=31 -> one lane per leftover sample
+    (150, 7.5, 13, 9, 16, 25),   # npad 224, NB=14 (single-slot obstacle passes)
+    (200, 10.0, 15, 40, 12, 25),  # the c4 shape, NB=16
+    (256, 8.0, 9, 6, 12, 25),    # npad 256, no leftover
+]
+
+
+def _scene(n, t_f, m, l, seed, crowd):
+    from paper_2109_10392_b200.scenes import LANES
+
+    rng = np.random.default_rng(seed)
+    times = np.linspace(0.0, t_f, n)
+    # obstacles close to the ego's path so plenty of samples fall inside ellipses
+    x0 = rng.uniform(5.0 if crowd else -30.0, 60.0 if crowd else 120.0, m)
+    y0 = rng.choice(LANES, m)
+    vx = rng.uniform(8.0, 25.0, m)
+    xi_x = (x0[:, None] + vx[:, None] * times[None, :]).ravel()
+    xi_y = np.repeat(y0, n).astype(np.float64)
+    v0 = rng.uniform(15.0, 25.0)
+    y_ego = rng.choice(LANES)
+    yg = rng.uniform(-5.25, 5.25, l)
+    vg = rng.uniform(10.0, 30.0, l)
+    b_xy = np.zeros((12, l))
+    b_xy[1], b_xy[3], b_xy[4] = v0, vg * t_f, vg
+    b_xy[6], b_xy[9] = y_ego, yg
+    return xi_x, xi_y, b_xy, np.zeros((4, l))
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=[f"n{s[0]}_d{s[2]}_m{s[3]}" for s in SHAPES])
+def test_shape_parity(cuda, shape):
+    import am_oracle as O
+
+    from paper_2109_10392_b200 import ProblemBatch, make_solver
+
+    n, t_f, degree, m, l, sweeps = shape
+    xi_x, xi_y, b_xy, b_psi = _scene(n, t_f, m, l, seed=n + m, crowd=m >= 5)
+    a, b, v_min, v_max, a_max = 5.6, 2.4, 0.1, 35.0, 8.0
+    o = O.OracleSolver(n, t_f, degree, m)
+    ref = o.solve(xi_x, xi_y, b_xy, b_psi, a, b, v_min, v_max, a_max, max_iter=sweeps)
+    scr = o.solve(xi_x * (1 + 2.2e-16), xi_y, b_xy, b_psi, a, b, v_min, v_max, a_max, max_iter=sweeps)
+    P = o.P
+    div = np.zeros(l)
+    for k in ("c_x", "c_y", "c_psi"):
+        tr = P @ ref[k]
+        div = np.maximum(div, np.abs(P @ scr[k] - tr).max(axis=0) / np.maximum(1.0, np.abs(tr).max(axis=0)))
+    stable = div <= 1e-10
+    assert stable.sum() >= l // 2, f"only {stable.sum()}/{l} stable columns"
+
+    solver = make_solver(n, t_f, degree, m)
+    batch = ProblemBatch(l=l, xi_x=xi_x, xi_y=xi_y, a=a, b=b, v_min=v_min, v_max=v_max, a_max=a_max,
+                         b_xy=b_xy, b_psi=b_psi)
+    state, info = solver.solve(batch, max_iter=sweeps, tol=0.0)
+    err = np.zeros(l)
+    for k in ("c_x", "c_y", "c_psi"):
+        tr = P @ ref[k]
+        err = np.maximum(err, np.abs(P @ getattr(state, k) - tr).max(axis=0) / np.maximum(1.0, np.abs(tr).max(axis=0)))
+    print(f"n={n} nb={degree + 1} m={m}: stable {stable.sum()}/{l}, max rel err {err[stable].max():.2e}")
+    assert err[stable].max() <= 1e-8
+    hist = np.stack([[h.r_obs, h.r_acc, h.r_nonhol] for h in info.residual_history])
+    np.testing.assert_allclose(hist[-1][:, stable], ref["history"][-1][:, stable], rtol=1e-6, atol=1e-9)
