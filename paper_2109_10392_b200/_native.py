@@ -39,7 +39,7 @@ class SolveOpts(Structure):
         ("w_alpha", c_void_p), ("w_d", c_void_p), ("w_alpha_a", c_void_p), ("w_d_a", c_void_p),
         ("w_v", c_void_p), ("w_c_psi", c_void_p),
         ("w_l_x", c_void_p), ("w_l_y", c_void_p), ("w_l_psi", c_void_p),
-        ("status_dev", c_void_p), ("w_mask", c_void_p),
+        ("status_dev", c_void_p), ("w_mask", c_void_p), ("team_warps", c_int),
     ]
 
 

@@ -68,6 +68,7 @@ typedef struct {
   double tol;
   int* notconv;
   const int* iters_dev;  // non-NULL: sweep count read on the device (0 = nothing to do)
+  int team;              // warps per instance (1, 2 or 4)
 } bmpc_solve_args;
 
 // Doubles of carried state per instance: lambda_x, lambda_y, lambda_psi, G_x,
@@ -112,7 +113,11 @@ typedef struct {
 #endif
 BMPC_HD constexpr bool bmpc_stores_xy(int npad) { return npad <= BMPC_XY_NPAD_MAX; }
 BMPC_HD constexpr int bmpc_sample_arrays(int npad) { return bmpc_stores_xy(npad) ? 5 : 3; }
-BMPC_HD constexpr int bmpc_warp_scratch_doubles(int npad) {
-  return 288 + bmpc_sample_arrays(npad) * npad + 32 * 33;
+// Team layout (team = the TW warps sharing one instance): per warp 288 KKT
+// doubles + the 32 x 33 transpose buffer + 72 exchange doubles; per team the
+// per-sample arrays once.
+BMPC_HD constexpr int bmpc_warp_private_doubles() { return 288 + 32 * 33 + 72; }
+BMPC_HD constexpr int bmpc_team_doubles(int npad, int tw) {
+  return tw * bmpc_warp_private_doubles() + bmpc_sample_arrays(npad) * npad;
 }
 #endif

@@ -4,16 +4,17 @@
 
 namespace bmpc {
 
-size_t am_solve_smem_bytes(int nb, int npad, int kxs, int kps, int warps);
+size_t am_solve_smem_bytes(int nb, int npad, int kxs, int kps, int warps, int team);
 
-template <int NB, int NKM, bool F32>
+template <int NB, int NKM, bool F32, bool TEAMS = false>
 static cudaError_t launch_t(const bmpc_dev_consts& C, const bmpc_solve_args& A, int warps,
                             cudaStream_t st) {
-  const size_t smem = am_solve_smem_bytes(NB, C.npad, C.kxs, C.kps, warps);
-  auto kfn = am_solve_kernel<NB, NKM, F32>;
+  const size_t smem = am_solve_smem_bytes(NB, C.npad, C.kxs, C.kps, warps, A.team);
+  auto kfn = am_solve_kernel<NB, NKM, F32, TEAMS>;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int grid = (A.L + warps - 1) / warps;
+  const int ipb = warps / A.team;  // instances per block
+  const int grid = (A.L + ipb - 1) / ipb;
   kfn<<<grid, warps * 32, smem, st>>>(C, A);
   return cudaGetLastError();
 }
@@ -25,6 +26,14 @@ cudaError_t BMPC_CAT(launch_am_nb_, BMPC_INST_NB)(const bmpc_dev_consts& C,
                                                    const bmpc_solve_args& A, int warps,
                                                    cudaStream_t st) {
   const bool f32 = (A.flags & BMPC_F_F32) != 0;
+  if (A.team > 1) {  // teams: the small-batch latency mode, fp64, n <= 128
+    if (f32) return cudaErrorNotSupported;
+    switch (C.npad) {
+      case 64: return launch_t<BMPC_INST_NB, 2, false, true>(C, A, warps, st);
+      case 128: return launch_t<BMPC_INST_NB, 4, false, true>(C, A, warps, st);
+      default: return cudaErrorNotSupported;
+    }
+  }
   switch (C.npad) {  // the host pads n to 64, 128, 224 or 256 samples
     case 64: return f32 ? launch_t<BMPC_INST_NB, 2, true>(C, A, warps, st)
                                  : launch_t<BMPC_INST_NB, 2, false>(C, A, warps, st);

@@ -7,11 +7,11 @@
 
 namespace bmpc {
 
-size_t am_solve_smem_bytes(int nb, int npad, int kxs, int kps, int warps) {
+size_t am_solve_smem_bytes(int nb, int npad, int kxs, int kps, int warps, int team) {
   // basis, KKT inverse + matrix for both systems, M, P^T P, Pddot^T Pddot, Pdot^T Pdot, tau, per-warp scratch
   return sizeof(double) *
          ((size_t)3 * nb * npad + 2 * (size_t)(nb + 6) * kxs + 2 * (size_t)(nb + 4) * kps + (size_t)((4 * nb * (nb | 1) + 1) & ~1) + npad +
-          (size_t)warps * bmpc_warp_scratch_doubles(npad));
+          (size_t)(warps / team) * bmpc_team_doubles(npad, team));
 }
 
 #define BMPC_DECL(NB)                                                                      \

@@ -441,7 +441,7 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
   BMPC_PROF_NS(13);
 }
 
-template <int NB, int NKM, bool F32>
+template <int NB, int NKM, bool F32, bool TEAMS>
 #ifndef BMPC_MINB
 #define BMPC_MINB 1
 #endif
@@ -476,12 +476,33 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
   double* sMdd = sMp + NB * C.kms;  // Pddot^T Pddot
   double* sMd = sMdd + NB * C.kms;  // Pdot^T Pdot
   double* sTau = sM + ((4 * NB * C.kms + 1) & ~1);  // keep the double2 scratch 16-byte aligned
-  double* wbase = sTau + npad + warp * bmpc_warp_scratch_doubles(npad);
-  double* arr = wbase + kWarpScratch;
+  // team = the TW warps sharing one instance; each keeps private KKT vectors,
+  // transpose buffer and exchange slots, the per-sample arrays are shared
+  const int TW = TEAMS ? A.team : 1;  // compile-time 1 outside the team build
+  const int team = warp / TW, wt = warp - team * TW;
+  double* tbase = sTau + npad + team * bmpc_team_doubles(npad, TW);
+  double* wbase = tbase + wt * bmpc_warp_private_doubles();
+  double* arr = tbase + TW * bmpc_warp_private_doubles();
   WarpScratch ws{wbase,       wbase + 64,   wbase + 128, wbase + 192, wbase + 224, wbase + 256,
                  arr,         arr + npad,   arr + 2 * npad,
                  kStoreXY ? arr + 3 * npad : nullptr, kStoreXY ? arr + 4 * npad : nullptr,
-                 arr + bmpc_sample_arrays(npad) * npad};
+                 wbase + kWarpScratch};
+  // exchange slots of team warp w: [0, 32) P^T theta, [32, 64) G, [64, 67) squared
+  // residuals, [67] unwrap flag
+  auto xch_of = [&](int w) { return tbase + w * bmpc_warp_private_doubles() + kWarpScratch + kRedSize; };
+  double* xch = xch_of(wt);
+  // named barrier 1 + team (a block holds at most 4 teams: W <= 8, TW >= 2);
+  // immediate ids so ptxas reserves only barriers 0-4
+  auto team_sync = [&]() {
+    if (TW == 1) return;
+    const int nt = TW * 32;
+    switch (team) {
+      case 0: asm volatile("bar.sync 1, %0;" ::"r"(nt) : "memory"); break;
+      case 1: asm volatile("bar.sync 2, %0;" ::"r"(nt) : "memory"); break;
+      case 2: asm volatile("bar.sync 3, %0;" ::"r"(nt) : "memory"); break;
+      default: asm volatile("bar.sync 4, %0;" ::"r"(nt) : "memory"); break;
+    }
+  };
   const SlotLayout sl = slot_layout(n);
   const int nslots = sl.F + (sl.R > 0 ? 1 : 0);
 
@@ -502,8 +523,8 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
   __syncthreads();  // the initialised barrier is visible to every thread
   mbar_wait_parity(&s_cbar, 0);
 
-  const int inst = blockIdx.x * W + warp;
-  if (inst >= L) return;  // no block-wide barriers below this point
+  const int inst = blockIdx.x * (W / TW) + team;
+  if (inst >= L) return;  // team-uniform; no block-wide barriers below this point
 
   const double* __restrict__ sP = sPT;
   const double* __restrict__ sPd = sPT + NB * npad;
@@ -699,6 +720,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
     //     Acceleration block (_speedups.pyx:179-198) in exact form: unclipped
     //     samples give g_acc = (xddot, yddot) and r = 0, so Pddot^T g_acc =
     //     (Pddot^T Pddot) c plus a sparse correction from the clipped samples.
+    double pth;                     // owner lanes: P^T theta
     double Gx[NB], Gy[NB], pt[NB];  // Gx, Gy: lane partials of F_axis^T g beyond the Gram terms
 #pragma unroll
     for (int i = 0; i < NB; ++i) Gx[i] = Gy[i] = pt[i] = 0.0;
@@ -707,8 +729,8 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
       bool wrap = false;
       double prev_last = 0.0;  // theta of sample 32 r - 1: lane 31 of the previous slot
       const double amax2 = A.a_max * A.a_max;
-      // full chunks of CH slots (every slot valid at compile time), then the
-      // NKM % CH remainder; chunks stay rolled for the instruction cache
+      // this warp's slots r = wt, wt + TW, ... in chunks of CH (every slot of a
+      // chunk valid at compile time); chunks stay rolled for the instruction cache
       auto chunk_a = [&](auto nsc, const int r0) {
         constexpr int NSC = decltype(nsc)::value;
         int k[NSC];
@@ -716,7 +738,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
         double xx[NSC], yy[NSC], xd[NSC], yd[NSC], xdd[NSC], ydd[NSC];
 #pragma unroll
         for (int s = 0; s < NSC; ++s) {
-          k[s] = lane + 32 * (r0 + s);
+          k[s] = lane + 32 * (r0 + s * TW);
           v[s] = k[s] < n;
           xx[s] = yy[s] = xd[s] = yd[s] = xdd[s] = ydd[s] = 0.0;
         }
@@ -746,7 +768,10 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
           const double last = __shfl_sync(BMPC_FULL, th[s], 31);
           if (lane == 0) prev = prev_last;
           prev_last = last;
-          if (v[s] && k[s] > 0 && !(fabs(th[s] - prev) < CUDART_PI)) wrap = true;
+          // lane 0's predecessor belongs to another warp of a team: checked
+          // after the team barrier
+          if (v[s] && k[s] > 0 && (lane > 0 || TW == 1) && !(fabs(th[s] - prev) < CUDART_PI))
+            wrap = true;
           if (v[s]) {
             ws.th[k[s]] = th[s];
             ws.xd[k[s]] = xd[s];
@@ -792,18 +817,17 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
           }
         }
       };
+      int r0 = wt;
 #pragma unroll 1
-      for (int r0 = 0; r0 + CH <= NKM; r0 += CH) chunk_a(std::integral_constant<int, CH>{}, r0);
-      if constexpr (NKM % CH != 0) chunk_a(std::integral_constant<int, NKM % CH>{}, NKM - NKM % CH);
+      for (; r0 + (CH - 1) * TW < NKM; r0 += CH * TW) chunk_a(std::integral_constant<int, CH>{}, r0);
+      if (CH > 1 && r0 < NKM) chunk_a(std::integral_constant<int, 1>{}, r0);  // CH = 2: one left
       BMPC_PROF(2);
-      if (__any_sync(BMPC_FULL, wrap)) {  // rare: exact numpy unwrap, then P^T theta again
-        __syncwarp();
-        if (lane == 0) np_unwrap_serial(ws.th, n);
-        __syncwarp();
+      // P^T theta of this warp's slots (again after an unwrap)
+      auto pt_slots = [&]() {
 #pragma unroll
         for (int i = 0; i < NB; ++i) pt[i] = 0.0;
-#pragma unroll
-        for (int r = 0; r < NKM; ++r) {
+#pragma unroll 1
+        for (int r = wt; r < NKM; r += TW) {
           const int k = lane + 32 * r;
           if (k < n) {
             const double t = ws.th[k];
@@ -811,15 +835,50 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
             for (int i = 0; i < NB; ++i) pt[i] = fma(sP[i * npad + k], t, pt[i]);
           }
         }
-      }
-    }
-    double pth;
-    {
+      };
+      auto pt_colsum = [&]() {
 #pragma unroll
-      for (int i = 0; i < NB; ++i) ws.red[lane * kRedStride + i] = pt[i];
-      __syncwarp();
-      pth = owner ? column_sum(ws.red, li) : 0.0;  // lanes i and 16+i both get sum_k P_ki theta_k
-      __syncwarp();
+        for (int i = 0; i < NB; ++i) ws.red[lane * kRedStride + i] = pt[i];
+        __syncwarp();
+        const double c = owner ? column_sum(ws.red, li) : 0.0;  // lanes i and 16+i: sum_k P_ki theta_k
+        __syncwarp();
+        return c;
+      };
+      if (TW == 1) {
+        if (__any_sync(BMPC_FULL, wrap)) {  // rare: exact numpy unwrap, then P^T theta again
+          __syncwarp();
+          if (lane == 0) np_unwrap_serial(ws.th, n);
+          __syncwarp();
+          pt_slots();
+        }
+        pth = pt_colsum();
+      } else {
+        // team: partial sums and unwrap flags through the exchange slots; the
+        // slot-boundary tests (sample 32 r against 32 r - 1) by every warp
+        const double part = pt_colsum();
+        if (owner) xch[li] = part;
+        const bool wf = __any_sync(BMPC_FULL, wrap);
+        if (lane == 0) xch[67] = wf ? 1.0 : 0.0;
+        team_sync();
+        bool gw = false;
+        for (int w = 0; w < TW; ++w) gw |= xch_of(w)[67] != 0.0;
+        for (int r = 1 + lane; r < NKM; r += 32) {
+          const int k = 32 * r;
+          if (k < n && !(fabs(ws.th[k] - ws.th[k - 1]) < CUDART_PI)) gw = true;
+        }
+        if (__any_sync(BMPC_FULL, gw)) {  // rare: serial numpy unwrap by one warp
+          team_sync();
+          if (wt == 0 && lane == 0) np_unwrap_serial(ws.th, n);
+          team_sync();
+          pt_slots();
+          const double p2 = pt_colsum();
+          if (owner) xch[li] = p2;
+          team_sync();
+        }
+        double acc = 0.0;
+        for (int w = 0; w < TW; ++w) acc += owner ? xch_of(w)[li] : 0.0;
+        pth = acc;
+      }
     }
     BMPC_PROF(3);
 
@@ -828,16 +887,16 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
     //     over lane groups.
     {
       TailArgs T{sP, cxy, xi, kStoreXY ? ws.x : nullptr, kStoreXY ? ws.y : nullptr, n, m, a, b};
-      int r = 0;
+      int r = wt;  // this warp's slots r = wt, wt + TW, ...
       if (kPairSlots<NB>) {
 #pragma unroll 1
-        for (; r + 1 < sl.F; r += 2) {
-          const int ks[2] = {lane + 32 * r, lane + 32 * (r + 1)};
+        for (; r + TW < sl.F; r += 2 * TW) {
+          const int ks[2] = {lane + 32 * r, lane + 32 * (r + TW)};
           obstacle_block<2, NB, npad, F32>(T, ks, 0, 1, 0, true, true, Gx, Gy, sqo);
         }
       }
 #pragma unroll 1
-      for (; r < nslots; ++r) {
+      for (; r < nslots; r += TW) {
         const Slot S = slot(r, lane, sl);
         const int ks[1] = {S.k};
         obstacle_block<1, NB, npad, F32>(T, ks, S.j0, S.js, (r == sl.F) ? sl.g : 1, S.valid,
@@ -887,7 +946,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
       double ps[NSC];
 #pragma unroll
       for (int s = 0; s < NSC; ++s) {
-        k[s] = lane + 32 * (r0 + s);
+        k[s] = lane + 32 * (r0 + s * TW);
         v[s] = k[s] < n;
         ps[s] = 0.0;
       }
@@ -944,9 +1003,12 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
         }
       }
     };
+    {
+      int r0 = wt;
 #pragma unroll 1
-    for (int r0 = 0; r0 + CH <= NKM; r0 += CH) chunk_b(std::integral_constant<int, CH>{}, r0);
-    if constexpr (NKM % CH != 0) chunk_b(std::integral_constant<int, NKM % CH>{}, NKM - NKM % CH);
+      for (; r0 + (CH - 1) * TW < NKM; r0 += CH * TW) chunk_b(std::integral_constant<int, CH>{}, r0);
+      if (CH > 1 && r0 < NKM) chunk_b(std::integral_constant<int, 1>{}, r0);
+    }
     BMPC_PROF(12);
 
     // (6) G = F_axis^T g = m (P^T P) c + (Pddot^T Pddot) c + the lane partials
@@ -961,11 +1023,29 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
       ws.red[lane * kRedStride + 16 + i] = Gy[i];
     }
     __syncwarp();
-    const double gn = owner ? column_sum(ws.red, lane) : 0.0;
+    double gn = owner ? column_sum(ws.red, lane) : 0.0;
     sqo = warp_sum(sqo);
     sqa = warp_sum(sqa);
     sqn = warp_sum(sqn);
     __syncwarp();
+    if (TW > 1) {  // team: sum the warps' partials in a fixed order
+      if (owner) xch[32 + lane] = gn;
+      if (lane == 0) {
+        xch[64] = sqo;
+        xch[65] = sqa;
+        xch[66] = sqn;
+      }
+      team_sync();
+      gn = 0.0;
+      sqo = sqa = sqn = 0.0;
+      for (int w = 0; w < TW; ++w) {
+        const double* xw = xch_of(w);
+        gn += owner ? xw[32 + lane] : 0.0;
+        sqo += xw[64];
+        sqa += xw[65];
+        sqn += xw[66];
+      }
+    }
     BMPC_PROF(6);
     if (owner) {
       const double* m1 = sMp + li * C.kms;
@@ -985,14 +1065,14 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
     }
     if (!yax && owner) lamp -= rho * Lp;
     const double res = sqrt(lane == 16 ? sqo : (lane == 17 ? sqa : sqn));  // lanes 16..18
-    if (A.notconv) {  // global early stop: flag this sweep unless every residual <= tol
+    if (A.notconv && wt == 0) {  // global early stop: flag this sweep unless every residual <= tol
       const bool nc = __any_sync(BMPC_FULL, lane >= 16 && lane < 19 && !(res <= A.tol));
       if (lane == 0 && nc) {
         int* f = A.notconv + A.hist_offset + t;
         if (*(volatile int*)f == 0) *f = 1;
       }
     }
-    if (lane >= 16 && lane < 19) {
+    if (lane >= 16 && lane < 19 && wt == 0) {
       if (A.flags & BMPC_F_HISTORY)
         A.hist[((size_t)(A.hist_offset + t) * 3 + (lane - 16)) * L + inst] = res;
       if (last && A.res_final) A.res_final[(size_t)(lane - 16) * L + inst] = res;
@@ -1005,7 +1085,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
   // ------------------------------------------------- fused planner scoring ----
   // sample_plan + filter_candidates + meta_cost of this instance straight from
   // the on-chip coefficients (planner.py:210-245, :412-423; csrc/score.cuh).
-  if (A.flags & BMPC_F_SCORE) {
+  if ((A.flags & BMPC_F_SCORE) && wt == 0) {
     const bmpc_fused_score& F = A.score;
     const ScoreParams sp{n, m, F.kind, a, b, F.v_cruise, F.v_max, F.y_rl, F.w1, F.w2,
                          F.heading_limit, F.residual_tol, F.ratio_min};
@@ -1035,6 +1115,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
   BMPC_PROF(8);
 
   // ------------------------------------------------------------- outputs ----
+  if (wt != 0) return;  // the team's warp 0 holds the same state and writes it
   if (owner) {
     const size_t o = (size_t)li * L + inst;
     if (!yax) {

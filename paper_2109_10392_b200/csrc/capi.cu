@@ -15,7 +15,7 @@
 namespace bmpc {
 cudaError_t launch_am_solve(const bmpc_dev_consts& C, const bmpc_solve_args& A, int warps,
                             cudaStream_t st);
-size_t am_solve_smem_bytes(int nb, int npad, int kxs, int kps, int warps);
+size_t am_solve_smem_bytes(int nb, int npad, int kxs, int kps, int warps, int team);
 cudaError_t op_obstacle_update(int n, int l, long long mn, const double* x, const double* y,
                                const double* xi_x, const double* xi_y, double a, double b,
                                double* alpha, double* d, cudaStream_t st);
@@ -243,14 +243,15 @@ static int check_problem(const bmpc_ctx* ctx, const bmpc_problem* p) {
 // Warps (= instances) per CTA: about one CTA per SM for small batches, at most
 // 8 (the register file holds 8 warps of this kernel), and never more than the
 // opt-in shared memory per block allows.
-static int auto_warps(const bmpc_ctx* ctx, int L, int req) {
-  int w = req > 0 ? req : (L + ctx->sms - 1) / ctx->sms;
-  if (w < 1) w = 1;
-  if (w > BMPC_MAX_WARPS) w = BMPC_MAX_WARPS;
-  while (w > 1 && bmpc::am_solve_smem_bytes(ctx->C.nb, ctx->C.npad, ctx->C.kxs, ctx->C.kps, w) >
-                      (size_t)ctx->smem_optin)
-    --w;
-  return w;
+static int auto_warps(const bmpc_ctx* ctx, int L, int req, int team) {
+  // warps per block: a multiple of the team size, about one block per SM
+  int ipb = req > 0 ? req / team : (L + ctx->sms - 1) / ctx->sms;
+  if (ipb < 1) ipb = 1;
+  if (ipb * team > BMPC_MAX_WARPS) ipb = BMPC_MAX_WARPS / team;
+  while (ipb > 1 && bmpc::am_solve_smem_bytes(ctx->C.nb, ctx->C.npad, ctx->C.kxs, ctx->C.kps,
+                                              ipb * team, team) > (size_t)ctx->smem_optin)
+    --ipb;
+  return ipb * team;
 }
 
 // Launch `iters` sweeps; xi2 is the packed (S, m, n) double2 buffer.
@@ -286,6 +287,7 @@ static int launch_sweeps(bmpc_ctx* ctx, const bmpc_problem* p, const double* xi2
   A.w_v = o->w_v;
   A.w_cpsi = o->w_c_psi;
   A.w_mask = o->w_mask;
+  A.team = o->team_warps > 1 ? o->team_warps : 1;
   const bool keep = o->keep_multipliers != 0;
   A.w_lx = keep ? o->w_l_x : nullptr;
   A.w_ly = keep ? o->w_l_y : nullptr;
@@ -308,7 +310,8 @@ static int launch_sweeps(bmpc_ctx* ctx, const bmpc_problem* p, const double* xi2
     A.score = *fsc;
   }
   if (L == 0 || iters <= 0) return BMPC_OK;
-  CK(bmpc::launch_am_solve(ctx->C, A, auto_warps(ctx, L, o->warps_per_block), st), "am_solve launch");
+  CK(bmpc::launch_am_solve(ctx->C, A, auto_warps(ctx, L, o->warps_per_block, A.team), st),
+     "am_solve launch");
   return BMPC_OK;
 }
 
@@ -417,6 +420,10 @@ static int solve_impl(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opt
   if (!o || !out) return fail(BMPC_EINVAL, "null opts/out");
   if (o->precision != 0 && o->precision != 1) return fail(BMPC_EINVAL, "precision must be 0 (fp64) or 1 (fp32 obstacle block)");
   if (o->max_iter < 1) return fail(BMPC_EINVAL, "max_iter must be >= 1");
+  if (o->team_warps != 0 && o->team_warps != 1 && o->team_warps != 2 && o->team_warps != 4)
+    return fail(BMPC_EINVAL, "team_warps must be 0, 1, 2 or 4");
+  if (o->team_warps > 1 && (o->precision != 0 || ctx->C.npad > 128))
+    return fail(BMPC_EINVAL, "team_warps > 1 needs fp64 and n <= 128");
   if (!out->res_final) return fail(BMPC_EINVAL, "the res_final output is required");
   if ((rc = check_warm(o, p))) return rc;
   cudaStream_t st = S_(stream);

@@ -323,6 +323,9 @@ class PlannerConfig:
     warm_start: bool = True
     warm_residual_cap: float = 0.2
     limits: FilterLimits = FilterLimits()
+    # warps per instance in the MPC solve: 0 = auto (a team of 4 when the batch
+    # is small enough to leave SMs idle, l <= 148 with n <= 128; else 1)
+    team_warps: int = 0
 
 
 class Planner:
@@ -462,8 +465,10 @@ class Planner:
         prob = self.solver.device_problem(batch)
         warm, mask = self._warm_device(prob, batch) if c.warm_start else (None, None)
         start = time.perf_counter()
+        team = c.team_warps or (4 if batch.l <= 148 and c.n <= 128 else 1)
         sol = self.solver.solve_device(prob, max_iter=c.max_iter, tol=c.tol, warm=warm,
-                                       keep_multipliers=True, want_v=False, warm_mask=mask)
+                                       keep_multipliers=True, want_v=False, warm_mask=mask,
+                                       team_warps=team)
         hist = sol.history[: sol.iterations].cpu().numpy()
         solve_time = time.perf_counter() - start
         history = [Residuals(r_obs=h[0].copy(), r_acc=h[1].copy(), r_nonhol=h[2].copy()) for h in hist]

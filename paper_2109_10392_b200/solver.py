@@ -293,7 +293,7 @@ class BatchSolver:
 
     def solve_device(self, prob, max_iter: int = 150, tol: float = 1e-3, warm: dict | None = None,
                      keep_multipliers: bool = False, want_v: bool = True, warps_per_block: int = 0,
-                     precision: str = "fp64", warm_mask=None):
+                     precision: str = "fp64", warm_mask=None, team_warps: int = 0):
         """Solve a DeviceProblem (one or many scenes) with every buffer in HBM.
 
         ``warm`` maps AmState field names to device tensors; ``warm_mask`` (L
@@ -313,7 +313,7 @@ class BatchSolver:
         opts = nat.SolveOpts(max_iter=int(max_iter), tol=float(tol),
                              keep_multipliers=int(bool(keep_multipliers)),
                              warps_per_block=int(warps_per_block), want_v=int(bool(want_v)),
-                             precision=_precision_code(precision))
+                             precision=_precision_code(precision), team_warps=int(team_warps))
         if warm is not None:
             for fld, key in (("w_alpha", "alpha"), ("w_d", "d"), ("w_alpha_a", "alpha_a"),
                              ("w_d_a", "d_a"), ("w_v", "v"), ("w_c_psi", "c_psi"),

@@ -367,3 +367,42 @@ def test_async_plan_matches_sync(cuda, tol_mode):
         assert cuda.equal(getattr(s0, k), getattr(s1, k)), k
     for k in ("meta_cost", "flags", "best_index", "argmin_all", "argmin_hc"):
         assert cuda.equal(getattr(k0, k), getattr(k1, k)), k
+
+
+@pytest.mark.parametrize("team", [2, 4])
+@pytest.mark.parametrize("name", ["c0", "c1", "c3s", "reverse"])
+def test_team_parity(cuda, name, team):
+    """Teams of 2 or 4 warps per instance (the small-batch latency mode) meet
+    the same contract; a fixed team size is bitwise reproducible."""
+    from paper_2109_10392_b200 import device as D
+
+    z = golden(name)
+    solver = _solver(z)
+    S = _Scenes(z)
+    prob = D.DeviceProblem.from_host(int(z["n"]), S.xi_x, S.xi_y, S.b_xy, S.b_psi, S.l, S.a, S.b,
+                                     S.v_min, S.v_max, S.a_max)
+    sol = solver.solve_device(prob, max_iter=int(z["iters"]), tol=0.0, team_warps=team)
+    got = {k: getattr(sol, k).cpu().numpy() for k in ("c_x", "c_y", "c_psi")}
+    err = traj_err(solver.basis.P, got, z)
+    stable = z["screen_div"] <= SCREEN
+    print(f"team {team} {name}: max rel traj err {err[stable].max():.3e}")
+    assert err[stable].max() <= TRAJ_TOL
+    np.testing.assert_allclose(sol.res_final.cpu().numpy()[:, stable], z["res_final"][:, stable],
+                               rtol=1e-6, atol=1e-9)
+    again = solver.solve_device(prob, max_iter=int(z["iters"]), tol=0.0, team_warps=team)
+    assert cuda.equal(again.c_x, sol.c_x) and cuda.equal(again.c_psi, sol.c_psi)
+
+
+def test_team_validation(cuda):
+    """Teams are the fp64, n <= 128 latency mode: other requests fail loudly."""
+    from paper_2109_10392_b200 import device as D
+
+    z = golden("c4s")  # n = 200
+    solver = _solver(z)
+    S = _Scenes(z)
+    prob = D.DeviceProblem.from_host(int(z["n"]), S.xi_x, S.xi_y, S.b_xy, S.b_psi, S.l, S.a, S.b,
+                                     S.v_min, S.v_max, S.a_max)
+    with pytest.raises(ValueError, match="team_warps"):
+        solver.solve_device(prob, max_iter=3, tol=0.0, team_warps=4)
+    with pytest.raises(ValueError, match="team_warps"):
+        solver.solve_device(prob, max_iter=3, tol=0.0, team_warps=3)
