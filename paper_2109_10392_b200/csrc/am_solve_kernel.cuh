@@ -326,7 +326,10 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
     }
     BMPC_PROF_NS(10);
     const int qstep = js * T.n;
-    constexpr int U = NS == 1 ? 4 : 2;  // obstacles in flight per sample (NS * U terms)
+#ifndef BMPC_UPAIR
+#define BMPC_UPAIR 2
+#endif
+    constexpr int U = NS == 1 ? 4 : BMPC_UPAIR;  // obstacles in flight per sample (NS * U terms)
     const double2* qp[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) qp[s] = T.xi + j0 * T.n + k[s];
@@ -465,7 +468,10 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
   constexpr int RX = NB + 6, RP = NB + 4;
 
   constexpr bool kStoreXY = bmpc_stores_xy(npad);  // else the obstacle block re-evaluates x, y
-  constexpr int CH = NKM < 2 ? NKM : 2;              // sample slots per pass A / B chunk
+#ifndef BMPC_CH
+#define BMPC_CH 2
+#endif
+  constexpr int CH = NKM < BMPC_CH ? NKM : BMPC_CH;  // sample slots per pass A / B chunk
   double* sPT = sm;                          // P^T, Pdot^T, Pddot^T
   double* sKxf = sPT + 3 * NB * npad;
   double* sKxa = sKxf + RX * C.kxs;
@@ -820,7 +826,8 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
       int r0 = wt;
 #pragma unroll 1
       for (; r0 + (CH - 1) * TW < NKM; r0 += CH * TW) chunk_a(std::integral_constant<int, CH>{}, r0);
-      if (CH > 1 && r0 < NKM) chunk_a(std::integral_constant<int, 1>{}, r0);  // CH = 2: one left
+#pragma unroll 1
+      for (; CH > 1 && r0 < NKM; r0 += TW) chunk_a(std::integral_constant<int, 1>{}, r0);  // remainder
       BMPC_PROF(2);
       // P^T theta of this warp's slots (again after an unwrap)
       auto pt_slots = [&]() {
@@ -1007,7 +1014,8 @@ __global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bm
       int r0 = wt;
 #pragma unroll 1
       for (; r0 + (CH - 1) * TW < NKM; r0 += CH * TW) chunk_b(std::integral_constant<int, CH>{}, r0);
-      if (CH > 1 && r0 < NKM) chunk_b(std::integral_constant<int, 1>{}, r0);
+#pragma unroll 1
+      for (; CH > 1 && r0 < NKM; r0 += TW) chunk_b(std::integral_constant<int, 1>{}, r0);
     }
     BMPC_PROF(12);
 
