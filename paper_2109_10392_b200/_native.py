@@ -72,6 +72,7 @@ class ScoreOut(Structure):
 EXPORTS = {
     # name: (argtypes, restype)
     "bmpc_abi_version": ([], c_int),
+    "bmpc_abi_layout": ([POINTER(c_longlong), c_int], c_int),
     "bmpc_last_error": ([], ctypes.c_char_p),
     "bmpc_ctx_create": ([c_int, c_int, c_double] + [_dp] * 9 + [POINTER(c_void_p)], c_int),
     "bmpc_ctx_destroy": ([c_void_p], c_int),

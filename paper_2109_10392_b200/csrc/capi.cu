@@ -1,6 +1,7 @@
 // capi.cu -- extern "C" boundary (include/batchmpc_b200.h) over the sm_100a kernels.
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stddef.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <string.h>
@@ -122,7 +123,21 @@ struct DevBuf {
 extern "C" {
 
 const char* bmpc_last_error(void) { return g_err.c_str(); }
-int bmpc_abi_version(void) { return 1; }
+int bmpc_abi_version(void) { return 2; }
+
+int bmpc_abi_layout(long long* out, int n) {
+  // sizes and last-field offsets of the ABI structs, for binding checks
+  const long long v[] = {
+      (long long)sizeof(bmpc_problem),    (long long)offsetof(bmpc_problem, a_max),
+      (long long)sizeof(bmpc_solve_opts), (long long)offsetof(bmpc_solve_opts, team_warps),
+      (long long)sizeof(bmpc_solve_out),  (long long)offsetof(bmpc_solve_out, converged),
+      (long long)sizeof(bmpc_score_spec), (long long)offsetof(bmpc_score_spec, collision_margin),
+      (long long)sizeof(bmpc_score_out),  (long long)offsetof(bmpc_score_out, n_feasible)};
+  const int count = (int)(sizeof(v) / sizeof(v[0]));
+  if (!out) return count;
+  for (int i = 0; i < n && i < count; ++i) out[i] = v[i];
+  return count;
+}
 
 int bmpc_carry_doubles(const bmpc_ctx* ctx) { return ctx ? carry_doubles(ctx->C.nb) : -1; }
 

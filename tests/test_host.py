@@ -148,7 +148,23 @@ def test_native_library_exports_every_header_symbol():
         assert hasattr(lib, nm), nm
     assert names <= set(_native.EXPORTS)
     lib2 = _native.load()
-    assert lib2.bmpc_abi_version() == 1
+    assert lib2.bmpc_abi_version() == 2
+
+
+def test_ctypes_struct_layout_matches_c():
+    """The ctypes Structures have the C sizes and field offsets (bmpc_abi_layout
+    needs no GPU)."""
+    lib = _native.load()
+    n = lib.bmpc_abi_layout(None, 0)
+    buf = (ctypes.c_longlong * n)()
+    lib.bmpc_abi_layout(buf, n)
+    got = list(buf)
+    exp = []
+    for cls, last in ((_native.Problem, "a_max"), (_native.SolveOpts, "team_warps"),
+                      (_native.SolveOut, "converged"), (_native.ScoreSpec, "collision_margin"),
+                      (_native.ScoreOut, "n_feasible")):
+        exp += [ctypes.sizeof(cls), getattr(cls, last).offset]
+    assert got == exp
 
 
 def test_no_oracle_in_product_package():
