@@ -448,10 +448,13 @@ template <int NB, int NKM, bool F32, bool TEAMS>
 #ifndef BMPC_MINB
 #define BMPC_MINB 1
 #endif
+#ifndef BMPC_TEAM_MINB
+#define BMPC_TEAM_MINB 1
+#endif
 #ifndef BMPC_MAXT
 #define BMPC_MAXT (32 * BMPC_MAX_WARPS)
 #endif
-__global__ void __launch_bounds__(BMPC_MAXT, BMPC_MINB) am_solve_kernel(const bmpc_dev_consts C,
+__global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB) am_solve_kernel(const bmpc_dev_consts C,
                                                        const bmpc_solve_args A) {
   extern __shared__ __align__(16) double sm[];
   // device-decided sweep count (the early-stop re-run): 0 = nothing to do
