@@ -16,6 +16,7 @@ from paper_2109_10392_b200.scenes import CONFIGS, make_workload  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--configs", nargs="+", default=["c0", "c1"])
 ap.add_argument("--teams", nargs="+", type=int, default=[1, 2, 4])
+ap.add_argument("--warps", type=int, default=0, help="warps per block (0 = auto)")
 a = ap.parse_args()
 for cfg_name in a.configs:
     cfg = CONFIGS[cfg_name]
@@ -29,7 +30,7 @@ for cfg_name in a.configs:
     out = D.solution_struct(sol)
     sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
     for tw in a.teams:
-        opts = nat.SolveOpts(max_iter=cfg.iters, tol=0.0, team_warps=tw)
+        opts = nat.SolveOpts(max_iter=cfg.iters, tol=0.0, team_warps=tw, warps_per_block=a.warps)
         ts = []
         for r in range(4):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
