@@ -63,3 +63,48 @@ def allgather_winner(record: np.ndarray, group=None) -> tuple[int | None, int]:
     dist.all_gather(out, t, group=group)
     recs = np.stack([o.cpu().numpy() for o in out])
     return merge_winners(recs)
+
+
+def allgather_winner_payload(record: np.ndarray, payload: np.ndarray, group=None):
+    """Like allgather_winner, with the winning column's data riding in the same
+    all-gather: each rank contributes its local winner record
+    and a fixed-size payload (e.g. the winner's coefficients, 3 n_b doubles);
+    every rank gets (best global index or None, n_feasible, winner payload or
+    None)."""
+    import torch
+    import torch.distributed as dist
+
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    pay = np.ascontiguousarray(payload, dtype=np.float64).ravel()
+    t = torch.tensor(np.concatenate([np.asarray(record, dtype=np.float64), pay]), device=dev)
+    out = [torch.empty_like(t) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(out, t, group=group)
+    rows = np.stack([o.cpu().numpy() for o in out])
+    best, nf = merge_winners(rows[:, :3])
+    if best is None:
+        return None, nf, None
+    owner = int(np.nonzero(rows[:, 1] == best)[0][0])
+    return best, nf, rows[owner, 3:].reshape(np.shape(payload))
+
+
+def global_first_converged(local_worst: np.ndarray, tol: float, group=None) -> tuple[int, bool]:
+    """Exact global early stop across shards (solver.py:437-439): the sweep
+    count and converged flag of the single-GPU solve, from each rank's worst
+    residual per sweep (max over its instances, NaN propagating) -- one
+    all-reduce(MAX) of the per-sweep vector.  Ranks whose local solve ran
+    longer re-run this many sweeps (instances are deterministic)."""
+    import torch
+    import torch.distributed as dist
+
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    w = np.asarray(local_worst, dtype=np.float64)
+    # NaN is "not converged": map it to +inf before the MAX (NaN has no MAX rule)
+    t = torch.tensor(np.where(np.isnan(w), np.inf, w), device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    g = t.cpu().numpy()
+    ok = np.nonzero(g <= tol)[0]
+    if ok.size == 0:
+        return len(g), False
+    return int(ok[0]) + 1, True

@@ -51,3 +51,74 @@ def test_gloo_world2_argmin(case):
     mp.spawn(_worker, args=(2, port, costs, feas, out), nprocs=2, join=True)
     expect = int(np.argmin(np.where(feas, costs, np.inf))) if feas.any() else -1
     assert out[0] == out[1] == (expect, int(feas.sum()))
+
+
+def _worker_payload(rank, world, port, costs, feas, coefs, out):
+    import torch.distributed as dist
+
+    from paper_2109_10392_b200.dist import allgather_winner_payload, local_winner, shard_range
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lo, hi = shard_range(len(costs), rank, world)
+        rec = local_winner(costs[lo:hi], feas[lo:hi], lo)
+        i = int(rec[1]) - lo if rec[1] >= 0 else 0
+        best, nf, pay = allgather_winner_payload(rec, coefs[:, :, lo + i])
+        out[rank] = (best if best is not None else -1, nf, None if pay is None else pay.tolist())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_winner_payload():
+    """The winning column's coefficients reach every rank inside the all-gather."""
+    rng = np.random.default_rng(3)
+    L, nb = 512, 11
+    costs = rng.normal(100.0, 10.0, L)
+    feas = rng.random(L) < 0.4
+    coefs = rng.normal(size=(3, nb, L))
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker_payload, args=(2, _free_port(), costs, feas, coefs, out), nprocs=2, join=True)
+    expect = int(np.argmin(np.where(feas, costs, np.inf)))
+    for r in (0, 1):
+        best, nf, pay = out[r]
+        assert best == expect and nf == int(feas.sum())
+        np.testing.assert_array_equal(np.array(pay), coefs[:, :, expect])
+
+
+def _worker_tol(rank, world, port, worst, tol, out):
+    import torch.distributed as dist
+
+    from paper_2109_10392_b200.dist import global_first_converged
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out[rank] = global_first_converged(worst[rank], tol)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", ["global_later", "never", "nan"])
+def test_gloo_world2_global_early_stop(case):
+    """Per-shard worst residuals -> the single-GPU early-stop sweep count."""
+    it = 30
+    t = np.arange(it, dtype=np.float64)
+    worst = np.stack([1.0 / (1 + t), 2.0 / (1 + t)])  # rank 1 converges later
+    tol = 0.1
+    if case == "never":
+        tol = 1e-9
+    if case == "nan":
+        worst[1, 25:] = np.nan
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker_tol, args=(2, _free_port(), worst, tol, out), nprocs=2, join=True)
+    g = np.max(np.where(np.isnan(worst), np.inf, worst), axis=0)
+    ok = np.nonzero(g <= tol)[0]
+    expect = (int(ok[0]) + 1, True) if ok.size else (it, False)
+    assert out[0] == out[1] == expect
+    if case == "global_later":
+        assert expect[0] == 20  # rank 0 alone would stop at 10
