@@ -41,7 +41,9 @@ __device__ __forceinline__ void score_instance(const ScoreParams& S, const doubl
     for (int j = 0; j < S.m; ++j) {
       const double2 q = __ldg(xi + j * S.n + k);
       const double wx = __ddiv_rn(__dsub_rn(x, q.x), S.a), wy = __ddiv_rn(__dsub_rn(y, q.y), S.b);
-      rmin = fmin(rmin, __dsqrt_rn(__dadd_rn(__dmul_rn(wx, wx), __dmul_rn(wy, wy))));
+      // the squared ratio: the correctly rounded sqrt is monotone, so the
+      // square root of the minimum is the minimum of the square roots
+      rmin = fmin(rmin, __dadd_rn(__dmul_rn(wx, wx), __dmul_rn(wy, wy)));
     }
     if (S.kind == 0) {
       const double dv = __dsub_rn(v, S.v_cruise);
@@ -53,7 +55,7 @@ __device__ __forceinline__ void score_instance(const ScoreParams& S, const doubl
     }
   }
   hmax = warp_max(hmax);
-  rmin = warp_min(rmin);
+  rmin = __dsqrt_rn(warp_min(rmin));
   cost = warp_sum(cost);
   if (__any_sync(BMPC_FULL, any_nan)) hmax = NAN;  // np.abs(psi).max() propagates NaN
   const double rmax = (r0 != r0 || r1 != r1 || r2 != r2) ? NAN : fmax(r0, fmax(r1, r2));
