@@ -221,6 +221,7 @@ def run_ours(args, rank, world, local_rank):
 
     def kernel_only():
         out = D.solution_struct(sol)
+        out.history = None  # as in the step
         nat.check(lib.bmpc_sweeps(ctx, ctypes.byref(pstruct), ctypes.byref(opts), iters, 0, 0, None,
                                   0, ctypes.byref(out), sp))
 

@@ -43,6 +43,7 @@ sol = D.alloc_solution(solver.basis.n_b, W.n, W.L, iters, False, dev)
 opts = nat.SolveOpts(max_iter=iters, tol=0.0, warps_per_block=args.warps,
                      precision=1 if args.precision == "fp32" else 0)
 out = D.solution_struct(sol)
+out.history = None  # the plan path does not write the residual history either
 ps = prob.c_struct()
 sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 lib = nat.load()
