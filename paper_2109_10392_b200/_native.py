@@ -78,6 +78,7 @@ EXPORTS = {
     "bmpc_ctx_destroy": ([c_void_p], c_int),
     "bmpc_carry_doubles": ([c_void_p], c_int),
     "bmpc_ctx_info": ([c_void_p, POINTER(c_int), POINTER(c_int), POINTER(c_int), POINTER(c_void_p)], c_int),
+    "bmpc_ctx_qp_info": ([c_void_p, POINTER(c_double), POINTER(c_double), POINTER(c_int)], c_int),
     "bmpc_solve": ([c_void_p, POINTER(Problem), POINTER(SolveOpts), POINTER(SolveOut), c_void_p], c_int),
     "bmpc_sweeps": ([c_void_p, POINTER(Problem), POINTER(SolveOpts), c_int, c_int, c_int, c_void_p,
                      c_int, POINTER(SolveOut), c_void_p], c_int),

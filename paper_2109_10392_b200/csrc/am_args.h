@@ -20,10 +20,22 @@ typedef struct {
   const double* Kxa;  // [nb+6][kxs] the per-axis KKT matrix (refinement residual)
   const double* Kpf;  // [nb+4][kps] inverse of the heading KKT matrix
   const double* Kpa;  // [nb+4][kps] the heading KKT matrix
-  const double* M;    // [4][nb][kms] F_axis^T F_axis, P^T P, Pddot^T Pddot, Pdot^T Pdot
+  const double* M;    // [4][nb][kms] F_axis^T F_axis, P^T P, Pddot^T Pddot, Pdot^T Pdot,
+                      // then the null-space QP blocks Z_xy, H_xy, Z_psi, H_psi [nb][kms],
+                      // B_xy [nb][8], B_psi [nb][4] (capi.cu: reduced_qp)
   int const_doubles;  // size of the whole constant image starting at PT (even; the
                       // kernel's shared-memory layout, copied in one bulk transfer)
+  int refine;         // QP refinement step: bit 0 xy, bit 1 psi
 } bmpc_dev_consts;
+
+// Doubles of the constant image (shared-memory layout): basis, the four Gram
+// blocks, the four null-space QP blocks, the two boundary maps and tau.
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+static inline size_t bmpc_const_image_doubles(int nb, int npad) {
+  return (size_t)3 * nb * npad + (size_t)8 * nb * (nb | 1) + (size_t)12 * nb + (size_t)npad;
+}
 
 enum { BMPC_INIT_COLD = 0, BMPC_INIT_WARM = 1, BMPC_INIT_RESUME = 2 };
 enum {

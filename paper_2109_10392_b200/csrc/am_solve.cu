@@ -8,10 +8,11 @@
 namespace bmpc {
 
 size_t am_solve_smem_bytes(int nb, int npad, int kxs, int kps, int warps, int team) {
-  // basis, KKT inverse + matrix for both systems, M, P^T P, Pddot^T Pddot, Pdot^T Pdot, tau, per-warp scratch
+  // the constant image (am_args.h) and the per-team scratch
+  (void)kxs;
+  (void)kps;
   return sizeof(double) *
-         ((size_t)3 * nb * npad + 2 * (size_t)(nb + 6) * kxs + 2 * (size_t)(nb + 4) * kps + (size_t)((4 * nb * (nb | 1) + 1) & ~1) + npad +
-          (size_t)(warps / team) * bmpc_team_doubles(npad, team));
+         (bmpc_const_image_doubles(nb, npad) + (size_t)(warps / team) * bmpc_team_doubles(npad, team));
 }
 
 #define BMPC_DECL(NB)                                                                      \

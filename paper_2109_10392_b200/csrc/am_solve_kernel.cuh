@@ -475,16 +475,19 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
 #define BMPC_CH 2
 #endif
   constexpr int CH = NKM < BMPC_CH ? NKM : BMPC_CH;  // sample slots per pass A / B chunk
+  // constant image (am_args.h, capi.cu bmpc_ctx_create)
   double* sPT = sm;                          // P^T, Pdot^T, Pddot^T
-  double* sKxf = sPT + 3 * NB * npad;
-  double* sKxa = sKxf + RX * C.kxs;
-  double* sKpf = sKxa + RX * C.kxs;
-  double* sKpa = sKpf + RP * C.kps;
-  double* sM = sKpa + RP * C.kps;   // F_axis^T F_axis = m P^T P + Pddot^T Pddot + Pdot^T Pdot
-  double* sMp = sM + NB * C.kms;    // P^T P
-  double* sMdd = sMp + NB * C.kms;  // Pddot^T Pddot
-  double* sMd = sMdd + NB * C.kms;  // Pdot^T Pdot
-  double* sTau = sM + ((4 * NB * C.kms + 1) & ~1);  // keep the double2 scratch 16-byte aligned
+  double* sM = sPT + 3 * NB * npad;  // F_axis^T F_axis = m P^T P + Pddot^T Pddot + Pdot^T Pdot
+  double* sMp = sM + NB * C.kms;     // P^T P
+  double* sMdd = sMp + NB * C.kms;   // Pddot^T Pddot
+  double* sMd = sMdd + NB * C.kms;   // Pdot^T Pdot
+  double* sZx = sMd + NB * C.kms;    // H_mm^-1 of the xy QP in full index space
+  double* sHx = sZx + NB * C.kms;    // H = Q + rho F_axis^T F_axis (refinement)
+  double* sZp = sHx + NB * C.kms;    // the same for the psi QP
+  double* sHp = sZp + NB * C.kms;
+  double* sBx = sHp + NB * C.kms;    // [NB][8]: c = Z rhs + B b (boundary map)
+  double* sBp = sBx + 8 * NB;        // [NB][4]
+  double* sTau = sBp + 4 * NB;       // even offset: the double2 scratch stays 16-byte aligned
   // team = the TW warps sharing one instance; each keeps private KKT vectors,
   // transpose buffer and exchange slots, the per-sample arrays are shared
   const int TW = TEAMS ? A.team : 1;  // compile-time 1 outside the team build
@@ -555,6 +558,59 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
   if (li < 6) bnd = A.b_xy[(size_t)(yax ? 6 + li : li) * L + inst];
   if (yax && li < 4) bps = A.b_psi[(size_t)li * L + inst];
 
+  // Null-space QP steps (capi.cu reduced_qp): the boundary rows pin the first
+  // and last XM0 (xy) / PM0 (psi) coefficients, c_f = T^-1 b, and the free
+  // ones solve H_mm c_m = rhs_m - H_mf c_f:  c = cb + Z rhs, with the
+  // per-instance boundary part cb = B b computed once here.
+  constexpr int XM0 = 3, XM1 = NB - 3, PM0 = 2, PM1 = NB - 2;
+  const int lrow = owner ? li : 0;
+  const int hbase = lane & 16;  // first lane of this lane's axis
+  const bool xfree = li >= XM0 && li < XM1;
+  const bool pfree = !yax && li >= PM0 && li < PM1;
+  const bool refine_xy = (C.refine & 1) != 0, refine_psi = (C.refine & 2) != 0;
+  double cbx, cbp;
+  {
+    const double* br = sBx + lrow * 8;
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int r = 0; r < 6; ++r) {
+      const double v = __shfl_sync(BMPC_FULL, bnd, hbase + r);
+      if (r & 1) s1 = fma(br[r], v, s1); else s0 = fma(br[r], v, s0);
+    }
+    cbx = s0 + s1;
+    const double* bq = sBp + lrow * 4;
+    double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const double v = __shfl_sync(BMPC_FULL, bps, 16 + r);
+      if (r & 1) t1 = fma(bq[r], v, t1); else t0 = fma(bq[r], v, t0);
+    }
+    cbp = t0 + t1;
+  }
+  // c = c + Z (rhs - H c) over the free rows (one refinement step,
+  // solver.py:164-168); `sh` is the lane's axis base for the shuffles
+  auto qp_refine = [&](const double* Zr, const double* Hr, double rhs, double c, int sh, int m0,
+                       int m1, bool free_row) {
+    double h[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int j = 0; j < NB; ++j) h[j & 3] = fma(Hr[j], __shfl_sync(BMPC_FULL, c, sh + j), h[j & 3]);
+    const double r = rhs - ((h[0] + h[1]) + (h[2] + h[3]));
+    double s[2] = {0.0, 0.0};
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+      if (j >= m0 && j < m1) s[j & 1] = fma(Zr[j], __shfl_sync(BMPC_FULL, r, sh + j), s[j & 1]);
+    return free_row ? c + (s[0] + s[1]) : c;
+  };
+  // plain apply c = cb + Z rhs
+  auto qp_apply = [&](const double* Zr, double rhs, double cb, int sh, int m0, int m1,
+                      bool free_row) {
+    double s[2] = {0.0, 0.0};
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+      if (j >= m0 && j < m1) s[j & 1] = fma(Zr[j], __shfl_sync(BMPC_FULL, rhs, sh + j), s[j & 1]);
+    return free_row ? cb + (s[0] + s[1]) : cb;
+  };
+
   // ---------------------------------------------------------------- init ----
   bool have_sol = false;  // [c; mu] of the previous sweep available for refinement
   if (A.init_mode == BMPC_INIT_RESUME) {
@@ -565,12 +621,9 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
       G = cr[(yax ? 4 : 3) * NB + li];
     }
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int q = lane + 32 * h;
-      if (q < 2 * RX) ws.sol[(q >= RX ? kYOff : 0) + q - (q >= RX ? RX : 0)] = cr[5 * NB + q];
-    }
-    if (lane < RP) ws.solp[lane] = cr[5 * NB + 2 * RX + lane];
-    __syncwarp();
+    // the previous sweep's coefficients: the refinement base
+    if (owner) cown = cr[5 * NB + (yax ? RX : 0) + li];
+    if (owner && !yax) cpown = cr[5 * NB + 2 * RX + li];
     have_sol = true;
   } else {
     // Initial targets g = assemble_g(alpha, d, alpha_a, d_a, v, psi) contracted
@@ -671,54 +724,18 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
   // ----------------------------------------------------------- AM sweeps ----
   for (int t = 0; t < iters; ++t) {
     const bool last = t == iters - 1;
-    // (1) xy QP: [c; mu] = K^-1 [rho*G + lambda ; b] with one refinement step,
-    //     the 2*(nb+6) rows of both axes spread over the lanes (two per lane max).
-    //     The first sweep refines the plain inverse apply; later sweeps refine
-    //     the previous sweep's [c; mu] instead -- the same accuracy
-    //     for one matrix pass less.
+    // (1) xy QP (solver.py:302-312) in null-space form: c = cb + Z (rho G +
+    //     lambda), lane i / 16+i coefficient i of x / y.  Ill-conditioned
+    //     shapes add one refinement step; it starts from the previous sweep's
+    //     c once there is one (the same accuracy, one matrix pass less).
     {
-      double* rb = ws.bc + (yax ? kYOff : 0);
-      if (owner) rb[li] = rho * G + lam;
-      if (li < 6) rb[NB + li] = bnd;
+      const double rhs = rho * G + lam;  // owner lanes (G = lam = 0 elsewhere)
+      const double* zr = sZx + lrow * C.kms;
+      double c = (refine_xy && have_sol) ? cown : qp_apply(zr, rhs, cbx, hbase, XM0, XM1, xfree);
+      if (refine_xy) c = qp_refine(zr, sHx + lrow * C.kms, rhs, c, hbase, XM0, XM1, xfree);
+      cown = c;
+      if (owner) ws.cxy[2 * li + (yax ? 1 : 0)] = c;
       __syncwarp();
-      // rows q = lane and lane + 32 of the stacked (x, y) system: both dot
-      // products are evaluated unconditionally (clamped rows) so they
-      // interleave; only valid rows are stored
-      const int q0 = lane < 2 * RX ? lane : 2 * RX - 1, q1 = lane + 32 < 2 * RX ? lane + 32 : 2 * RX - 1;
-      const int ax0 = q0 >= RX ? 1 : 0, row0 = q0 - ax0 * RX;
-      const int ax1 = q1 >= RX ? 1 : 0, row1 = q1 - ax1 * RX;
-      const int o0 = ax0 * kYOff + row0, o1 = ax1 * kYOff + row1;
-      const bool w0 = lane < 2 * RX, w1 = lane + 32 < 2 * RX;
-      if (!have_sol) {
-        const double d0 = kkt_row_dot<RX>(sKxf + row0 * C.kxs, ws.bc + ax0 * kYOff);
-        const double d1 = kkt_row_dot<RX>(sKxf + row1 * C.kxs, ws.bc + ax1 * kYOff);
-        if (w0) ws.sol[o0] = d0;
-        if (w1) ws.sol[o1] = d1;
-        __syncwarp();
-      }
-      {
-        const double d0 = kkt_row_dot<RX>(sKxa + row0 * C.kxs, ws.sol + ax0 * kYOff);
-        const double d1 = kkt_row_dot<RX>(sKxa + row1 * C.kxs, ws.sol + ax1 * kYOff);
-        const double r0 = ws.bc[o0] - d0, r1 = ws.bc[o1] - d1;
-        if (w0) ws.res[o0] = r0;
-        if (w1) ws.res[o1] = r1;
-      }
-      __syncwarp();
-      {  // each lane rewrites only its own rows of sol
-        const double d0 = kkt_row_dot<RX>(sKxf + row0 * C.kxs, ws.res + ax0 * kYOff);
-        const double d1 = kkt_row_dot<RX>(sKxf + row1 * C.kxs, ws.res + ax1 * kYOff);
-        const double s0 = ws.sol[o0] + d0, s1 = ws.sol[o1] + d1;
-        if (w0) {
-          ws.sol[o0] = s0;
-          if (row0 < NB) ws.cxy[2 * row0 + ax0] = s0;
-        }
-        if (w1) {
-          ws.sol[o1] = s1;
-          if (row1 < NB) ws.cxy[2 * row1 + ax1] = s1;
-        }
-      }
-      __syncwarp();
-      if (owner) cown = ws.cxy[2 * li + (yax ? 1 : 0)];
     }
     BMPC_PROF(1);
     const double2* __restrict__ cxy = reinterpret_cast<const double2*>(ws.cxy);
@@ -915,24 +932,15 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
     }
     BMPC_PROF(5);
 
-    // (4) psi QP
+    // (4) psi QP (solver.py:322-328), null-space form on lanes 0..NB-1
     {
-      if (!yax && owner) ws.bc[li] = rho * pth + lamp;
-      if (yax && li < 4) ws.bc[NB + li] = bps;
+      const double rhs = rho * pth + lamp;  // x owner lanes
+      const double* zr = sZp + lrow * C.kms;
+      double c = (refine_psi && have_sol) ? cpown : qp_apply(zr, rhs, cbp, 0, PM0, PM1, pfree);
+      if (refine_psi) c = qp_refine(zr, sHp + lrow * C.kms, rhs, c, 0, PM0, PM1, pfree);
+      cpown = c;
+      if (!yax && owner) ws.cp[li] = c;
       __syncwarp();
-      if (!have_sol) {
-        if (lane < RP) ws.solp[lane] = kkt_row_dot<RP>(sKpf + lane * C.kps, ws.bc);
-        __syncwarp();
-      }
-      if (lane < RP) ws.res[lane] = ws.bc[lane] - kkt_row_dot<RP>(sKpa + lane * C.kps, ws.solp);
-      __syncwarp();
-      if (lane < RP) {
-        const double s = ws.solp[lane] + kkt_row_dot<RP>(sKpf + lane * C.kps, ws.res);
-        ws.solp[lane] = s;
-        if (lane < NB) ws.cp[lane] = s;
-      }
-      __syncwarp();
-      if (!yax && owner) cpown = ws.cp[li];
     }
     // lambda_psi step P^T (psi - theta) = (P^T P) c_psi - P^T theta (solver.py:494)
     double Lp = 0.0;
@@ -1145,14 +1153,10 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
       cr[(yax ? 4 : 3) * NB + li] = G;
     }
   }
-  if (A.flags & BMPC_F_CARRY) {  // the refinement base of the next sweep
+  if ((A.flags & BMPC_F_CARRY) && owner) {  // the refinement base of the next sweep
     double* cr = A.carry + (size_t)inst * carry_doubles(NB);
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int q = lane + 32 * h;
-      if (q < 2 * RX) cr[5 * NB + q] = ws.sol[(q >= RX ? kYOff : 0) + q - (q >= RX ? RX : 0)];
-    }
-    if (lane < RP) cr[5 * NB + 2 * RX + lane] = ws.solp[lane];
+    cr[5 * NB + (yax ? RX : 0) + li] = cown;
+    if (!yax) cr[5 * NB + 2 * RX + li] = cpown;
   }
   BMPC_PROF(9);
   BMPC_PROF_FLUSH

@@ -4,6 +4,7 @@
 #include <stddef.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <mutex>
@@ -77,6 +78,7 @@ cudaError_t op_block_norms(int n, long long l, long long mn, const double* r_x, 
 struct bmpc_ctx {
   bmpc_dev_consts C;
   double* dmem = nullptr;  // one allocation for every constant
+  double cond_xy = 0.0, cond_psi = 0.0;  // 1-norm condition numbers of the reduced Hessians
   int sms = 148;
   int smem_optin = 227 * 1024;
   // pinned staging for bmpc_plan_host's results (grown on demand)
@@ -86,6 +88,8 @@ struct bmpc_ctx {
 };
 
 static thread_local std::string g_err;
+// reduced-Hessian condition number above which the QP steps refine
+static constexpr double kRefineCond = 1.0e4;
 
 static int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -141,6 +145,105 @@ int bmpc_abi_layout(long long* out, int n) {
 
 int bmpc_carry_doubles(const bmpc_ctx* ctx) { return ctx ? carry_doubles(ctx->C.nb) : -1; }
 
+}  // extern "C"
+
+// Gauss-Jordan inverse with partial pivoting in extended precision (the
+// reduced QP blocks are at most 12 x 12); false if singular.
+static bool inverse_ld(int k, std::vector<long double>& a, std::vector<long double>& inv) {
+  inv.assign((size_t)k * k, 0.0L);
+  for (int i = 0; i < k; ++i) inv[(size_t)i * k + i] = 1.0L;
+  for (int col = 0; col < k; ++col) {
+    int piv = col;
+    for (int r = col + 1; r < k; ++r)
+      if (fabsl(a[(size_t)r * k + col]) > fabsl(a[(size_t)piv * k + col])) piv = r;
+    if (a[(size_t)piv * k + col] == 0.0L) return false;
+    if (piv != col)
+      for (int j = 0; j < k; ++j) {
+        std::swap(a[(size_t)piv * k + j], a[(size_t)col * k + j]);
+        std::swap(inv[(size_t)piv * k + j], inv[(size_t)col * k + j]);
+      }
+    const long double d = a[(size_t)col * k + col];
+    for (int j = 0; j < k; ++j) {
+      a[(size_t)col * k + j] /= d;
+      inv[(size_t)col * k + j] /= d;
+    }
+    for (int r = 0; r < k; ++r) {
+      if (r == col) continue;
+      const long double f = a[(size_t)r * k + col];
+      if (f == 0.0L) continue;
+      for (int j = 0; j < k; ++j) {
+        a[(size_t)r * k + j] -= f * a[(size_t)col * k + j];
+        inv[(size_t)r * k + j] -= f * inv[(size_t)col * k + j];
+      }
+    }
+  }
+  return true;
+}
+
+// Null-space form of one KKT block K = [[H, A^T], [A, 0]] (solver.py:120-176).
+// The default BoundarySpec pins orders 0..rows/2-1 at both ends, and the
+// Bernstein endpoint rows are supported on the first / last rows/2
+// coefficients only (basis.py:45-49), so A fixes those coefficients c_f
+// through a triangular system and leaves the middle ones free:
+//   c_f = T^-1 b,  c_m = H_mm^-1 (rhs_m - H_mf c_f).
+// Outputs in the full coefficient index space: Z = H_mm^-1 placed in the
+// middle block (zero rows/columns for fixed coefficients), B (nb x rows) with
+// c = Z rhs + B b, and the 1-norm condition number of H_mm.
+static int reduced_qp(int nb, int rows, const double* K, std::vector<double>& Z,
+                      std::vector<double>& B, double* cond1) {
+  const int kd = nb + rows, h = rows / 2, nm = nb - rows;
+  if (nm < 0) return fail(BMPC_EINVAL, "boundary rows exceed the basis size");
+  auto fixed_col = [&](int q) { return q < h ? q : nb - rows + q; };  // q-th fixed coefficient
+  auto mid_col = [&](int q) { return h + q; };
+  for (int r = 0; r < rows; ++r)
+    for (int q = 0; q < nm; ++q)
+      if (K[(size_t)(nb + r) * kd + mid_col(q)] != 0.0)
+        return fail(BMPC_EINVAL, "boundary rows are not supported on the end coefficients");
+  std::vector<long double> T((size_t)rows * rows), Ti, Hm((size_t)nm * nm), Hi;
+  for (int r = 0; r < rows; ++r)
+    for (int q = 0; q < rows; ++q) T[(size_t)r * rows + q] = K[(size_t)(nb + r) * kd + fixed_col(q)];
+  if (!inverse_ld(rows, T, Ti)) return fail(BMPC_ESINGULAR, "KKT factorization failed: singular boundary block");
+  for (int i = 0; i < nm; ++i)
+    for (int j = 0; j < nm; ++j) Hm[(size_t)i * nm + j] = K[(size_t)mid_col(i) * kd + mid_col(j)];
+  std::vector<long double> Hm0 = Hm;
+  if (nm > 0 && !inverse_ld(nm, Hm, Hi)) return fail(BMPC_ESINGULAR, "KKT factorization failed: singular reduced Hessian");
+  Z.assign((size_t)nb * nb, 0.0);
+  B.assign((size_t)nb * rows, 0.0);
+  for (int i = 0; i < nm; ++i)
+    for (int j = 0; j < nm; ++j) Z[(size_t)mid_col(i) * nb + mid_col(j)] = (double)Hi[(size_t)i * nm + j];
+  for (int q = 0; q < rows; ++q)
+    for (int r = 0; r < rows; ++r) B[(size_t)fixed_col(q) * rows + r] = (double)Ti[(size_t)q * rows + r];
+  for (int i = 0; i < nm; ++i)
+    for (int r = 0; r < rows; ++r) {
+      long double s = 0.0L;  // -(H_mm^-1 H_mf T^-1)[i][r]
+      for (int j = 0; j < nm; ++j) {
+        long double hf = 0.0L;
+        for (int q = 0; q < rows; ++q)
+          hf += (long double)K[(size_t)mid_col(j) * kd + fixed_col(q)] * Ti[(size_t)q * rows + r];
+        s += Hi[(size_t)i * nm + j] * hf;
+      }
+      B[(size_t)mid_col(i) * rows + r] = (double)(-s);
+    }
+  long double n1 = 0.0L, n2 = 0.0L;
+  for (int j = 0; j < nm; ++j) {
+    long double s1 = 0.0L, s2 = 0.0L;
+    for (int i = 0; i < nm; ++i) {
+      s1 += fabsl(Hm0[(size_t)i * nm + j]);
+      s2 += fabsl(Hi[(size_t)i * nm + j]);
+    }
+    n1 = s1 > n1 ? s1 : n1;
+    n2 = s2 > n2 ? s2 : n2;
+  }
+  *cond1 = (double)(n1 * n2);
+  for (double v : Z)
+    if (!isfinite(v)) return fail(BMPC_ESINGULAR, "KKT factorization failed: non-finite reduced inverse");
+  for (double v : B)
+    if (!isfinite(v)) return fail(BMPC_ESINGULAR, "KKT factorization failed: non-finite boundary map");
+  return BMPC_OK;
+}
+
+extern "C" {
+
 int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pdot,
                     const double* Pddot, const double* tau, const double* kinv_axis,
                     const double* k_axis, const double* kinv_psi, const double* k_psi,
@@ -148,7 +251,7 @@ int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pd
   if (!out || !P || !Pdot || !Pddot || !tau || !kinv_axis || !k_axis || !kinv_psi || !k_psi ||
       !ftf_axis)
     return fail(BMPC_EINVAL, "bmpc_ctx_create: null argument");
-  if (nb < 4 || nb > 16) return fail(BMPC_EINVAL, "bmpc_ctx_create: need 4 <= n_b <= 16");
+  if (nb < 6 || nb > 16) return fail(BMPC_EINVAL, "bmpc_ctx_create: need 6 <= n_b <= 16");
   if (n < 2 || n > 256) return fail(BMPC_EINVAL, "bmpc_ctx_create: need 2 <= n <= 256");
   if (!(rho > 0.0)) return fail(BMPC_EINVAL, "bmpc_ctx_create: rho must be positive");
   const int rx = nb + 6, rp = nb + 4;
@@ -156,30 +259,34 @@ int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pd
     if (!isfinite(kinv_axis[i])) return fail(BMPC_ESINGULAR, "KKT xy inverse is not finite");
   for (int i = 0; i < rp * rp; ++i)
     if (!isfinite(kinv_psi[i])) return fail(BMPC_ESINGULAR, "KKT psi inverse is not finite");
+  // null-space form of both QP blocks (the persistent kernel's QP steps)
+  std::vector<double> Zx, Bx, Zp, Bp;
+  double cond_x = 0.0, cond_p = 0.0;
+  int rc = reduced_qp(nb, 6, k_axis, Zx, Bx, &cond_x);
+  if (rc != BMPC_OK) return rc;
+  rc = reduced_qp(nb, 4, k_psi, Zp, Bp, &cond_p);
+  if (rc != BMPC_OK) return rc;
   // = 32 * NKM of the kernel instantiations (csrc/am_inst.cu)
   const int npad = n <= 64 ? 64 : (n <= 128 ? 128 : (n <= 224 ? 224 : 256));
   const int kxs = rx | 1, kps = rp | 1, kms = nb | 1;
   const size_t nPT = (size_t)3 * nb * npad, nKx = (size_t)rx * kxs, nKp = (size_t)rp * kps;
-  // the kernel's shared-memory image: M and P^T P padded to an even count so
-  // tau (and the total) stay 16-byte aligned for the bulk copy
-  const size_t nM = ((size_t)4 * nb * kms + 1) & ~(size_t)1;
-  std::vector<double> h(nPT + 2 * nKx + 2 * nKp + nM + npad, 0.0);
+  // The kernel's shared-memory image (every block an even number of doubles,
+  // so tau and the total stay 16-byte aligned for the bulk copy):
+  //   P^T, Pdot^T, Pddot^T | F_axis^T F_axis, P^T P, Pddot^T Pddot, Pdot^T Pdot |
+  //   Z_xy, H_xy, Z_psi, H_psi | B_xy [nb][8], B_psi [nb][4] | tau
+  // followed in global memory only by the full KKT inverse / matrix pairs
+  // (the step API's refined solves, csrc/steps.cu).
+  const size_t nimg = bmpc_const_image_doubles(nb, npad);
+  std::vector<double> h(nimg + 2 * nKx + 2 * nKp, 0.0);
   const double* mats[3] = {P, Pdot, Pddot};
   for (int q = 0; q < 3; ++q)
     for (int i = 0; i < nb; ++i)
       for (int k = 0; k < n; ++k) h[((size_t)q * nb + i) * npad + k] = mats[q][(size_t)k * nb + i];
-  size_t o = nPT;
-  const double* blocks[5] = {kinv_axis, k_axis, kinv_psi, k_psi, ftf_axis};
-  const int dims[5] = {rx, rx, rp, rp, nb}, strides[5] = {kxs, kxs, kps, kps, kms};
-  size_t offs[5];
-  for (int q = 0; q < 5; ++q) {
-    offs[q] = o;
-    for (int i = 0; i < dims[q]; ++i)
-      for (int j = 0; j < dims[q]; ++j) h[o + (size_t)i * strides[q] + j] = blocks[q][(size_t)i * dims[q] + j];
-    o += (size_t)dims[q] * strides[q];
-  }
-  // P^T P, Pddot^T Pddot, Pdot^T Pdot right after M (the exact-form sweep and
-  // multiplier identities), accumulated in extended precision
+  const size_t oM = nPT;
+  for (int i = 0; i < nb; ++i)
+    for (int j = 0; j < nb; ++j) h[oM + (size_t)i * kms + j] = ftf_axis[(size_t)i * nb + j];
+  // P^T P, Pddot^T Pddot, Pdot^T Pdot right after F_axis^T F_axis (the
+  // exact-form sweep and multiplier identities), in extended precision
   const double* grams[3] = {P, Pddot, Pdot};
   for (int q = 0; q < 3; ++q)
     for (int i = 0; i < nb; ++i)
@@ -187,10 +294,37 @@ int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pd
         long double acc = 0.0L;
         for (int k = 0; k < n; ++k)
           acc += (long double)grams[q][(size_t)k * nb + i] * grams[q][(size_t)k * nb + j];
-        h[o + ((size_t)q * nb + i) * kms + j] = (double)acc;
+        h[oM + ((size_t)(q + 1) * nb + i) * kms + j] = (double)acc;
       }
-  o = offs[4] + nM;
-  for (int k = 0; k < n; ++k) h[o + k] = tau[k];
+  size_t o = oM + (size_t)4 * nb * kms;
+  const double* qp[4] = {Zx.data(), k_axis, Zp.data(), k_psi};
+  const int qps[4] = {nb, rx, nb, rp};  // source row strides (H = top-left nb x nb of K)
+  for (int q = 0; q < 4; ++q, o += (size_t)nb * kms)
+    for (int i = 0; i < nb; ++i)
+      for (int j = 0; j < nb; ++j) h[o + (size_t)i * kms + j] = qp[q][(size_t)i * qps[q] + j];
+  for (int i = 0; i < nb; ++i)
+    for (int r = 0; r < 6; ++r) h[o + (size_t)i * 8 + r] = Bx[(size_t)i * 6 + r];
+  o += (size_t)8 * nb;
+  for (int i = 0; i < nb; ++i)
+    for (int r = 0; r < 4; ++r) h[o + (size_t)i * 4 + r] = Bp[(size_t)i * 4 + r];
+  o += (size_t)4 * nb;
+  const size_t otau = o;
+  for (int k = 0; k < n; ++k) h[otau + k] = tau[k];
+  size_t offs[4];
+  o = nimg;
+  const double* blocks[4] = {kinv_axis, k_axis, kinv_psi, k_psi};
+  const int dims[4] = {rx, rx, rp, rp}, strides[4] = {kxs, kxs, kps, kps};
+  for (int q = 0; q < 4; ++q) {
+    offs[q] = o;
+    for (int i = 0; i < dims[q]; ++i)
+      for (int j = 0; j < dims[q]; ++j) h[o + (size_t)i * strides[q] + j] = blocks[q][(size_t)i * dims[q] + j];
+    o += (size_t)dims[q] * strides[q];
+  }
+  // One refinement step (solver.py:164-168) per QP only where the reduced
+  // Hessian is ill-conditioned: the explicit inverse loses about cond * eps.
+  // BMPC_QP_REFINE=0/1/2/3 (bit 0 xy, bit 1 psi) overrides, for experiments.
+  int refine = (cond_x > kRefineCond ? 1 : 0) | (cond_p > kRefineCond ? 2 : 0);
+  if (const char* env = getenv("BMPC_QP_REFINE")) refine = atoi(env) & 3;
   bmpc_ctx* c = new bmpc_ctx();
   cudaError_t e = cudaMalloc(&c->dmem, h.size() * sizeof(double));
   if (e != cudaSuccess) { delete c; return cuda_fail(e, "bmpc_ctx_create/cudaMalloc"); }
@@ -219,9 +353,12 @@ int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pd
   c->C.Kxa = c->dmem + offs[1];
   c->C.Kpf = c->dmem + offs[2];
   c->C.Kpa = c->dmem + offs[3];
-  c->C.M = c->dmem + offs[4];
-  c->C.tau = c->dmem + o;
-  c->C.const_doubles = (int)h.size();
+  c->C.M = c->dmem + oM;
+  c->C.tau = c->dmem + otau;
+  c->C.const_doubles = (int)nimg;
+  c->C.refine = refine;
+  c->cond_xy = cond_x;
+  c->cond_psi = cond_p;
   *out = c;
   return BMPC_OK;
 }
@@ -231,6 +368,14 @@ int bmpc_ctx_destroy(bmpc_ctx* ctx) {
   cudaFree(ctx->dmem);
   if (ctx->stage) cudaFreeHost(ctx->stage);
   delete ctx;
+  return BMPC_OK;
+}
+
+int bmpc_ctx_qp_info(const bmpc_ctx* ctx, double* cond_xy, double* cond_psi, int* refine) {
+  if (!ctx) return fail(BMPC_EINVAL, "null ctx");
+  if (cond_xy) *cond_xy = ctx->cond_xy;
+  if (cond_psi) *cond_psi = ctx->cond_psi;
+  if (refine) *refine = ctx->C.refine;
   return BMPC_OK;
 }
 

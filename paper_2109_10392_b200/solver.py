@@ -215,8 +215,8 @@ class BatchSolver:
             raise ValueError("constant matrices were built from a different basis")
         if mats.boundary != BoundarySpec():
             raise ValueError("the device path supports the default BoundarySpec only")
-        if not 4 <= basis.n_b <= 16:
-            raise ValueError(f"basis size {basis.n_b} outside the supported 4..16")
+        if not 6 <= basis.n_b <= 16:
+            raise ValueError(f"basis size {basis.n_b} outside the supported 6..16")
         if not 2 <= basis.grid.n <= 256:
             raise ValueError(f"horizon samples {basis.grid.n} outside the supported 2..256")
         self.basis = basis
@@ -250,6 +250,16 @@ class BatchSolver:
                   "bmpc_ctx_create")
         self._ctx, self._ctx_device = c, dev
         return c
+
+    def qp_info(self) -> dict:
+        """Null-space QP form of the device solve: the 1-norm condition numbers
+        of the reduced xy / psi Hessians and whether each QP step refines."""
+        c = self._context()
+        cx, cp, rf = ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
+        nat.check(nat.load().bmpc_ctx_qp_info(c, ctypes.byref(cx), ctypes.byref(cp), ctypes.byref(rf)),
+                  "bmpc_ctx_qp_info")
+        return {"cond_xy": cx.value, "cond_psi": cp.value, "refine_xy": bool(rf.value & 1),
+                "refine_psi": bool(rf.value & 2)}
 
     def __del__(self):
         try:
