@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
   constexpr int CH = NKM < BMPC_CH ? NKM : BMPC_CH;  // sample slots per pass A / B chunk
   // constant image (am_args.h, capi.cu bmpc_ctx_create)
   double* sPT = sm;                          // P^T, Pdot^T, Pddot^T
-  double* sM = sPT + 3 * NB * npad;  // F_axis^T F_axis = m P^T P + Pddot^T Pddot + Pdot^T Pdot
+  double* sM = sPT + 3 * NB * npad;  // m P^T P + Pddot^T Pddot (written above)
   double* sMp = sM + NB * C.kms;     // P^T P
   double* sMdd = sMp + NB * C.kms;   // Pddot^T Pddot
   double* sMd = sMdd + NB * C.kms;   // Pdot^T Pdot
@@ -534,6 +534,15 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
   }
   __syncthreads();  // the initialised barrier is visible to every thread
   mbar_wait_parity(&s_cbar, 0);
+  {
+    // the G Gram block of this launch's obstacle count: m P^T P + Pddot^T Pddot
+    // (overwrites the image's F_axis^T F_axis block, which the sweep never reads)
+    const double md = (double)A.m;
+    double* g = sm + 3 * NB * npad;
+    for (int q = threadIdx.x; q < NB * C.kms; q += blockDim.x)
+      g[q] = fma(md, g[NB * C.kms + q], g[2 * NB * C.kms + q]);
+    __syncthreads();
+  }
 
   const int inst = blockIdx.x * (W / TW) + team;
   if (inst >= L) return;  // team-uniform; no block-wide barriers below this point
@@ -957,6 +966,9 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
     //     contracted onto Pdot.
     // full chunks of CH slots (every slot valid at compile time), then the
     // NKM % CH remainder; chunks stay rolled for the instruction cache
+    double cps_reg[NB];  // c_psi, held in registers for every chunk
+#pragma unroll
+    for (int i = 0; i < NB; ++i) cps_reg[i] = ws.cp[i];
     auto chunk_b = [&](auto nsc, const int r0) {
       constexpr int NSC = decltype(nsc)::value;
       int k[NSC];
@@ -968,13 +980,20 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
         v[s] = k[s] < n;
         ps[s] = 0.0;
       }
+      // two partial sums per slot: half the dependent chain
+      double ps1[NSC];
+#pragma unroll
+      for (int s = 0; s < NSC; ++s) ps1[s] = 0.0;
 #pragma unroll
       for (int i = 0; i < NB; ++i) {
-        const double cpi = ws.cp[i];
 #pragma unroll
-        for (int s = 0; s < NSC; ++s)
-          ps[s] = fma(sP[i * npad + k[s]], cpi, ps[s]);
+        for (int s = 0; s < NSC; ++s) {
+          if (i & 1) ps1[s] = fma(sP[i * npad + k[s]], cps_reg[i], ps1[s]);
+          else ps[s] = fma(sP[i * npad + k[s]], cps_reg[i], ps[s]);
+        }
       }
+#pragma unroll
+      for (int s = 0; s < NSC; ++s) ps[s] += ps1[s];
       // branch-free sin/cos for every slot first, so the slots interleave; the
       // full-range fallback (huge / non-finite headings) is one rare branch
       double sps[NSC], cps[NSC];
@@ -1067,29 +1086,26 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
     }
     BMPC_PROF(6);
     if (owner) {
-      const double* m1 = sMp + li * C.kms;
-      const double* m2 = sMdd + li * C.kms;
-      const double* m3 = sMd + li * C.kms;
-      double a1[2] = {0.0, 0.0}, a2[2] = {0.0, 0.0}, a3[2] = {0.0, 0.0};
+      const double* m1 = sM + li * C.kms;   // m P^T P + Pddot^T Pddot
+      const double* m3 = sMd + li * C.kms;  // Pdot^T Pdot
+      double a1[2] = {0.0, 0.0}, a3[2] = {0.0, 0.0};
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
         const double cj = ws.cxy[2 * j + (yax ? 1 : 0)];
         a1[j & 1] = fma(m1[j], cj, a1[j & 1]);
-        a2[j & 1] = fma(m2[j], cj, a2[j & 1]);
         a3[j & 1] = fma(m3[j], cj, a3[j & 1]);
       }
       const double rest = gn;
-      G = fma((double)m, a1[0] + a1[1], a2[0] + a2[1]) + rest;
+      G = (a1[0] + a1[1]) + rest;
       lam -= rho * ((a3[0] + a3[1]) - rest);
     }
     if (!yax && owner) lamp -= rho * Lp;
     const double res = sqrt(lane == 16 ? sqo : (lane == 17 ? sqa : sqn));  // lanes 16..18
     if (A.notconv && wt == 0) {  // global early stop: flag this sweep unless every residual <= tol
       const bool nc = __any_sync(BMPC_FULL, lane >= 16 && lane < 19 && !(res <= A.tol));
-      if (lane == 0 && nc) {
-        int* f = A.notconv + A.hist_offset + t;
-        if (*(volatile int*)f == 0) *f = 1;
-      }
+      // a plain store: the flag only ever goes 0 -> 1, and a read-before-write
+      // would stall the warp on a coherent L2 round trip every sweep
+      if (lane == 0 && nc) A.notconv[A.hist_offset + t] = 1;
     }
     if (lane >= 16 && lane < 19 && wt == 0) {
       if (A.flags & BMPC_F_HISTORY)

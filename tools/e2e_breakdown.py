@@ -71,3 +71,23 @@ hpg = np.empty(big.numel())
 t_d2h_page = timeit(lambda: hpg.__setitem__(slice(None), big.cpu().numpy()), args.reps)
 print(f"{args.config}: plan_batch {t_plan:.3f} ms | device bmpc_plan {t_dev:.3f} ms | "
       f"D2H coef pinned {t_d2h_pin:.3f} ms pageable {t_d2h_page:.3f} ms")
+
+# the C-ABI host entry alone (structs prebuilt): plan_batch minus Python
+xi_x, xi_y = h.xi_x, h.xi_y
+prob_h = nat.Problem(W.m, W.l, W.S, xi_x.ctypes.data, xi_y.ctypes.data, h.b_xy.ctypes.data,
+                     h.b_psi.ctypes.data, W.a, W.b, W.v_min, W.v_max, W.a_max)
+coef = np.empty((3, solver.basis.n_b, W.L))
+res = np.empty((3, W.L))
+out_h = nat.SolveOut(coef[0].ctypes.data, coef[1].ctypes.data, coef[2].ctypes.data, None, None,
+                     None, None, None, res.ctypes.data, 0, 0)
+meta, mr, hm = np.empty((3, W.L))
+flags = np.empty(W.L, dtype=np.uint8)
+best, amin, ahc, nf = np.empty((4, W.S), dtype=np.int64)
+so = nat.ScoreOut(meta.ctypes.data, mr.ctypes.data, hm.ctypes.data, flags.ctypes.data,
+                  best.ctypes.data, amin.ctypes.data, ahc.ctypes.data, nf.ctypes.data)
+t_host = timeit(lambda: nat.check(lib.bmpc_plan_host(ctx, ctypes.byref(prob_h), ctypes.byref(opts),
+                                                     ctypes.byref(out_h), ctypes.byref(sspec),
+                                                     ctypes.byref(so), sp)), args.reps)
+t_empty = timeit(lambda: torch.cuda.synchronize(), args.reps)
+print(f"{args.config}: bmpc_plan_host (ctypes, structs prebuilt) {t_host:.3f} ms | "
+      f"python plan_batch overhead {t_plan - t_host:.3f} ms | bare sync {t_empty:.3f} ms")
