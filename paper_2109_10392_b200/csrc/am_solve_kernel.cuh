@@ -1125,16 +1125,28 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
     const ScoreParams sp{n, m, F.kind, a, b, F.v_cruise, F.v_max, F.y_rl, F.w1, F.w2,
                          F.heading_limit, F.residual_tol, F.ratio_min};
     const double2* __restrict__ cxy2 = reinterpret_cast<const double2*>(ws.cxy);
+    // x, y, xdot, ydot of the final coefficients were stored by the last
+    // sweep's pass A (the same sequential fma chains as k_score's sampling, so
+    // the fused and stand-alone scores agree bit for bit); psi is sampled here
     auto sample = [&](int k, double& x, double& y, double& xd, double& yd, double& ps) {
-      x = y = xd = yd = ps = 0.0;
-      for (int i = 0; i < NB; ++i) {
-        const double p = sP[i * npad + k], pd = sPd[i * npad + k];
-        const double2 c = cxy2[i];
-        x = __fma_rn(p, c.x, x);
-        y = __fma_rn(p, c.y, y);
-        xd = __fma_rn(pd, c.x, xd);
-        yd = __fma_rn(pd, c.y, yd);
-        ps = __fma_rn(p, ws.cp[i], ps);
+      xd = ws.xd[k];
+      yd = ws.yd[k];
+      ps = 0.0;
+      if constexpr (kStoreXY) {
+        x = ws.x[k];
+        y = ws.y[k];
+#pragma unroll
+        for (int i = 0; i < NB; ++i) ps = __fma_rn(sP[i * npad + k], ws.cp[i], ps);
+      } else {
+        x = y = 0.0;
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+          const double p = sP[i * npad + k];
+          const double2 c = cxy2[i];
+          x = __fma_rn(p, c.x, x);
+          y = __fma_rn(p, c.y, y);
+          ps = __fma_rn(p, ws.cp[i], ps);
+        }
       }
     };
     double cost, rmin, hmax;

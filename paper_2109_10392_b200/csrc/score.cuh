@@ -38,12 +38,14 @@ __device__ __forceinline__ void score_instance(const ScoreParams& S, const doubl
     const double ah = fabs(ps);
     if (ah != ah) any_nan = true;
     hmax = fmax(hmax, ah);
+    // ratio^2 (a b)^2 = (b (x - qx))^2 + (a (y - qy))^2: no division per term
+    // (the sweep's outside test); the one division and square root come after
+    // the minimum
+#pragma unroll 4
     for (int j = 0; j < S.m; ++j) {
       const double2 q = __ldg(xi + j * S.n + k);
-      const double wx = __ddiv_rn(__dsub_rn(x, q.x), S.a), wy = __ddiv_rn(__dsub_rn(y, q.y), S.b);
-      // the squared ratio: the correctly rounded sqrt is monotone, so the
-      // square root of the minimum is the minimum of the square roots
-      rmin = fmin(rmin, __dadd_rn(__dmul_rn(wx, wx), __dmul_rn(wy, wy)));
+      const double px = __dmul_rn(S.b, __dsub_rn(x, q.x)), py = __dmul_rn(S.a, __dsub_rn(y, q.y));
+      rmin = fmin(rmin, __fma_rn(px, px, __dmul_rn(py, py)));
     }
     if (S.kind == 0) {
       const double dv = __dsub_rn(v, S.v_cruise);
@@ -55,7 +57,7 @@ __device__ __forceinline__ void score_instance(const ScoreParams& S, const doubl
     }
   }
   hmax = warp_max(hmax);
-  rmin = __dsqrt_rn(warp_min(rmin));
+  rmin = __ddiv_rn(__dsqrt_rn(warp_min(rmin)), __dmul_rn(S.a, S.b));
   cost = warp_sum(cost);
   if (__any_sync(BMPC_FULL, any_nan)) hmax = NAN;  // np.abs(psi).max() propagates NaN
   const double rmax = (r0 != r0 || r1 != r1 || r2 != r2) ? NAN : fmax(r0, fmax(r1, r2));

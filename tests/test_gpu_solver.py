@@ -406,3 +406,31 @@ def test_team_validation(cuda):
         solver.solve_device(prob, max_iter=3, tol=0.0, team_warps=4)
     with pytest.raises(ValueError, match="team_warps"):
         solver.solve_device(prob, max_iter=3, tol=0.0, team_warps=3)
+
+
+def test_null_space_qp_info_and_refinement(cuda, monkeypatch):
+    """The persistent solve's null-space QP (capi.cu reduced_qp): well-conditioned
+    shapes skip the refinement step, ill-conditioned ones (c4) keep it, and
+    forcing the refinement on a well-conditioned shape changes the trajectories
+    by no more than rounding."""
+    from paper_2109_10392_b200 import make_solver
+
+    info = make_solver(100, 5.0, 10, 10).qp_info()
+    assert not info["refine_xy"] and not info["refine_psi"]
+    assert 1.0 < info["cond_xy"] < 1e4 and 1.0 < info["cond_psi"] < 1e4
+    info4 = make_solver(200, 10.0, 15, 50).qp_info()
+    assert info4["refine_xy"] and info4["cond_xy"] > 1e4
+
+    z = golden("c1")
+    solver, res = _plan(z)
+    monkeypatch.setenv("BMPC_QP_REFINE", "3")
+    forced = _solver(z)
+    assert forced.qp_info()["refine_xy"] and forced.qp_info()["refine_psi"]
+    from paper_2109_10392_b200.planner import FilterLimits, MetaCostSpec, plan_batch
+
+    res2 = plan_batch(forced, _Scenes(z), max_iter=int(z["iters"]), tol=0.0,
+                      spec=MetaCostSpec("cruise", v_cruise=20.0), limits=FilterLimits())
+    err = traj_err(solver.basis.P, {"c_x": res2.c_x, "c_y": res2.c_y, "c_psi": res2.c_psi},
+                   {"c_x": res.c_x, "c_y": res.c_y, "c_psi": res.c_psi})
+    assert err.max() <= 1e-11, err.max()
+    assert res.best_index == res2.best_index
