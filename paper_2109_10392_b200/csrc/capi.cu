@@ -722,6 +722,38 @@ int bmpc_sample(bmpc_ctx* ctx, int L, const double* c_x, const double* c_y, cons
   return BMPC_OK;
 }
 
+// Results block of bmpc_plan_host (arena order): coefficients (c_x, c_y,
+// c_psi), res_final, then with scoring meta_cost, min_ratio, heading_max, the
+// four per-scene index rows, flags, and the {iterations, converged} status.
+struct ResultsLayout {
+  size_t coef, rf, meta, mr, hm, best, fl, stat, bytes;
+};
+static ResultsLayout results_layout(int nb, size_t L, size_t S, bool score) {
+  ResultsLayout r;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { const size_t at = off; off += (bytes + 15) & ~(size_t)15; return at; };
+  r.coef = take(3 * nb * L * 8);
+  r.rf = take(3 * L * 8);
+  r.meta = take(score ? L * 8 : 0);
+  r.mr = take(score ? L * 8 : 0);
+  r.hm = take(score ? L * 8 : 0);
+  r.best = take(score ? 4 * S * 8 : 0);
+  r.fl = take(score ? L : 0);
+  r.stat = take(2 * sizeof(int));
+  r.bytes = off;
+  return r;
+}
+
+int bmpc_plan_host_layout(const bmpc_ctx* ctx, int S, int l, int score, long long* out, int n) {
+  if (!ctx || S < 1 || l < 0) return fail(BMPC_EINVAL, "bmpc_plan_host_layout: bad arguments");
+  const ResultsLayout r = results_layout(ctx->C.nb, (size_t)S * l, (size_t)S, score != 0);
+  const long long v[] = {(long long)r.coef, (long long)r.rf,   (long long)r.meta,
+                         (long long)r.mr,   (long long)r.hm,   (long long)r.best,
+                         (long long)r.fl,   (long long)r.stat, (long long)r.bytes};
+  for (int i = 0; i < n && i < 9; ++i) out[i] = v[i];
+  return BMPC_OK;
+}
+
 int bmpc_plan_host(bmpc_ctx* ctx, const bmpc_problem* hp, const bmpc_solve_opts* o,
                    bmpc_solve_out* ho, const bmpc_score_spec* spec, bmpc_score_out* hs,
                    void* stream) {
@@ -744,11 +776,35 @@ int bmpc_plan_host(bmpc_ctx* ctx, const bmpc_problem* hp, const bmpc_solve_opts*
                o_lam = take(3 * nb * L * 8),
                o_v = take(o->want_v && ho->v ? n * L * 8 : 0);
   const size_t o_res0 = off;  // results block
-  const size_t o_coef = take(3 * nb * L * 8), o_rf = take(3 * L * 8);
-  const size_t o_meta = take(score ? L * 8 : 0), o_mr = take(score ? L * 8 : 0),
-               o_hm = take(score ? L * 8 : 0), o_best = take(score ? 4 * S * 8 : 0),
-               o_fl = take(score ? L : 0), o_stat = take(2 * sizeof(int));
-  const size_t res_bytes = off - o_res0;
+  const ResultsLayout R = results_layout(nb, L, S, score);
+  off += R.bytes;
+  const size_t o_coef = o_res0 + R.coef, o_rf = o_res0 + R.rf, o_meta = o_res0 + R.meta,
+               o_mr = o_res0 + R.mr, o_hm = o_res0 + R.hm, o_best = o_res0 + R.best,
+               o_fl = o_res0 + R.fl, o_stat = o_res0 + R.stat;
+  const size_t res_bytes = R.bytes;
+  // Zero-copy return: when the caller's outputs already sit in one pinned
+  // block laid out like the results block (bmpc_plan_host_layout), the block
+  // comes back with one copy straight into place -- no staging buffer, no
+  // host memcpy.
+  char* direct = nullptr;
+  if (ho->c_x) {
+    char* base = (char*)ho->c_x - R.coef;
+    bool ok = (char*)ho->c_y == base + R.coef + nb * L * 8 &&
+              (char*)ho->c_psi == base + R.coef + 2 * nb * L * 8 && (char*)ho->res_final == base + R.rf;
+    if (ok && score)
+      ok = (char*)hs->meta_cost == base + R.meta && (char*)hs->min_ratio == base + R.mr &&
+           (char*)hs->heading_max == base + R.hm && (char*)hs->flags == base + R.fl &&
+           (char*)hs->best_index == base + R.best && (char*)hs->argmin_all == base + R.best + S * 8 &&
+           (char*)hs->argmin_hc == base + R.best + 2 * S * 8 &&
+           (char*)hs->n_feasible == base + R.best + 3 * S * 8;
+    if (ok) {
+      cudaPointerAttributes at;
+      if (cudaPointerGetAttributes(&at, base) == cudaSuccess && at.type == cudaMemoryTypeHost)
+        direct = base;
+      else
+        cudaGetLastError();  // clear a sticky "invalid value" from pageable memory
+    }
+  }
   DevBuf B(st);
   char* arena = B.alloc<char>(off);
   if (!arena) return fail(BMPC_ECUDA, "device allocation failed");
@@ -809,6 +865,14 @@ int bmpc_plan_host(bmpc_ctx* ctx, const bmpc_problem* hp, const bmpc_solve_opts*
   };
   for (const Cp& c : extra)
     if (c.h && c.d && c.bytes) CK(cudaMemcpyAsync(c.h, c.d, c.bytes, cudaMemcpyDeviceToHost, st), "d2h");
+  if (direct) {
+    CK(cudaMemcpyAsync(direct, arena + o_res0, res_bytes, cudaMemcpyDeviceToHost, st), "d2h");
+    CK(cudaStreamSynchronize(st), "sync");
+    const int* stat = (const int*)(direct + R.stat);
+    ho->iterations = stat[0];
+    ho->converged = stat[1];
+    return BMPC_OK;
+  }
   // the results block in one copy through the pinned staging buffer
   std::lock_guard<std::mutex> lk(ctx->stage_mu);
   if (ctx->stage_bytes < res_bytes) {

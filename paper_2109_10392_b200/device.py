@@ -14,18 +14,26 @@ import numpy as np
 from . import _native as nat
 
 
+_CUDA_OK = False
+
+
 def _torch():
+    global _CUDA_OK
     import torch
 
-    if not torch.cuda.is_available():
-        raise RuntimeError("paper_2109_10392_b200 needs a CUDA device (sm_100a); no CPU fallback")
+    if not _CUDA_OK:
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2109_10392_b200 needs a CUDA device (sm_100a); no CPU fallback")
+        _CUDA_OK = True
     return torch
 
 
 def stream_ptr(stream=None) -> int:
     torch = _torch()
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return s.cuda_stream
+    if stream is not None:
+        return stream.cuda_stream
+    # torch's current stream on the current device, without building a Stream object
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
 
 
 def ptr(t) -> int | None:

@@ -513,6 +513,30 @@ class PlanResult:
         return self.flags == 7
 
 
+_LAYOUT_CACHE: dict = {}
+
+
+def _results_block(solver: BatchSolver, ctx, S: int, l: int) -> dict:
+    """Fresh numpy views (caller-owned) into one pinned host block with the
+    offsets of bmpc_plan_host_layout."""
+    import torch
+
+    key = (ctx.value, S, l)
+    lay = _LAYOUT_CACHE.get(key)
+    if lay is None:
+        o = (ctypes.c_longlong * 9)()
+        nat.check(nat.load().bmpc_plan_host_layout(ctx, S, l, 1, o, 9), "bmpc_plan_host_layout")
+        nb, L = solver.basis.n_b, S * l
+        f8, i8, u1 = np.float64, np.int64, np.uint8
+        lay = (int(o[8]), [("coef", o[0], 3 * nb * L, f8), ("rf", o[1], 3 * L, f8),
+                           ("meta", o[2], L, f8), ("mr", o[3], L, f8), ("hm", o[4], L, f8),
+                           ("best", o[5], 4 * S, i8), ("fl", o[6], L, u1)])
+        _LAYOUT_CACHE[key] = lay
+    total, fields = lay
+    raw = torch.empty(total, dtype=torch.uint8, pin_memory=True).numpy()
+    return {name: raw[off:off + cnt * np.dtype(dt).itemsize].view(dt) for name, off, cnt, dt in fields}
+
+
 def plan_batch(solver: BatchSolver, scenes, max_iter: int = 100, tol: float = 0.0,
                spec: MetaCostSpec | None = None, limits: FilterLimits | None = None,
                stream=None, precision: str = "fp64") -> PlanResult:
@@ -542,13 +566,17 @@ def plan_batch(solver: BatchSolver, scenes, max_iter: int = 100, tol: float = 0.
                        b_xy.ctypes.data, b_psi.ctypes.data, scenes.a, scenes.b, scenes.v_min,
                        scenes.v_max, scenes.a_max)
     opts = nat.SolveOpts(max_iter=int(max_iter), tol=float(tol), precision=_precision_code(precision))
-    coef = np.empty((3, nb, L))
-    res = np.empty((3, L))
+    # every output is a view of one page-locked block laid out like the
+    # device results block, so they come back with one copy straight into
+    # place; the block returns to torch's pinned caching allocator when the
+    # last view is dropped
+    blk = _results_block(solver, ctx, S, l)
+    coef = blk["coef"].reshape(3, nb, L)
+    res = blk["rf"].reshape(3, L)
     out = nat.SolveOut(coef[0].ctypes.data, coef[1].ctypes.data, coef[2].ctypes.data, None, None,
                        None, None, None, res.ctypes.data, 0, 0)
-    meta, mr, hm = np.empty((3, L))
-    flags = np.empty(L, dtype=np.uint8)
-    best, amin, ahc, nf = np.empty((4, S), dtype=np.int64)
+    meta, mr, hm, flags = blk["meta"], blk["mr"], blk["hm"], blk["fl"]
+    best, amin, ahc, nf = blk["best"].reshape(4, S)
     so = nat.ScoreOut(meta.ctypes.data, mr.ctypes.data, hm.ctypes.data, flags.ctypes.data,
                       best.ctypes.data, amin.ctypes.data, ahc.ctypes.data, nf.ctypes.data)
     nat.check(nat.load().bmpc_plan_host(ctx, ctypes.byref(prob), ctypes.byref(opts), ctypes.byref(out),

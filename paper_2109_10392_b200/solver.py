@@ -234,11 +234,11 @@ class BatchSolver:
     def _context(self):
         import torch
 
+        if self._ctx is not None and self._ctx_device == torch._C._cuda_getDevice():
+            return self._ctx
         if not torch.cuda.is_available():
             raise RuntimeError("BatchSolver needs a CUDA device (sm_100a); there is no CPU fallback")
         dev = torch.cuda.current_device()
-        if self._ctx is not None and self._ctx_device == dev:
-            return self._ctx
         lib = nat.load()
         c = ctypes.c_void_p()
         b = self.basis

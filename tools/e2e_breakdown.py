@@ -91,3 +91,21 @@ t_host = timeit(lambda: nat.check(lib.bmpc_plan_host(ctx, ctypes.byref(prob_h), 
 t_empty = timeit(lambda: torch.cuda.synchronize(), args.reps)
 print(f"{args.config}: bmpc_plan_host (ctypes, structs prebuilt) {t_host:.3f} ms | "
       f"python plan_batch overhead {t_plan - t_host:.3f} ms | bare sync {t_empty:.3f} ms")
+
+
+def host_fresh():
+    coef = np.empty((3, solver.basis.n_b, W.L))
+    res = np.empty((3, W.L))
+    o = nat.SolveOut(coef[0].ctypes.data, coef[1].ctypes.data, coef[2].ctypes.data, None, None,
+                     None, None, None, res.ctypes.data, 0, 0)
+    meta, mr, hm = np.empty((3, W.L))
+    flags = np.empty(W.L, dtype=np.uint8)
+    best, amin, ahc, nf = np.empty((4, W.S), dtype=np.int64)
+    s = nat.ScoreOut(meta.ctypes.data, mr.ctypes.data, hm.ctypes.data, flags.ctypes.data,
+                     best.ctypes.data, amin.ctypes.data, ahc.ctypes.data, nf.ctypes.data)
+    nat.check(lib.bmpc_plan_host(ctx, ctypes.byref(prob_h), ctypes.byref(opts), ctypes.byref(o),
+                                 ctypes.byref(sspec), ctypes.byref(s), sp))
+
+
+t_fresh = timeit(host_fresh, args.reps)
+print(f"{args.config}: bmpc_plan_host with fresh numpy outputs {t_fresh:.3f} ms")
