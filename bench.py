@@ -128,8 +128,21 @@ def make_step_workload(cfg_name: str, world: int, rank: int):
 
 
 # ------------------------------------------------------------ CPU oracle ----
+def _oracle_kind() -> str:
+    """"ref": the reference's own compiled Cython kernels (oracle/_ref, built from
+    /root/reference by build() and shipped with the tree) under the oracle's
+    restatement of solver.py; "c": the oracle's C restatement of those kernels."""
+    return "ref" if any((ROOT / "oracle" / "_ref").glob("_speedups*.so")) else "c"
+
+
+def _cpu_sample_text(kind: str) -> str:
+    return ("oracle/am_oracle.py (solver.py restated op for op in numpy) + the reference's compiled "
+            "Cython kernels (oracle/_ref)" if kind == "ref" else "oracle/am_oracle.py + am_oracle.c")
+
+
 def _cpu_worker(args):
-    cfg_name, l_lo, l_hi, iters, world_l = args
+    cfg_name, l_lo, l_hi, iters, world_l = args[:5]
+    kind = args[5] if len(args) > 5 else "c"
     from threadpoolctl import threadpool_limits
 
     sys.path.insert(0, str(ROOT / "oracle"))
@@ -143,23 +156,24 @@ def _cpu_worker(args):
         o = O.OracleSolver(cfg.n, cfg.t_f, cfg.degree, cfg.m)
         t = time.perf_counter()
         r = o.solve(W.xi_x[0], W.xi_y[0], W.b_xy[:, l_lo:l_hi], W.b_psi[:, l_lo:l_hi], W.a, W.b,
-                    W.v_min, W.v_max, W.a_max, iters, kernel="c")
+                    W.v_min, W.v_max, W.a_max, iters, kernel=kind)
         sc = o.score(r, W.xi_x[0], W.xi_y[0], W.a, W.b, kind="cruise", v_cruise=20.0)
         return time.perf_counter() - t, l_hi - l_lo, sc["best_index"]
 
 
-def cpu_oracle_rate(cfg_name: str, goals: int, iters: int, procs: int, reps: int = 1):
-    """Aggregate problems/s of the oracle port: `procs` processes, 1 BLAS thread each,
-    disjoint goal blocks of one scene (SURVEY.md 8d CPU-baseline recipe)."""
+def cpu_oracle_rate(cfg_name: str, goals: int, iters: int, procs: int, reps: int = 3,
+                    kind: str = "c"):
+    """Aggregate problems/s of the CPU path: `procs` processes, 1 BLAS thread each,
+    disjoint goal blocks of one scene, best of `reps` (SURVEY.md 8d CPU-baseline recipe)."""
     import multiprocessing as mp
 
     per = int(math.ceil(goals / procs))
-    jobs = [(cfg_name, i * per, min(goals, (i + 1) * per), iters, goals) for i in range(procs)
+    jobs = [(cfg_name, i * per, min(goals, (i + 1) * per), iters, goals, kind) for i in range(procs)
             if i * per < goals]
     ctx = mp.get_context("spawn")
     best = None
     with ctx.Pool(len(jobs)) as pool:
-        pool.map(_cpu_worker, [(cfg_name, 0, 1, 1, goals)] * len(jobs))  # warm-up imports
+        pool.map(_cpu_worker, [(cfg_name, 0, 1, 1, goals, kind)] * len(jobs))  # warm-up imports
         for _ in range(reps):
             t0 = time.perf_counter()
             pool.map(_cpu_worker, jobs)
@@ -311,11 +325,13 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         procs = os.cpu_count() or 1
         goals = min(cfg.l, 1024)  # bounded sample: scene 0, at most 1024 goals of this config
-        rate, secs, used = cpu_oracle_rate(args.config, goals, iters, procs)
-        cpu = {"value": rate, "unit": "problems/s", "cores": used, "kind": "port",
+        kind = _oracle_kind()
+        rate, secs, used = cpu_oracle_rate(args.config, goals, iters, procs, kind=kind)
+        cpu = {"value": rate, "unit": "problems/s", "cores": used,
+               "kind": "reference" if kind == "ref" else "port",
                "sample": f"{args.config} scene 0, {goals} goals x {iters} sweeps + scoring, split "
-                         f"over {used} processes (1 BLAS thread each), {secs:.2f}s wall; "
-                         f"oracle/am_oracle.py + am_oracle.c"}
+                         f"over {used} processes (1 BLAS thread each), best of 3, {secs:.2f}s wall; "
+                         + _cpu_sample_text(kind)}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "problems/s", "n_gpus": world,
@@ -378,10 +394,11 @@ def run_reference(args, rank, world):
 
     per = int(math.ceil(goals / procs))
     cfg_name = args.config
-    jobs = [(cfg_name, i * per, min(goals, (i + 1) * per), iters, goals) for i in range(procs)
+    kind = _oracle_kind()
+    jobs = [(cfg_name, i * per, min(goals, (i + 1) * per), iters, goals, kind) for i in range(procs)
             if i * per < goals]
     with mp.get_context("spawn").Pool(len(jobs)) as pool:
-        pool.map(_cpu_worker, [(cfg_name, 0, 1, 1, goals)] * len(jobs))
+        pool.map(_cpu_worker, [(cfg_name, 0, 1, 1, goals, kind)] * len(jobs))
         for _ in range(args.warmup):
             pool.map(_cpu_worker, jobs)
         for _ in range(args.steps):
@@ -396,9 +413,11 @@ def run_reference(args, rank, world):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.config, "problems_per_step": goals, "iters": iters,
                    "tol": 0.0},
-        "cpu_baseline": {"value": value, "unit": "problems/s", "cores": len(jobs), "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "problems/s", "cores": len(jobs),
+                         "kind": "reference" if kind == "ref" else "port",
                          "sample": f"{cfg_name} scene 0, {goals} goals x {iters} sweeps + scoring per "
-                                   f"step over {len(jobs)} processes (1 BLAS thread each)"},
+                                   f"step over {len(jobs)} processes (1 BLAS thread each); "
+                                   + _cpu_sample_text(kind)},
         "e2e": {"value": value, "unit": "problems/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))

@@ -63,6 +63,7 @@ typedef struct {
   int hist_offset;      // first history row written by this launch
   double a, b, v_min, v_max, a_max;
   const double* xi;     // [S][m][n] interleaved (xi_x, xi_y) pairs
+  const double* xis;    // the same pairs in the ellipse frame: (b xi_x, a xi_y)
   const double* b_xy;   // [12][L]
   const double* b_psi;  // [4][L]
   // warm start (BMPC_INIT_WARM), reference AmState layouts (rows, L)

@@ -220,23 +220,29 @@ __device__ __forceinline__ bool obstacle_inside(double x, double y, double2 q, d
   const double px = b * (x - q.x), py = a * (y - q.y);
   return !(fma(px, px, py * py) >= ab2);
 }
-// Inside term of the sweep's obstacle block: residual r_j = w - (a cos, b sin)
-// (g_j - x = -r_j), accumulated with its square.
-__device__ __forceinline__ void obstacle_inside_res(double x, double y, double2 q, double a,
-                                                    double b, double& srx, double& sry,
-                                                    double& sq, double& cin) {
-  const double wx = x - q.x, wy = y - q.y;
-  const double px = b * wx, py = a * wy;
+// The sweep's form: position and prediction already in the ellipse frame
+// (xs = b x, ys = a y; qs = (b qx, a qy), packed once per solve), so a term
+// costs two subtractions, a multiply and an fma.  The rounding differs from
+// b (x - qx) only in the last bits, which moves the d = 1 boundary by
+// rounding, as the reference's own r / (a b) does.
+__device__ __forceinline__ bool obstacle_inside_s(double xs, double ys, double2 qs, double ab2) {
+  const double px = xs - qs.x, py = ys - qs.y;
+  return !(fma(px, px, py * py) >= ab2);
+}
+// Inside term in the ellipse frame: w = (px / b, py / a), r_j = w - (a cos, b sin).
+__device__ __forceinline__ void obstacle_inside_res_s(double xs, double ys, double2 qs, double a,
+                                                      double b, double ia, double ib, double& srx,
+                                                      double& sry, double& sq, double& cin) {
+  const double px = xs - qs.x, py = ys - qs.y;
   const double r2 = fma(px, px, py * py);
   const double ri = rsqrt_nb(r2);
   const double ca = r2 > 0.0 ? px * ri : 1.0, sa = py * ri;  // r = 0 -> (1, 0)
-  const double rx = wx - a * ca, ry = wy - b * sa;
+  const double rx = fma(px, ib, -a * ca), ry = fma(py, ia, -b * sa);
   sq = fma(rx, rx, fma(ry, ry, sq));
   srx += rx;
   sry += ry;
   cin += 1.0;
 }
-
 __device__ __forceinline__ void obstacle_inside_term(double x, double y, double2 q, double a,
                                                      double b, double& gix, double& giy,
                                                      double& sq, double& cin) {
@@ -261,21 +267,22 @@ constexpr bool kPairSlots = NB <= 12;
 struct TailArgs {
   const double* P;
   const double2* cxy;
-  const double2* xi;
+  const double2* xi;  // predictions in the ellipse frame (b qx, a qy)
   const double *xs, *ys;  // sampled positions (pass A) or nullptr: recompute from c
   int n, m;
   double a, b;
+  double ia, ib;  // 1 / a, 1 / b
 };
 
 // fp32 mode inside term (the outside test runs in fp64 in both modes): with
 // d = 1 the residual is r = w - (a cos, b sin) and g = x - r, evaluated in fp32
 // from w rounded off the fp64 difference, so far and virtual obstacles (+1e4 m)
 // never see |w| rounded in fp32.
-__device__ __forceinline__ void obstacle_term_f32(double x, double y, double2 q, float a, float b,
-                                                  float ab2, float& srx, float& sry, float& sq,
-                                                  double& cin) {
+__device__ __forceinline__ void obstacle_term_f32(double xs, double ys, double2 qs, float a, float b,
+                                                  float ab2, double ia, double ib, float& srx,
+                                                  float& sry, float& sq, double& cin) {
   cin += 1.0;
-  const float wx = (float)(x - q.x), wy = (float)(y - q.y);
+  const float wx = (float)((xs - qs.x) * ib), wy = (float)((ys - qs.y) * ia);
   const float px = b * wx, py = a * wy;
   const float r2 = fmaf(px, px, py * py);
   const float ri = rsqrtf(r2);
@@ -324,6 +331,13 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
         }
       }
     }
+    // into the ellipse frame
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      x[s] *= T.b;
+      y[s] *= T.a;
+    }
+    const double ia = T.ia, ib = T.ib;
     BMPC_PROF_NS(10);
     const int qstep = js * T.n;
 #ifndef BMPC_UPAIR
@@ -368,7 +382,7 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
         for (int u = 0; u < U; ++u)
 #pragma unroll
           for (int s = 0; s < NS; ++s) {
-            in[s][u] = obstacle_inside(x[s], y[s], q[s][u], T.a, T.b, abd2);
+            in[s][u] = obstacle_inside_s(x[s], y[s], q[s][u], abd2);
             any |= in[s][u];
           }
         if (any) {
@@ -378,9 +392,11 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
             for (int s = 0; s < NS; ++s)
               if (in[s][u]) {
                 if constexpr (F32)
-                  obstacle_term_f32(x[s], y[s], q[s][u], af, bf, ab2, srx[s], sry[s], sqf[s], cin[s]);
+                  obstacle_term_f32(x[s], y[s], q[s][u], af, bf, ab2, ia, ib, srx[s], sry[s], sqf[s],
+                                    cin[s]);
                 else
-                  obstacle_inside_res(x[s], y[s], q[s][u], T.a, T.b, gsx[s], gsy[s], sq[s], cin[s]);
+                  obstacle_inside_res_s(x[s], y[s], q[s][u], T.a, T.b, ia, ib, gsx[s], gsy[s], sq[s],
+                                        cin[s]);
               }
         }
       }
@@ -391,11 +407,11 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
         const double2 q = __ldg(qp[s]);
-        if (obstacle_inside(x[s], y[s], q, T.a, T.b, abd2)) {
+        if (obstacle_inside_s(x[s], y[s], q, abd2)) {
           if constexpr (F32)
-            obstacle_term_f32(x[s], y[s], q, af, bf, ab2, srx[s], sry[s], sqf[s], cin[s]);
+            obstacle_term_f32(x[s], y[s], q, af, bf, ab2, ia, ib, srx[s], sry[s], sqf[s], cin[s]);
           else
-            obstacle_inside_res(x[s], y[s], q, T.a, T.b, gsx[s], gsy[s], sq[s], cin[s]);
+            obstacle_inside_res_s(x[s], y[s], q, T.a, T.b, ia, ib, gsx[s], gsy[s], sq[s], cin[s]);
         }
         qp[s] += qstep;
       }
@@ -552,8 +568,11 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
   const double* __restrict__ sPdd = sPT + 2 * NB * npad;
   const double2* __restrict__ xi =
       reinterpret_cast<const double2*>(A.xi) + (size_t)(inst / A.l) * A.m * n;
+  const double2* __restrict__ xis =
+      reinterpret_cast<const double2*>(A.xis) + (size_t)(inst / A.l) * A.m * n;
   const int m = A.m;
   const double a = A.a, b = A.b, rho = C.rho;
+  const double inv_a = 1.0 / a, inv_b = 1.0 / b;
 
   const int li = lane & 15;
   const bool yax = lane >= 16;
@@ -922,7 +941,8 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
     //     slot(): full slots two at a time, the n % 32 leftover samples split
     //     over lane groups.
     {
-      TailArgs T{sP, cxy, xi, kStoreXY ? ws.x : nullptr, kStoreXY ? ws.y : nullptr, n, m, a, b};
+      TailArgs T{sP, cxy, xis, kStoreXY ? ws.x : nullptr, kStoreXY ? ws.y : nullptr, n, m, a, b,
+                 inv_a, inv_b};
       int r = wt;  // this warp's slots r = wt, wt + TW, ...
       if (kPairSlots<NB>) {
 #pragma unroll 1

@@ -51,7 +51,7 @@ cudaError_t op_score(const ScoreArgs& S, cudaStream_t st);
 cudaError_t op_argmin(int S, int l, const double* meta, const uint8_t* flags, long long* best,
                       long long* best_all, long long* best_hc, long long* nfeas, cudaStream_t st);
 cudaError_t op_pack_xi(long long total, const double* xi_x, const double* xi_y, double* out,
-                       cudaStream_t st);
+                       cudaStream_t st, double* scaled = nullptr, double a = 1.0, double b = 1.0);
 cudaError_t op_first_clear(int iters, const int* notconv, int* tstar, cudaStream_t st);
 cudaError_t op_assemble(int S, int V, int m, int n, int l, const double* veh, const int* nveh,
                         const double* ego, const double* goals, const double* rel, double* xi_x,
@@ -438,6 +438,7 @@ static int launch_sweeps(bmpc_ctx* ctx, const bmpc_problem* p, const double* xi2
   A.v_max = p->v_max;
   A.a_max = p->a_max;
   A.xi = xi2;
+  A.xis = xi2 ? xi2 + 2 * (size_t)p->S * p->m * ctx->C.n : nullptr;
   A.b_xy = p->b_xy;
   A.b_psi = p->b_psi;
   A.w_alpha = o->w_alpha;
@@ -501,8 +502,9 @@ int bmpc_sweeps(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opts* o, 
   const long long tot = (long long)p->S * p->m * ctx->C.n;
   double* xi2 = nullptr;
   if (tot > 0) {
-    CK(cudaMallocAsync(&xi2, tot * 2 * sizeof(double), st), "cudaMallocAsync");
-    CK(bmpc::op_pack_xi(tot, p->xi_x, p->xi_y, xi2, st), "pack_xi");
+    // raw pairs, then the ellipse-frame pairs for the sweeps' outside test
+    CK(cudaMallocAsync(&xi2, tot * 4 * sizeof(double), st), "cudaMallocAsync");
+    CK(bmpc::op_pack_xi(tot, p->xi_x, p->xi_y, xi2, st, xi2 + 2 * tot, p->a, p->b), "pack_xi");
   }
   const int mode = resume ? BMPC_INIT_RESUME : (is_warm(o) ? BMPC_INIT_WARM : BMPC_INIT_COLD);
   rc = launch_sweeps(ctx, p, xi2, o, iters, mode, hist_offset, carry, write_carry, out, st);
@@ -594,8 +596,9 @@ static int solve_impl(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opt
   // per sweep, [max_iter + 1] re-run sweep count, [max_iter + 2, + 3] status
   int* scr = nullptr;
   if (tot > 0) {
-    CK(cudaMallocAsync(&xi2, tot * 2 * sizeof(double), st), "cudaMallocAsync");
-    CK(bmpc::op_pack_xi(tot, p->xi_x, p->xi_y, xi2, st), "pack_xi");
+    // raw pairs, then the ellipse-frame pairs for the sweeps' outside test
+    CK(cudaMallocAsync(&xi2, tot * 4 * sizeof(double), st), "cudaMallocAsync");
+    CK(bmpc::op_pack_xi(tot, p->xi_x, p->xi_y, xi2, st, xi2 + 2 * tot, p->a, p->b), "pack_xi");
   }
   const int mode = is_warm(o) ? BMPC_INIT_WARM : BMPC_INIT_COLD;
   const int M = o->max_iter;

@@ -375,10 +375,16 @@ __global__ void k_argmin(int l, const double* __restrict__ meta, const uint8_t* 
 }
 
 // ------------------------------------------------------------------- misc --
+// (xi_x, xi_y) pairs, and optionally the pairs scaled to the ellipse frame
+// (b xi_x, a xi_y) that the sweep's outside test reads.
 __global__ void k_pack_xi(long long total, const double* __restrict__ xi_x,
-                          const double* __restrict__ xi_y, double2* __restrict__ out) {
+                          const double* __restrict__ xi_y, double2* __restrict__ out,
+                          double2* __restrict__ scaled, double a, double b) {
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e < total) out[e] = make_double2(xi_x[e], xi_y[e]);
+  if (e >= total) return;
+  const double x = xi_x[e], y = xi_y[e];
+  out[e] = make_double2(x, y);
+  if (scaled) scaled[e] = make_double2(b * x, a * y);
 }
 
 // First iteration t whose worst residual over all instances is <= tol
@@ -473,9 +479,10 @@ cudaError_t op_argmin(int S, int l, const double* meta, const uint8_t* flags, lo
   return cudaGetLastError();
 }
 cudaError_t op_pack_xi(long long total, const double* xi_x, const double* xi_y, double* out,
-                       cudaStream_t st) {
+                       cudaStream_t st, double* scaled, double a, double b) {
   if (total > 0)
-    k_pack_xi<<<nblk(total), kTB, 0, st>>>(total, xi_x, xi_y, reinterpret_cast<double2*>(out));
+    k_pack_xi<<<nblk(total), kTB, 0, st>>>(total, xi_x, xi_y, reinterpret_cast<double2*>(out),
+                                           reinterpret_cast<double2*>(scaled), a, b);
   return cudaGetLastError();
 }
 // Device-side early-stop decision: the re-run sweep count (0 = none) and the
