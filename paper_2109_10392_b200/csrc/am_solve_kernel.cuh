@@ -1120,14 +1120,19 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
       lam -= rho * ((a3[0] + a3[1]) - rest);
     }
     if (!yax && owner) lamp -= rho * Lp;
-    const double res = sqrt(lane == 16 ? sqo : (lane == 17 ? sqa : sqn));  // lanes 16..18
+    const double sqv = lane == 16 ? sqo : (lane == 17 ? sqa : sqn);  // lanes 16..18
     if (A.notconv && wt == 0) {  // global early stop: flag this sweep unless every residual <= tol
-      const bool nc = __any_sync(BMPC_FULL, lane >= 16 && lane < 19 && !(res <= A.tol));
+      // res = sqrt(sqv) <= tol; for tol = 0 (the fixed-sweep benchmarks) that is
+      // exactly sqv <= 0 (sqrt is exact at +-0 and keeps NaN), so the square
+      // root stays off the sweep's critical path
+      const bool ok = A.tol > 0.0 ? sqrt(sqv) <= A.tol : (A.tol == 0.0 && sqv <= 0.0);
+      const bool nc = __any_sync(BMPC_FULL, lane >= 16 && lane < 19 && !ok);
       // a plain store: the flag only ever goes 0 -> 1, and a read-before-write
       // would stall the warp on a coherent L2 round trip every sweep
       if (lane == 0 && nc) A.notconv[A.hist_offset + t] = 1;
     }
-    if (lane >= 16 && lane < 19 && wt == 0) {
+    if (lane >= 16 && lane < 19 && wt == 0 && ((A.flags & BMPC_F_HISTORY) || last)) {
+      const double res = sqrt(sqv);
       if (A.flags & BMPC_F_HISTORY)
         A.hist[((size_t)(A.hist_offset + t) * 3 + (lane - 16)) * L + inst] = res;
       if (last && A.res_final) A.res_final[(size_t)(lane - 16) * L + inst] = res;
