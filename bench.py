@@ -221,9 +221,9 @@ def run_ours(args, rank, world, local_rank):
     status_dev = torch.zeros(2, dtype=torch.int32, device=dev)
     opts_async = nat.SolveOpts(max_iter=iters, tol=0.0, precision=prec, status_dev=status_dev.data_ptr())
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    # pack_xi, am_solve (+ fused scoring), first_clear, rerun_plan, am_solve (early-stop
-    # re-run: exits at once when there is none), argmin
-    launches_per_step = 6
+    # pack_xi, am_solve (+ fused scoring), early_stop, am_solve (early-stop re-run:
+    # exits at once when there is none), argmin
+    launches_per_step = 5
 
     def step():
         # the residual history is not requested (plan_batch does not return it)

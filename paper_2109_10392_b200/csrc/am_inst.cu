@@ -1,5 +1,7 @@
 // am_inst.cu -- one n_b instantiation of the persistent AM kernel (compiled
 // once per n_b with -DBMPC_INST_NB=<n_b> so the builds run in parallel).
+#include <atomic>
+
 #include "am_solve_kernel.cuh"
 
 namespace bmpc {
@@ -11,8 +13,19 @@ static cudaError_t launch_t(const bmpc_dev_consts& C, const bmpc_solve_args& A, 
                             cudaStream_t st) {
   const size_t smem = am_solve_smem_bytes(NB, C.npad, C.kxs, C.kps, warps, A.team);
   auto kfn = am_solve_kernel<NB, NKM, F32, TEAMS>;
-  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  // raise the dynamic shared-memory limit once per device and size (a driver
+  // call per launch costs microseconds of host time on the critical path)
+  static std::atomic<int> granted[16];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::atomic<int>& g = granted[dev & 15];
+  if ((int)smem > g.load(std::memory_order_relaxed)) {
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int cur = g.load();
+    while ((int)smem > cur && !g.compare_exchange_weak(cur, (int)smem)) {
+    }
+  }
   const int ipb = warps / A.team;  // instances per block
   const int grid = (A.L + ipb - 1) / ipb;
   kfn<<<grid, warps * 32, smem, st>>>(C, A);

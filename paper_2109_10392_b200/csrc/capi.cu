@@ -7,6 +7,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <chrono>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -51,13 +52,13 @@ cudaError_t op_score(const ScoreArgs& S, cudaStream_t st);
 cudaError_t op_argmin(int S, int l, const double* meta, const uint8_t* flags, long long* best,
                       long long* best_all, long long* best_hc, long long* nfeas, cudaStream_t st);
 cudaError_t op_pack_xi(long long total, const double* xi_x, const double* xi_y, double* out,
-                       cudaStream_t st, double* scaled = nullptr, double a = 1.0, double b = 1.0);
-cudaError_t op_first_clear(int iters, const int* notconv, int* tstar, cudaStream_t st);
+                       cudaStream_t st, double* scaled = nullptr, double a = 1.0, double b = 1.0,
+                       int* zero = nullptr, int nzero = 0);
+cudaError_t op_early_stop(int max_iter, const int* notconv, int* rerun, int* status, int* status2,
+                          cudaStream_t st);
 cudaError_t op_assemble(int S, int V, int m, int n, int l, const double* veh, const int* nveh,
                         const double* ego, const double* goals, const double* rel, double* xi_x,
                         double* xi_y, double* b_xy, double* b_psi, cudaStream_t st);
-cudaError_t op_rerun_plan(int max_iter, const int* tstar, int* rerun, int* status, int* status2,
-                          cudaStream_t st);
 cudaError_t dfma_peak_tflops(int reps, double* tflops, cudaStream_t st);
 cudaError_t op_math_check(int fn, long long n, const double* a, const double* b, double* out,
                           double* out2, cudaStream_t st);
@@ -591,24 +592,23 @@ static int solve_impl(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opt
   cudaStream_t st = S_(stream);
   const int L = p->S * p->l;
   const long long tot = (long long)p->S * p->m * ctx->C.n;
-  double* xi2 = nullptr;
-  // scratch ints: [0] first converged sweep, [1, max_iter] not-converged flags
-  // per sweep, [max_iter + 1] re-run sweep count, [max_iter + 2, + 3] status
-  int* scr = nullptr;
-  if (tot > 0) {
-    // raw pairs, then the ellipse-frame pairs for the sweeps' outside test
-    CK(cudaMallocAsync(&xi2, tot * 4 * sizeof(double), st), "cudaMallocAsync");
-    CK(bmpc::op_pack_xi(tot, p->xi_x, p->xi_y, xi2, st, xi2 + 2 * tot, p->a, p->b), "pack_xi");
-  }
   const int mode = is_warm(o) ? BMPC_INIT_WARM : BMPC_INIT_COLD;
   const int M = o->max_iter;
   int status[2] = {M, 0};
-  if (L > 0) {
-    CK(cudaMallocAsync(&scr, (size_t)(M + 4) * sizeof(int), st), "cudaMallocAsync");
-    CK(cudaMemsetAsync(scr, 0x7f, sizeof(int), st), "memset");  // "none" = 0x7f7f7f7f
-    CK(cudaMemsetAsync(scr + 1, 0, (size_t)M * sizeof(int), st), "memset");
-  }
-  rc = launch_sweeps(ctx, p, xi2, o, M, mode, 0, nullptr, 0, out, st, fsc, scr ? scr + 1 : nullptr);
+  // One workspace: the packed predictions (raw pairs, then the ellipse-frame
+  // pairs of the sweeps' outside test) and the scratch ints -- [0, M) the
+  // per-sweep not-converged flags, [M] the re-run sweep count, [M + 1, M + 2]
+  // {iterations, converged}.  k_pack_xi zeroes the flags (no memset call).
+  const size_t xi_bytes = (size_t)tot * 4 * sizeof(double);
+  char* wsp = nullptr;
+  CK(cudaMallocAsync(&wsp, xi_bytes + (size_t)(M + 4) * sizeof(int), st), "cudaMallocAsync");
+  double* xi2 = tot > 0 ? reinterpret_cast<double*>(wsp) : nullptr;
+  int* scr = L > 0 ? reinterpret_cast<int*>(wsp + xi_bytes) : nullptr;
+  if (tot > 0 || L > 0)
+    CK(bmpc::op_pack_xi(tot, p->xi_x, p->xi_y, xi2, st, xi2 ? xi2 + 2 * tot : nullptr, p->a, p->b,
+                        scr, scr ? M : 0),
+       "pack_xi");
+  rc = launch_sweeps(ctx, p, xi2, o, M, mode, 0, nullptr, 0, out, st, fsc, scr);
   if (!rc && L > 0) {
     // Global early stop (solver.py:437-439): the first sweep whose worst
     // residual over every instance is <= tol.  When it is not the last one the
@@ -616,15 +616,13 @@ static int solve_impl(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opt
     // deterministic, so the re-run reproduces the same iterates).  The decision
     // and the re-run launch stay on the device -- the second launch exits at
     // once when there is nothing to redo -- so nothing waits on the host.
-    CK(bmpc::op_first_clear(M, scr + 1, scr, st), "first_clear");
-    CK(bmpc::op_rerun_plan(M, scr, scr + M + 1, scr + M + 2, o->status_dev, st), "rerun_plan");
-    rc = launch_sweeps(ctx, p, xi2, o, M, mode, 0, nullptr, 0, out, st, fsc, scr + 1, scr + M + 1);
+    CK(bmpc::op_early_stop(M, scr, scr + M, scr + M + 1, o->status_dev, st), "early_stop");
+    rc = launch_sweeps(ctx, p, xi2, o, M, mode, 0, nullptr, 0, out, st, fsc, scr, scr + M);
   }
   if (!rc && post) rc = post_solve(post, st);
   if (!rc && L > 0 && !o->status_dev)
-    CK(cudaMemcpyAsync(status, scr + M + 2, sizeof(status), cudaMemcpyDeviceToHost, st), "memcpy");
-  if (xi2) cudaFreeAsync(xi2, st);
-  if (scr) cudaFreeAsync(scr, st);
+    CK(cudaMemcpyAsync(status, scr + M + 1, sizeof(status), cudaMemcpyDeviceToHost, st), "memcpy");
+  cudaFreeAsync(wsp, st);
   if (rc) return rc;
   CK(cudaGetLastError(), "bmpc_solve");
   if (o->status_dev) {
@@ -757,6 +755,38 @@ int bmpc_plan_host_layout(const bmpc_ctx* ctx, int S, int l, int score, long lon
   return BMPC_OK;
 }
 
+// BMPC_TRACE=1: bmpc_plan_host prints its host / device phase times to stderr
+// (tools/e2e_breakdown.py); off by default.
+struct PlanTrace {
+  bool on = false;
+  cudaStream_t st = nullptr;
+  std::chrono::steady_clock::time_point h[8];
+  cudaEvent_t e[8];
+  int nh = 0, ne = 0;
+  explicit PlanTrace(cudaStream_t s) : st(s) {
+    static const bool env = getenv("BMPC_TRACE") != nullptr;
+    on = env;
+    if (on)
+      for (auto& ev : e) cudaEventCreate(&ev);
+  }
+  void host() { if (on && nh < 8) h[nh++] = std::chrono::steady_clock::now(); }
+  void dev() { if (on && ne < 8) cudaEventRecord(e[ne++], st); }
+  ~PlanTrace() {
+    if (!on) return;
+    fprintf(stderr, "[bmpc_trace] host us:");
+    for (int i = 1; i < nh; ++i)
+      fprintf(stderr, " %.1f", std::chrono::duration<double, std::micro>(h[i] - h[i - 1]).count());
+    fprintf(stderr, " | device us:");
+    for (int i = 1; i < ne; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e[i - 1], e[i]);
+      fprintf(stderr, " %.1f", ms * 1e3);
+    }
+    fprintf(stderr, "\n");
+    for (auto& ev : e) cudaEventDestroy(ev);
+  }
+};
+
 int bmpc_plan_host(bmpc_ctx* ctx, const bmpc_problem* hp, const bmpc_solve_opts* o,
                    bmpc_solve_out* ho, const bmpc_score_spec* spec, bmpc_score_out* hs,
                    void* stream) {
@@ -765,6 +795,8 @@ int bmpc_plan_host(bmpc_ctx* ctx, const bmpc_problem* hp, const bmpc_solve_opts*
   if (!o || !ho) return fail(BMPC_EINVAL, "null opts/out");
   if (is_warm(o)) return fail(BMPC_EINVAL, "bmpc_plan_host: warm starts use the device API");
   cudaStream_t st = S_(stream);
+  PlanTrace tr(st);
+  tr.host();
   const int n = ctx->C.n, nb = ctx->C.nb;
   const size_t L = (size_t)hp->S * hp->l, mn = (size_t)hp->m * n, S = (size_t)hp->S;
   const bool score = spec && hs;
@@ -815,10 +847,14 @@ int bmpc_plan_host(bmpc_ctx* ctx, const bmpc_problem* hp, const bmpc_solve_opts*
   double* xiy = (double*)(arena + o_xiy);
   double* bxy = (double*)(arena + o_bxy);
   double* bps = (double*)(arena + o_bps);
+  tr.host();
+  tr.dev();
   CK(cudaMemcpyAsync(xix, hp->xi_x, S * mn * 8, cudaMemcpyHostToDevice, st), "h2d");
   CK(cudaMemcpyAsync(xiy, hp->xi_y, S * mn * 8, cudaMemcpyHostToDevice, st), "h2d");
   CK(cudaMemcpyAsync(bxy, hp->b_xy, 12 * L * 8, cudaMemcpyHostToDevice, st), "h2d");
   CK(cudaMemcpyAsync(bps, hp->b_psi, 4 * L * 8, cudaMemcpyHostToDevice, st), "h2d");
+  tr.host();
+  tr.dev();
   bmpc_problem dp = *hp;
   dp.xi_x = xix;
   dp.xi_y = xiy;
@@ -859,6 +895,8 @@ int bmpc_plan_host(bmpc_ctx* ctx, const bmpc_problem* hp, const bmpc_solve_opts*
     rc = bmpc_solve(ctx, &dp, o, &dout, stream);
   }
   if (rc) return rc;
+  tr.host();
+  tr.dev();
   // rarely requested extras straight to the caller's memory
   struct Cp { void* h; const void* d; size_t bytes; };
   const Cp extra[] = {
@@ -870,7 +908,10 @@ int bmpc_plan_host(bmpc_ctx* ctx, const bmpc_problem* hp, const bmpc_solve_opts*
     if (c.h && c.d && c.bytes) CK(cudaMemcpyAsync(c.h, c.d, c.bytes, cudaMemcpyDeviceToHost, st), "d2h");
   if (direct) {
     CK(cudaMemcpyAsync(direct, arena + o_res0, res_bytes, cudaMemcpyDeviceToHost, st), "d2h");
+    tr.dev();
+    tr.host();
     CK(cudaStreamSynchronize(st), "sync");
+    tr.host();
     const int* stat = (const int*)(direct + R.stat);
     ho->iterations = stat[0];
     ho->converged = stat[1];

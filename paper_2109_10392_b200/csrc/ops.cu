@@ -379,24 +379,14 @@ __global__ void k_argmin(int l, const double* __restrict__ meta, const uint8_t* 
 // (b xi_x, a xi_y) that the sweep's outside test reads.
 __global__ void k_pack_xi(long long total, const double* __restrict__ xi_x,
                           const double* __restrict__ xi_y, double2* __restrict__ out,
-                          double2* __restrict__ scaled, double a, double b) {
+                          double2* __restrict__ scaled, double a, double b, int* zero,
+                          int nzero) {
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < nzero) zero[e] = 0;  // the solve's scratch flags (saves a memset call)
   if (e >= total) return;
   const double x = xi_x[e], y = xi_y[e];
   out[e] = make_double2(x, y);
   if (scaled) scaled[e] = make_double2(b * x, a * y);
-}
-
-// First iteration t whose worst residual over all instances is <= tol
-// (solver.py:437-439); rows >= iters leave *tstar untouched.
-// First sweep no instance flagged as not converged (the persistent kernel
-// raises notconv[t] for any worst residual that is not <= tol, NaN included).
-__global__ void k_first_clear(int iters, const int* __restrict__ notconv, int* tstar) {
-  int best = 0x7f7f7f7f;
-  for (int t = threadIdx.x; t < iters; t += blockDim.x)
-    if (notconv[t] == 0) best = min(best, t);
-  for (int o = 16; o >= 1; o >>= 1) best = min(best, __shfl_xor_sync(BMPC_FULL, best, o));
-  if ((threadIdx.x & 31) == 0 && best < 0x7f7f7f7f) atomicMin(tstar, best);
 }
 
 // ---------------------------------------------------------------- launchers --
@@ -479,18 +469,30 @@ cudaError_t op_argmin(int S, int l, const double* meta, const uint8_t* flags, lo
   return cudaGetLastError();
 }
 cudaError_t op_pack_xi(long long total, const double* xi_x, const double* xi_y, double* out,
-                       cudaStream_t st, double* scaled, double a, double b) {
-  if (total > 0)
-    k_pack_xi<<<nblk(total), kTB, 0, st>>>(total, xi_x, xi_y, reinterpret_cast<double2*>(out),
-                                           reinterpret_cast<double2*>(scaled), a, b);
+                       cudaStream_t st, double* scaled, double a, double b, int* zero, int nzero) {
+  const long long work = total > nzero ? total : nzero;
+  if (work > 0)
+    k_pack_xi<<<nblk(work), kTB, 0, st>>>(total, xi_x, xi_y, reinterpret_cast<double2*>(out),
+                                          reinterpret_cast<double2*>(scaled), a, b, zero, nzero);
   return cudaGetLastError();
 }
-// Device-side early-stop decision: the re-run sweep count (0 = none) and the
-// {iterations, converged} status of the solve.
-__global__ void k_rerun_plan(int max_iter, const int* tstar, int* rerun, int* status, int* status2) {
-  const int t = *tstar;
-  const bool conv = t < max_iter;
-  const int iters = conv ? t + 1 : max_iter;
+
+// Early-stop decision in one launch (solver.py:437-439): t* = the first sweep no
+// instance flagged as not converged; re-run t* + 1 sweeps unless that is all
+// of them (0 = no re-run); {iterations, converged} into status (and status2).
+__global__ void k_early_stop(int max_iter, const int* __restrict__ notconv, int* rerun, int* status,
+                             int* status2) {
+  __shared__ int wbest[8];
+  int best = 0x7f7f7f7f;
+  for (int t = threadIdx.x; t < max_iter; t += blockDim.x)
+    if (notconv[t] == 0) best = min(best, t);
+  for (int o = 16; o >= 1; o >>= 1) best = min(best, __shfl_xor_sync(BMPC_FULL, best, o));
+  if ((threadIdx.x & 31) == 0) wbest[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) best = min(best, wbest[w]);
+  const bool conv = best < max_iter;
+  const int iters = conv ? best + 1 : max_iter;
   *rerun = (conv && iters < max_iter) ? iters : 0;
   status[0] = iters;
   status[1] = conv ? 1 : 0;
@@ -500,16 +502,13 @@ __global__ void k_rerun_plan(int max_iter, const int* tstar, int* rerun, int* st
   }
 }
 
-cudaError_t op_rerun_plan(int max_iter, const int* tstar, int* rerun, int* status, int* status2,
+cudaError_t op_early_stop(int max_iter, const int* notconv, int* rerun, int* status, int* status2,
                           cudaStream_t st) {
-  k_rerun_plan<<<1, 1, 0, st>>>(max_iter, tstar, rerun, status, status2);
+  k_early_stop<<<1, 256, 0, st>>>(max_iter, notconv, rerun, status, status2);
   return cudaGetLastError();
 }
-
-cudaError_t op_first_clear(int iters, const int* notconv, int* tstar, cudaStream_t st) {
-  if (iters > 0) k_first_clear<<<1, 256, 0, st>>>(iters, notconv, tstar);
-  return cudaGetLastError();
-}
+// Device-side early-stop decision: the re-run sweep count (0 = none) and the
+// {iterations, converged} status of the solve.
 
 }  // namespace bmpc
 
