@@ -362,6 +362,11 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
 #pragma unroll
         for (int u = 0; u < U; ++u) qn[s][u] = __ldg(qp[s] + u * qstep);
     }
+#ifndef BMPC_OBST_UNROLL
+#define BMPC_OBST_UNROLL 1
+#endif
+    constexpr int kObstUnroll = BMPC_OBST_UNROLL;
+#pragma unroll kObstUnroll
     for (; j + (U - 1) * js < T.m; j += U * js) {
       double2 q[NS][U];
 #pragma unroll
