@@ -282,16 +282,18 @@ def test_smoke_entry(cuda):
     __graft_entry__.smoke()
 
 
-def test_fused_scoring_equals_standalone(cuda):
+@pytest.mark.parametrize("name", ["c3s", "c4s"])
+def test_fused_scoring_equals_standalone(cuda, name):
     """bmpc_plan's in-kernel scoring epilogue == bmpc_score on the solved
-    coefficients, bit for bit (same shared code, csrc/score.cuh)."""
+    coefficients, bit for bit (same shared code, csrc/score.cuh; c3s reads the
+    last sweep's stored positions, c4s (n = 200) re-samples them)."""
     import ctypes
 
     from paper_2109_10392_b200 import _native as nat
     from paper_2109_10392_b200 import device as D
     from paper_2109_10392_b200.planner import FilterLimits, MetaCostSpec, _spec_struct
 
-    z = golden("c3s")
+    z = golden(name)
     solver = _solver(z)
     S = _Scenes(z)
     prob = D.DeviceProblem.from_host(int(z["n"]), S.xi_x, S.xi_y, S.b_xy, S.b_psi, S.l, S.a, S.b,
@@ -434,3 +436,44 @@ def test_null_space_qp_info_and_refinement(cuda, monkeypatch):
                    {"c_x": res.c_x, "c_y": res.c_y, "c_psi": res.c_psi})
     assert err.max() <= 1e-11, err.max()
     assert res.best_index == res2.best_index
+
+
+def test_plan_host_direct_block_equals_staged(cuda):
+    """plan_batch's zero-copy result block (one pinned block at the
+    bmpc_plan_host_layout offsets) and the staged path (separate pageable
+    numpy outputs) return the same bits."""
+    import ctypes
+
+    from paper_2109_10392_b200 import _native as nat
+    from paper_2109_10392_b200.planner import FilterLimits, MetaCostSpec, _spec_struct, plan_batch
+
+    z = golden("c3s")
+    solver = _solver(z)
+    S = _Scenes(z)
+    spec, limits = MetaCostSpec("cruise", v_cruise=20.0), FilterLimits()
+    res = plan_batch(solver, S, max_iter=30, tol=0.0, spec=spec, limits=limits)
+    assert res.c_x.base is not None  # a view of the pinned block
+    nb, L, Sn = solver.basis.n_b, S.l * S.S, S.S
+    c = lambda a: np.ascontiguousarray(a, dtype=np.float64)  # noqa: E731
+    xi_x, xi_y, b_xy, b_psi = c(S.xi_x), c(S.xi_y), c(S.b_xy), c(S.b_psi)
+    prob = nat.Problem(xi_x.shape[1] // solver.basis.grid.n, S.l, Sn, xi_x.ctypes.data, xi_y.ctypes.data,
+                       b_xy.ctypes.data, b_psi.ctypes.data, S.a, S.b, S.v_min, S.v_max, S.a_max)
+    coef, rf = np.empty((3, nb, L)), np.empty((3, L))
+    out = nat.SolveOut(coef[0].ctypes.data, coef[1].ctypes.data, coef[2].ctypes.data, None, None, None,
+                       None, None, rf.ctypes.data, 0, 0)
+    meta, mr, hm = np.empty((3, L))
+    flags = np.empty(L, dtype=np.uint8)
+    idx = np.empty((4, Sn), dtype=np.int64)
+    so = nat.ScoreOut(meta.ctypes.data, mr.ctypes.data, hm.ctypes.data, flags.ctypes.data,
+                      idx[0].ctypes.data, idx[1].ctypes.data, idx[2].ctypes.data, idx[3].ctypes.data)
+    nat.check(nat.load().bmpc_plan_host(solver._context(), ctypes.byref(prob),
+                                        ctypes.byref(nat.SolveOpts(max_iter=30, tol=0.0)), ctypes.byref(out),
+                                        ctypes.byref(_spec_struct(spec, limits)), ctypes.byref(so), None),
+              "plan_host")
+    for got, want in ((res.c_x, coef[0]), (res.c_y, coef[1]), (res.c_psi, coef[2]), (res.res_final, rf),
+                      (res.meta_cost, meta), (res.min_ratio, mr), (res.heading_max, hm),
+                      (res.flags, flags), (res.argmin_all, idx[1]), (res.argmin_hc, idx[2]),
+                      (res.n_feasible, idx[3])):
+        assert np.array_equal(got, want, equal_nan=got.dtype.kind == "f")
+    assert [b if b is not None else -1 for b in res.best_index] == list(idx[0])
+    assert res.iterations == out.iterations == 30
