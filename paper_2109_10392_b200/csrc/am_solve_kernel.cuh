@@ -260,6 +260,16 @@ __device__ __forceinline__ void obstacle_inside_term(double x, double y, double2
   cin += 1.0;
 }
 
+// Obstacles in flight per sample: pair passes, single full slots, split leftover slots.
+#ifndef BMPC_UPAIR
+#define BMPC_UPAIR 2
+#endif
+#ifndef BMPC_USINGLE
+#define BMPC_USINGLE 5
+#endif
+#ifndef BMPC_USPLIT
+#define BMPC_USPLIT 1
+#endif
 // Two sample slots per obstacle pass when the accumulators leave register room.
 template <int NB>
 constexpr bool kPairSlots = NB <= 12;
@@ -304,7 +314,7 @@ __device__ __forceinline__ void obstacle_term_f32(double xs, double ys, double2 
 // summed over `group` consecutive lanes (warp-uniform) before the group leader
 // contributes them.  The acceleration and non-holonomic blocks run in passes
 // A and B of the sweep.
-template <int NS, int NB, int NPAD, bool F32>
+template <int NS, int NB, int NPAD, bool F32, int U>
 __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)[NS], int j0, int js,
                                                int group, bool valid, bool leader,
                                                double (&Gx)[NB], double (&Gy)[NB], double& sqo) {
@@ -340,10 +350,8 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
     const double ia = T.ia, ib = T.ib;
     BMPC_PROF_NS(10);
     const int qstep = js * T.n;
-#ifndef BMPC_UPAIR
-#define BMPC_UPAIR 2
-#endif
-    constexpr int U = NS == 1 ? 4 : BMPC_UPAIR;  // obstacles in flight per sample (NS * U terms)
+
+    // U obstacles in flight per sample (NS * U terms per group)
     const double2* qp[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) qp[s] = T.xi + j0 * T.n + k[s];
@@ -953,15 +961,19 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
 #pragma unroll 1
         for (; r + TW < sl.F; r += 2 * TW) {
           const int ks[2] = {lane + 32 * r, lane + 32 * (r + TW)};
-          obstacle_block<2, NB, npad, F32>(T, ks, 0, 1, 0, true, true, Gx, Gy, sqo);
+          obstacle_block<2, NB, npad, F32, BMPC_UPAIR>(T, ks, 0, 1, 0, true, true, Gx, Gy, sqo);
         }
       }
 #pragma unroll 1
       for (; r < nslots; r += TW) {
         const Slot S = slot(r, lane, sl);
         const int ks[1] = {S.k};
-        obstacle_block<1, NB, npad, F32>(T, ks, S.j0, S.js, (r == sl.F) ? sl.g : 1, S.valid,
-                                         S.leader, Gx, Gy, sqo);
+        if (r < sl.F)  // a full slot on its own
+          obstacle_block<1, NB, npad, F32, BMPC_USINGLE>(T, ks, S.j0, S.js, 1, S.valid, S.leader, Gx,
+                                                         Gy, sqo);
+        else  // the leftover samples, obstacles split over lane groups (js = g)
+          obstacle_block<1, NB, npad, F32, BMPC_USPLIT>(T, ks, S.j0, S.js, sl.g, S.valid, S.leader,
+                                                        Gx, Gy, sqo);
       }
     }
     BMPC_PROF(5);
