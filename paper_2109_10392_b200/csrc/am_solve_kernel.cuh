@@ -270,6 +270,11 @@ __device__ __forceinline__ void obstacle_inside_term(double x, double y, double2
 #ifndef BMPC_USPLIT
 #define BMPC_USPLIT 1
 #endif
+#ifndef BMPC_USPLIT_MANY
+// long horizons (n > 192): the leftover slot is split over fewer lanes per
+// sample, so each lane walks many obstacles (c4: m = 50 over g = 4 lanes)
+#define BMPC_USPLIT_MANY 4
+#endif
 // Two sample slots per obstacle pass when the accumulators leave register room.
 template <int NB>
 constexpr bool kPairSlots = NB <= 12;
@@ -972,8 +977,8 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
           obstacle_block<1, NB, npad, F32, BMPC_USINGLE>(T, ks, S.j0, S.js, 1, S.valid, S.leader, Gx,
                                                          Gy, sqo);
         else  // the leftover samples, obstacles split over lane groups (js = g)
-          obstacle_block<1, NB, npad, F32, BMPC_USPLIT>(T, ks, S.j0, S.js, sl.g, S.valid, S.leader,
-                                                        Gx, Gy, sqo);
+          obstacle_block<1, NB, npad, F32, (NKM >= 7 ? BMPC_USPLIT_MANY : BMPC_USPLIT)>(
+              T, ks, S.j0, S.js, sl.g, S.valid, S.leader, Gx, Gy, sqo);
       }
     }
     BMPC_PROF(5);
