@@ -509,6 +509,13 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
 #define BMPC_CH 2
 #endif
   constexpr int CH = NKM < BMPC_CH ? NKM : BMPC_CH;  // sample slots per pass A / B chunk
+#ifndef BMPC_CHUNK_UNROLL_A
+#define BMPC_CHUNK_UNROLL_A 2  // two pass-A chunks in flight (overlaps one chunk's atan2 with the next one's sampling)
+#endif
+#ifndef BMPC_CHUNK_UNROLL_B
+#define BMPC_CHUNK_UNROLL_B 1
+#endif
+  constexpr int kChunkUnrollA = BMPC_CHUNK_UNROLL_A, kChunkUnrollB = BMPC_CHUNK_UNROLL_B;
   // constant image (am_args.h, capi.cu bmpc_ctx_create)
   double* sPT = sm;                          // P^T, Pdot^T, Pddot^T
   double* sM = sPT + 3 * NB * npad;  // m P^T P + Pddot^T Pddot (written above)
@@ -890,7 +897,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
         }
       };
       int r0 = wt;
-#pragma unroll 1
+#pragma unroll kChunkUnrollA
       for (; r0 + (CH - 1) * TW < NKM; r0 += CH * TW) chunk_a(std::integral_constant<int, CH>{}, r0);
 #pragma unroll 1
       for (; CH > 1 && r0 < NKM; r0 += TW) chunk_a(std::integral_constant<int, 1>{}, r0);  // remainder
@@ -1084,7 +1091,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
     };
     {
       int r0 = wt;
-#pragma unroll 1
+#pragma unroll kChunkUnrollB
       for (; r0 + (CH - 1) * TW < NKM; r0 += CH * TW) chunk_b(std::integral_constant<int, CH>{}, r0);
 #pragma unroll 1
       for (; CH > 1 && r0 < NKM; r0 += TW) chunk_b(std::integral_constant<int, 1>{}, r0);
