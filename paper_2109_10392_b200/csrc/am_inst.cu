@@ -8,11 +8,11 @@ namespace bmpc {
 
 size_t am_solve_smem_bytes(int nb, int npad, int kxs, int kps, int warps, int team);
 
-template <int NB, int NKM, bool F32, bool TEAMS = false>
+template <int NB, int NKM, bool F32, bool TEAMS = false, bool XS = false>
 static cudaError_t launch_t(const bmpc_dev_consts& C, const bmpc_solve_args& A, int warps,
-                            cudaStream_t st) {
-  const size_t smem = am_solve_smem_bytes(NB, C.npad, C.kxs, C.kps, warps, A.team);
-  auto kfn = am_solve_kernel<NB, NKM, F32, TEAMS>;
+                            cudaStream_t st, size_t xs_bytes = 0) {
+  const size_t smem = am_solve_smem_bytes(NB, C.npad, C.kxs, C.kps, warps, A.team) + xs_bytes;
+  auto kfn = am_solve_kernel<NB, NKM, F32, TEAMS, XS>;
   // raise the dynamic shared-memory limit once per device and size (a driver
   // call per launch costs microseconds of host time on the critical path)
   static std::atomic<int> granted[16];
@@ -32,6 +32,22 @@ static cudaError_t launch_t(const bmpc_dev_consts& C, const bmpc_solve_args& A, 
   return cudaGetLastError();
 }
 
+// Bytes of staged predictions for one block (0: stage none).
+static size_t xs_stage_bytes(const bmpc_dev_consts& C, const bmpc_solve_args& A, int warps) {
+#ifdef BMPC_NO_XI_STAGE
+  return 0;
+#endif
+  if (A.team != 1 || C.npad > 128 || A.m <= 0 || !A.xis || A.l < warps) return 0;
+  const int scenes = (A.S > 1 && A.l % warps != 0) ? 2 : 1;
+  const size_t xs = (size_t)scenes * A.m * C.n * 16;
+  static int optin[16] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!optin[dev & 15]) cudaDeviceGetAttribute(&optin[dev & 15], cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t base = am_solve_smem_bytes(C.nb, C.npad, C.kxs, C.kps, warps, 1);
+  return base + xs <= (size_t)optin[dev & 15] ? xs : 0;
+}
+
 #define BMPC_CAT2(a, b) a##b
 #define BMPC_CAT(a, b) BMPC_CAT2(a, b)
 
@@ -45,6 +61,17 @@ cudaError_t BMPC_CAT(launch_am_nb_, BMPC_INST_NB)(const bmpc_dev_consts& C,
       case 64: return launch_t<BMPC_INST_NB, 2, false, true>(C, A, warps, st);
       case 128: return launch_t<BMPC_INST_NB, 4, false, true>(C, A, warps, st);
       default: return cudaErrorNotSupported;
+    }
+  }
+  // Obstacle predictions staged in shared memory (bulk copies with the
+  // constants) when the scene(s) of a block fit next to the scratch: n <= 128,
+  // fp64; a block spans at most two scenes when l >= its instance count.
+  const size_t xs = xs_stage_bytes(C, A, warps);
+  if (!f32 && xs > 0) {
+    switch (C.npad) {
+      case 64: return launch_t<BMPC_INST_NB, 2, false, false, true>(C, A, warps, st, xs);
+      case 128: return launch_t<BMPC_INST_NB, 4, false, false, true>(C, A, warps, st, xs);
+      default: break;
     }
   }
   switch (C.npad) {  // the host pads n to 64, 128, 224 or 256 samples

@@ -319,7 +319,17 @@ __device__ __forceinline__ void obstacle_term_f32(double xs, double ys, double2 
 // summed over `group` consecutive lanes (warp-uniform) before the group leader
 // contributes them.  The acceleration and non-holonomic blocks run in passes
 // A and B of the sweep.
-template <int NS, int NB, int NPAD, bool F32, int U>
+// Prediction loads: shared memory when the block staged its scene(s), else
+// the read-only global path.
+template <bool XS>
+__device__ __forceinline__ double2 ldq(const double2* p) {
+  if constexpr (XS)
+    return *p;
+  else
+    return __ldg(p);
+}
+
+template <int NS, int NB, int NPAD, bool F32, int U, bool XS>
 __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)[NS], int j0, int js,
                                                int group, bool valid, bool leader,
                                                double (&Gx)[NB], double (&Gy)[NB], double& sqo) {
@@ -373,7 +383,7 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
 #pragma unroll
       for (int s = 0; s < NS; ++s)
 #pragma unroll
-        for (int u = 0; u < U; ++u) qn[s][u] = __ldg(qp[s] + u * qstep);
+        for (int u = 0; u < U; ++u) qn[s][u] = ldq<XS>(qp[s] + u * qstep);
     }
 #ifndef BMPC_OBST_UNROLL
 #define BMPC_OBST_UNROLL 1
@@ -390,7 +400,7 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
 #pragma unroll
         for (int s = 0; s < NS; ++s)
 #pragma unroll
-          for (int u = 0; u < U; ++u) qn[s][u] = __ldg(qp[s] + (U + u) * qstep);
+          for (int u = 0; u < U; ++u) qn[s][u] = ldq<XS>(qp[s] + (U + u) * qstep);
       }
       {
         // outside test in fp64 for both modes; the rare inside terms in the
@@ -424,7 +434,7 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
     for (; j < T.m; j += js) {
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
-        const double2 q = __ldg(qp[s]);
+        const double2 q = ldq<XS>(qp[s]);
         if (obstacle_inside_s(x[s], y[s], q, abd2)) {
           if constexpr (F32)
             obstacle_term_f32(x[s], y[s], q, af, bf, ab2, ia, ib, srx[s], sry[s], sqf[s], cin[s]);
@@ -478,7 +488,7 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
   BMPC_PROF_NS(13);
 }
 
-template <int NB, int NKM, bool F32, bool TEAMS>
+template <int NB, int NKM, bool F32, bool TEAMS, bool XS>
 #ifndef BMPC_MINB
 #define BMPC_MINB 1
 #endif
@@ -564,14 +574,32 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
   // streams it in with bulk asynchronous copies (TMA, cp.async.bulk) that
   // complete on an mbarrier, instead of every warp issuing the loads.
   __shared__ __align__(8) unsigned long long s_cbar;
+  // XS: this block's scene(s) of ellipse-frame predictions ride in the same
+  // bulk transfer, after the scratch (instances blockIdx.x * ipb ... span at
+  // most two scenes, xs_stage_bytes in am_inst.cu)
+  const int ipb = W / TW;
+  const int first_inst = blockIdx.x * ipb;
+  const int scene0 = first_inst / A.l;
+  double* sXi = sm + C.const_doubles + (size_t)ipb * bmpc_team_doubles(npad, TW);
   if (threadIdx.x == 0) {
     const unsigned bytes = (unsigned)C.const_doubles * 8u;
+    unsigned xbytes = 0;
+    if constexpr (XS) {
+      const int last_inst = min(A.L, first_inst + ipb) - 1;
+      xbytes = (unsigned)((last_inst / A.l - scene0 + 1) * A.m * n * 16);
+    }
     mbar_init(&s_cbar, 1);
-    mbar_arrive_expect_tx(&s_cbar, bytes);
+    mbar_arrive_expect_tx(&s_cbar, bytes + xbytes);
     constexpr unsigned kChunk = 16384;
     for (unsigned o = 0; o < bytes; o += kChunk)
       bulk_copy_g2s(reinterpret_cast<char*>(sm) + o, reinterpret_cast<const char*>(C.PT) + o,
                     bytes - o < kChunk ? bytes - o : kChunk, &s_cbar);
+    if constexpr (XS) {
+      const char* src = reinterpret_cast<const char*>(A.xis) + (size_t)scene0 * A.m * n * 16;
+      for (unsigned o = 0; o < xbytes; o += kChunk)
+        bulk_copy_g2s(reinterpret_cast<char*>(sXi) + o, src + o, xbytes - o < kChunk ? xbytes - o : kChunk,
+                      &s_cbar);
+    }
   }
   __syncthreads();  // the initialised barrier is visible to every thread
   mbar_wait_parity(&s_cbar, 0);
@@ -594,7 +622,8 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
   const double2* __restrict__ xi =
       reinterpret_cast<const double2*>(A.xi) + (size_t)(inst / A.l) * A.m * n;
   const double2* __restrict__ xis =
-      reinterpret_cast<const double2*>(A.xis) + (size_t)(inst / A.l) * A.m * n;
+      XS ? reinterpret_cast<const double2*>(sXi) + (size_t)(inst / A.l - scene0) * A.m * n
+         : reinterpret_cast<const double2*>(A.xis) + (size_t)(inst / A.l) * A.m * n;
   const int m = A.m;
   const double a = A.a, b = A.b, rho = C.rho;
   const double inv_a = 1.0 / a, inv_b = 1.0 / b;
@@ -973,7 +1002,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
 #pragma unroll 1
         for (; r + TW < sl.F; r += 2 * TW) {
           const int ks[2] = {lane + 32 * r, lane + 32 * (r + TW)};
-          obstacle_block<2, NB, npad, F32, BMPC_UPAIR>(T, ks, 0, 1, 0, true, true, Gx, Gy, sqo);
+          obstacle_block<2, NB, npad, F32, BMPC_UPAIR, XS>(T, ks, 0, 1, 0, true, true, Gx, Gy, sqo);
         }
       }
 #pragma unroll 1
@@ -981,10 +1010,10 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
         const Slot S = slot(r, lane, sl);
         const int ks[1] = {S.k};
         if (r < sl.F)  // a full slot on its own
-          obstacle_block<1, NB, npad, F32, BMPC_USINGLE>(T, ks, S.j0, S.js, 1, S.valid, S.leader, Gx,
-                                                         Gy, sqo);
+          obstacle_block<1, NB, npad, F32, BMPC_USINGLE, XS>(T, ks, S.j0, S.js, 1, S.valid, S.leader,
+                                                             Gx, Gy, sqo);
         else  // the leftover samples, obstacles split over lane groups (js = g)
-          obstacle_block<1, NB, npad, F32, (NKM >= 7 ? BMPC_USPLIT_MANY : BMPC_USPLIT)>(
+          obstacle_block<1, NB, npad, F32, (NKM >= 7 ? BMPC_USPLIT_MANY : BMPC_USPLIT), XS>(
               T, ks, S.j0, S.js, sl.g, S.valid, S.leader, Gx, Gy, sqo);
       }
     }
