@@ -631,6 +631,10 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
   const int li = lane & 15;
   const bool yax = lane >= 16;
   const bool owner = li < NB;
+  // lanes holding the three block residuals after each sweep's reduction
+  constexpr bool kSqCols = NB + 3 <= 16;
+  constexpr int sq_lane0 = kSqCols ? NB : 16;
+  const bool is_sq_lane = lane >= sq_lane0 && lane < sq_lane0 + 3;
 
   // persistent per-lane state (owner lanes)
   double lam = 0.0, G = 0.0;   // lane i: lambda_x[i], G_x[i]; lane 16+i: lambda_y[i], G_y[i]
@@ -1133,20 +1137,32 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
     //     summation order), residual sums by xor butterflies (identical on all
     //     lanes).  lambda step F_axis^T (F_axis c - g) = (F_axis^T F_axis) c - G
     //     = (Pdot^T Pdot) c - lane partials.
+    // For n_b <= 13 the three squared-residual partials ride in the free
+    // x-half columns n_b, n_b+1, n_b+2 of the same transpose (lanes n_b..n_b+2
+    // end with the block totals); wider bases use xor butterflies (lanes 16..18).
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
       ws.red[lane * kRedStride + i] = Gx[i];
       ws.red[lane * kRedStride + 16 + i] = Gy[i];
     }
+    if constexpr (kSqCols) {
+      ws.red[lane * kRedStride + NB] = sqo;
+      ws.red[lane * kRedStride + NB + 1] = sqa;
+      ws.red[lane * kRedStride + NB + 2] = sqn;
+    }
     __syncwarp();
-    double gn = owner ? column_sum(ws.red, lane) : 0.0;
-    sqo = warp_sum(sqo);
-    sqa = warp_sum(sqa);
-    sqn = warp_sum(sqn);
+    double gn = (owner || is_sq_lane) ? column_sum(ws.red, lane) : 0.0;
+    if constexpr (!kSqCols) {
+      sqo = warp_sum(sqo);
+      sqa = warp_sum(sqa);
+      sqn = warp_sum(sqn);
+    }
     __syncwarp();
     if (TW > 1) {  // team: sum the warps' partials in a fixed order
       if (owner) xch[32 + lane] = gn;
-      if (lane == 0) {
+      if constexpr (kSqCols) {
+        if (is_sq_lane) xch[64 + lane - NB] = gn;
+      } else if (lane == 0) {
         xch[64] = sqo;
         xch[65] = sqa;
         xch[66] = sqn;
@@ -1156,7 +1172,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
       sqo = sqa = sqn = 0.0;
       for (int w = 0; w < TW; ++w) {
         const double* xw = xch_of(w);
-        gn += owner ? xw[32 + lane] : 0.0;
+        gn += owner ? xw[32 + lane] : (kSqCols && is_sq_lane ? xw[64 + lane - NB] : 0.0);
         sqo += xw[64];
         sqa += xw[65];
         sqn += xw[66];
@@ -1178,23 +1194,24 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
       lam -= rho * ((a3[0] + a3[1]) - rest);
     }
     if (!yax && owner) lamp -= rho * Lp;
-    const double sqv = lane == 16 ? sqo : (lane == 17 ? sqa : sqn);  // lanes 16..18
+    const double sqv = kSqCols ? gn : (lane == 16 ? sqo : (lane == 17 ? sqa : sqn));  // sq lanes
     if (A.notconv && wt == 0) {  // global early stop: flag this sweep unless every residual <= tol
       // res = sqrt(sqv) <= tol; for tol = 0 (the fixed-sweep benchmarks) that is
       // exactly sqv <= 0 (sqrt is exact at +-0 and keeps NaN), so the square
       // root stays off the sweep's critical path
       const bool ok = A.tol > 0.0 ? sqrt(sqv) <= A.tol : (A.tol == 0.0 && sqv <= 0.0);
-      const bool nc = __any_sync(BMPC_FULL, lane >= 16 && lane < 19 && !ok);
+      const bool nc = __any_sync(BMPC_FULL, is_sq_lane && !ok);
       // a plain store: the flag only ever goes 0 -> 1, and a read-before-write
       // would stall the warp on a coherent L2 round trip every sweep
       if (lane == 0 && nc) A.notconv[A.hist_offset + t] = 1;
     }
-    if (lane >= 16 && lane < 19 && wt == 0 && ((A.flags & BMPC_F_HISTORY) || last)) {
+    if (is_sq_lane && wt == 0 && ((A.flags & BMPC_F_HISTORY) || last)) {
       const double res = sqrt(sqv);
+      const int blk = lane - sq_lane0;  // 0 obstacle, 1 acceleration, 2 non-holonomic
       if (A.flags & BMPC_F_HISTORY)
-        A.hist[((size_t)(A.hist_offset + t) * 3 + (lane - 16)) * L + inst] = res;
-      if (last && A.res_final) A.res_final[(size_t)(lane - 16) * L + inst] = res;
-      if (last) ws.res[60 + lane - 16] = res;  // for the fused scoring below
+        A.hist[((size_t)(A.hist_offset + t) * 3 + blk) * L + inst] = res;
+      if (last && A.res_final) A.res_final[(size_t)blk * L + inst] = res;
+      if (last) ws.res[60 + blk] = res;  // for the fused scoring below
     }
     have_sol = true;
     BMPC_PROF(7);
