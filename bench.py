@@ -367,7 +367,11 @@ def roofline_entry(args, achieved, peak, k_ms, step_ms, n, m, nb):
                  f"instance-sweep (SURVEY.md 8d)",
          "kernel_timing": "CUDA events on the bench stream around bmpc_sweeps launches "
                           "(same inputs, L2 flushed), median",
-         "peak_source": "measured live: DFMA microbenchmark (csrc/peak.cu)"}
+         "peak_source": "measured live: DFMA microbenchmark (csrc/peak.cu)",
+         "note": "frac = canonical algorithmic work per second over the FP64 peak; the kernel "
+                 "executes less than W (exact-form obstacle/acceleration blocks: an outside test "
+                 "per obstacle term), so frac can exceed 1 on obstacle-heavy configs; the executed "
+                 "FP64-pipe utilisation is ncu.fp64_pipe_active_pct"}
     prof = ROOT / "profiles" / f"ncu_{args.config}_{args.precision}.json"
     if prof.exists():
         d = json.loads(prof.read_text())
