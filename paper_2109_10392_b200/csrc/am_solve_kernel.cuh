@@ -1033,15 +1033,6 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
       if (!yax && owner) ws.cp[li] = c;
       __syncwarp();
     }
-    // lambda_psi step P^T (psi - theta) = (P^T P) c_psi - P^T theta (solver.py:494)
-    double Lp = 0.0;
-    if (!yax && owner) {
-      const double* mr = sMp + li * C.kms;
-      double s4[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-      for (int j = 0; j < NB; ++j) s4[j & 3] = fma(mr[j], ws.cp[j], s4[j & 3]);
-      Lp = ((s4[0] + s4[1]) + (s4[2] + s4[3])) - pth;
-    }
     BMPC_PROF(4);
 
     // (5) pass B: psi = P c_psi and the non-holonomic block (_speedups.pyx:200-216),
@@ -1193,7 +1184,15 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
       G = (a1[0] + a1[1]) + rest;
       lam -= rho * ((a3[0] + a3[1]) - rest);
     }
-    if (!yax && owner) lamp -= rho * Lp;
+    // lambda_psi step P^T (psi - theta) = (P^T P) c_psi - P^T theta (solver.py:494),
+    // evaluated here where its latency overlaps the residual bookkeeping
+    if (!yax && owner) {
+      const double* mr = sMp + li * C.kms;
+      double s4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int j = 0; j < NB; ++j) s4[j & 3] = fma(mr[j], ws.cp[j], s4[j & 3]);
+      lamp -= rho * (((s4[0] + s4[1]) + (s4[2] + s4[3])) - pth);
+    }
     const double sqv = kSqCols ? gn : (lane == 16 ? sqo : (lane == 17 ? sqa : sqn));  // sq lanes
     if (A.notconv && wt == 0) {  // global early stop: flag this sweep unless every residual <= tol
       // res = sqrt(sqv) <= tol; for tol = 0 (the fixed-sweep benchmarks) that is
