@@ -116,7 +116,7 @@ typedef struct {
 #define BMPC_HD
 #endif
 // Per-warp shared scratch of the persistent kernel (csrc/am_solve_kernel.cuh):
-// 288 doubles of KKT vectors, the per-sample arrays (theta, xdot, ydot and,
+// 64 doubles of QP vectors (c_xy pairs, c_psi, residuals), the per-sample arrays (theta, xdot, ydot and,
 // for npad <= 128, x and y), and the 32 x 33 transpose buffer.
 #ifndef BMPC_XY_NPAD_MAX
 #define BMPC_XY_NPAD_MAX 128
@@ -126,10 +126,10 @@ typedef struct {
 #endif
 BMPC_HD constexpr bool bmpc_stores_xy(int npad) { return npad <= BMPC_XY_NPAD_MAX; }
 BMPC_HD constexpr int bmpc_sample_arrays(int npad) { return bmpc_stores_xy(npad) ? 5 : 3; }
-// Team layout (team = the TW warps sharing one instance): per warp 288 KKT
+// Team layout (team = the TW warps sharing one instance): per warp 64 QP
 // doubles + the 32 x 33 transpose buffer + 72 exchange doubles; per team the
 // per-sample arrays once.
-BMPC_HD constexpr int bmpc_warp_private_doubles() { return 288 + 32 * 33 + 72; }
+BMPC_HD constexpr int bmpc_warp_private_doubles() { return 64 + 32 * 33 + 72; }
 BMPC_HD constexpr int bmpc_team_doubles(int npad, int tw) {
   return tw * bmpc_warp_private_doubles() + bmpc_sample_arrays(npad) * npad;
 }

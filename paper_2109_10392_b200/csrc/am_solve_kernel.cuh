@@ -106,12 +106,9 @@ __device__ __forceinline__ void mbar_wait_parity(unsigned long long* bar, unsign
 }
 
 struct WarpScratch {
-  double* bc;    // 64: KKT right-hand sides (x at 0, y at kYOff)
-  double* sol;   // 64: [c; mu] of the xy QP, kept across sweeps (x at 0, y at kYOff)
-  double* res;   // 64: refinement residual rhs - K * sol
   double* cxy;   // 32: (c_x[i], c_y[i]) pairs
   double* cp;    // 16: c_psi
-  double* solp;  // 32: [c_psi; mu_psi], kept across sweeps
+  double* res;   // 16: the last sweep's block residuals (fused scoring)
   double* th;    // npad: theta per sample (read back only by the unwrap slow path)
   double* xd;    // npad: xdot per sample (pass A -> pass B)
   double* yd;    // npad: ydot per sample
@@ -119,13 +116,7 @@ struct WarpScratch {
   double* y;     // npad: y per sample
   double* red;   // 32 x kRedStride: transpose buffer of the sample contractions
 };
-constexpr int kWarpScratch = 288;
-// y-axis offset of the xy KKT vectors in bc/sol/res: odd, so the x-row and
-// y-row lanes' broadcast reads of element j hit different banks
-#ifndef BMPC_YOFF
-#define BMPC_YOFF 33
-#endif
-constexpr int kYOff = BMPC_YOFF;
+constexpr int kWarpScratch = 64;
 constexpr int kRedStride = 33;
 constexpr int kRedSize = 32 * kRedStride;
 
@@ -546,7 +537,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
   double* tbase = sTau + npad + team * bmpc_team_doubles(npad, TW);
   double* wbase = tbase + wt * bmpc_warp_private_doubles();
   double* arr = tbase + TW * bmpc_warp_private_doubles();
-  WarpScratch ws{wbase,       wbase + 64,   wbase + 128, wbase + 192, wbase + 224, wbase + 256,
+  WarpScratch ws{wbase,       wbase + 32,   wbase + 48,
                  arr,         arr + npad,   arr + 2 * npad,
                  kStoreXY ? arr + 3 * npad : nullptr, kStoreXY ? arr + 4 * npad : nullptr,
                  wbase + kWarpScratch};
@@ -1210,7 +1201,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
       if (A.flags & BMPC_F_HISTORY)
         A.hist[((size_t)(A.hist_offset + t) * 3 + blk) * L + inst] = res;
       if (last && A.res_final) A.res_final[(size_t)blk * L + inst] = res;
-      if (last) ws.res[60 + blk] = res;  // for the fused scoring below
+      if (last) ws.res[blk] = res;  // for the fused scoring below
     }
     have_sol = true;
     BMPC_PROF(7);
@@ -1250,7 +1241,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
     };
     double cost, rmin, hmax;
     unsigned char f;
-    score_instance(sp, xi, sample, ws.res[60], ws.res[61], ws.res[62], cost, rmin, hmax, f);
+    score_instance(sp, xi, sample, ws.res[0], ws.res[1], ws.res[2], cost, rmin, hmax, f);
     if (lane == 0) {
       F.meta[inst] = cost;
       F.min_ratio[inst] = rmin;
