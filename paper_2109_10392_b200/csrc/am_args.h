@@ -15,6 +15,8 @@ typedef struct {
   int kms;        // padded (odd) row stride of M
   double rho;
   const double* PT;   // [3][nb][npad]: P^T, Pdot^T, Pddot^T, zero padded past n
+  const double* IMG;  // the persistent kernel's constant image (shared-memory layout):
+                      // the basis in bmpc_basis_index order, then M, the QP blocks, tau
   const double* tau;  // [npad] (t_k - t0)/(tf - t0), cold-start line parameter
   const double* Kxf;  // [nb+6][kxs] inverse of the per-axis KKT matrix
   const double* Kxa;  // [nb+6][kxs] the per-axis KKT matrix (refinement residual)
@@ -35,6 +37,21 @@ __host__ __device__
 #endif
 static inline size_t bmpc_const_image_doubles(int nb, int npad) {
   return (size_t)3 * nb * npad + (size_t)8 * nb * (nb | 1) + (size_t)12 * nb + (size_t)npad;
+}
+
+// Basis order of the constant image.  When npad is a whole number of slot
+// pairs (64, 128, 256), row `row` (q * nb + i for basis q in {P, Pdot, Pddot})
+// at sample k sits at
+//   (row * npad / 64 + k / 64) * 64 + 2 * (k % 32) + (k / 32) % 2,
+// so samples k and k + 32 of an even slot pair are adjacent and one 16-byte
+// shared load feeds both slots of a pass chunk; otherwise (npad = 224) rows
+// are plain, row * npad + k.
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+static inline int bmpc_basis_index(int row, int k, int npad) {
+  return (npad & 63) ? row * npad + k
+                     : (row * (npad >> 6) + (k >> 6)) * 64 + ((k & 31) << 1) + ((k >> 5) & 1);
 }
 
 enum { BMPC_INIT_COLD = 0, BMPC_INIT_WARM = 1, BMPC_INIT_RESUME = 2 };

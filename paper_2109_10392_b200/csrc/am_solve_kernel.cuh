@@ -310,6 +310,29 @@ __device__ __forceinline__ void obstacle_term_f32(double xs, double ys, double2 
 // summed over `group` consecutive lanes (warp-uniform) before the group leader
 // contributes them.  The acceleration and non-holonomic blocks run in passes
 // A and B of the sweep.
+// Basis rows at the slots of a chunk: with PAIRED the NS == 2 slots are an even
+// slot pair (samples k and k + 32), adjacent in the paired-slot image, so one
+// 16-byte load returns both; otherwise one load per slot.
+template <int NS, bool PAIRED, int NPAD>
+__device__ __forceinline__ void basis1(const double* B, int i, const int (&k)[NS], double (&v)[NS]) {
+  if constexpr (PAIRED && NS == 2) {
+    const double2 w = *reinterpret_cast<const double2*>(B + bmpc_basis_index(i, k[0], NPAD));
+    v[0] = w.x;
+    v[1] = w.y;
+  } else {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) v[s] = B[bmpc_basis_index(i, k[s], NPAD)];
+  }
+}
+template <int NS, bool PAIRED, int NPAD>
+__device__ __forceinline__ void basis3(const double* B0, const double* B1, const double* B2, int i,
+                                       const int (&k)[NS], double (&v0)[NS], double (&v1)[NS],
+                                       double (&v2)[NS]) {
+  basis1<NS, PAIRED, NPAD>(B0, i, k, v0);
+  basis1<NS, PAIRED, NPAD>(B1, i, k, v1);
+  basis1<NS, PAIRED, NPAD>(B2, i, k, v2);
+}
+
 // Prediction loads: shared memory when the block staged its scene(s), else
 // the read-only global path.
 template <bool XS>
@@ -320,7 +343,7 @@ __device__ __forceinline__ double2 ldq(const double2* p) {
     return __ldg(p);
 }
 
-template <int NS, int NB, int NPAD, bool F32, int U, bool XS>
+template <int NS, int NB, int NPAD, bool F32, int U, bool XS, bool PAIRED>
 __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)[NS], int j0, int js,
                                                int group, bool valid, bool leader,
                                                double (&Gx)[NB], double (&Gy)[NB], double& sqo) {
@@ -339,11 +362,12 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
 #pragma unroll
       for (int i = 0; i < NB; ++i) {
         const double2 c = T.cxy[i];
+        double p[NS];
+        basis1<NS, PAIRED, NPAD>(T.P, i, k, p);
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
-          const double p = T.P[i * NPAD + k[s]];
-          x[s] = fma(p, c.x, x[s]);
-          y[s] = fma(p, c.y, y[s]);
+          x[s] = fma(p[s], c.x, x[s]);
+          y[s] = fma(p[s], c.y, y[s]);
         }
       }
     }
@@ -468,11 +492,12 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
   if (__any_sync(BMPC_FULL, any)) {
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
+      double p[NS];
+      basis1<NS, PAIRED, NPAD>(T.P, i, k, p);
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
-        const double p = T.P[i * NPAD + k[s]];
-        Gx[i] = fma(p, gsx[s], Gx[i]);
-        Gy[i] = fma(p, gsy[s], Gy[i]);
+        Gx[i] = fma(p[s], gsx[s], Gx[i]);
+        Gy[i] = fma(p[s], gsy[s], Gy[i]);
       }
     }
   }
@@ -518,7 +543,11 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
 #endif
   constexpr int kChunkUnrollA = BMPC_CHUNK_UNROLL_A, kChunkUnrollB = BMPC_CHUNK_UNROLL_B;
   // constant image (am_args.h, capi.cu bmpc_ctx_create)
-  double* sPT = sm;                          // P^T, Pdot^T, Pddot^T
+  // basis rows in paired-slot order when npad is a whole number of slot pairs
+  // (bmpc_basis_index); two-slot chunks are then even slot pairs (one warp per
+  // instance)
+  constexpr bool PAIRED = !TEAMS && (npad % 64) == 0;
+  double* sPT = sm;                  // P^T, Pdot^T, Pddot^T
   double* sM = sPT + 3 * NB * npad;  // m P^T P + Pddot^T Pddot (written above)
   double* sMp = sM + NB * C.kms;     // P^T P
   double* sMdd = sMp + NB * C.kms;   // Pddot^T Pddot
@@ -583,7 +612,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
     mbar_arrive_expect_tx(&s_cbar, bytes + xbytes);
     constexpr unsigned kChunk = 16384;
     for (unsigned o = 0; o < bytes; o += kChunk)
-      bulk_copy_g2s(reinterpret_cast<char*>(sm) + o, reinterpret_cast<const char*>(C.PT) + o,
+      bulk_copy_g2s(reinterpret_cast<char*>(sm) + o, reinterpret_cast<const char*>(C.IMG) + o,
                     bytes - o < kChunk ? bytes - o : kChunk, &s_cbar);
     if constexpr (XS) {
       const char* src = reinterpret_cast<const char*>(A.xis) + (size_t)scene0 * A.m * n * 16;
@@ -610,6 +639,8 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
   const double* __restrict__ sP = sPT;
   const double* __restrict__ sPd = sPT + NB * npad;
   const double* __restrict__ sPdd = sPT + 2 * NB * npad;
+  // basis value (row i of sP / sPd / sPdd) at sample k
+  auto bi = [](int i, int k) { return bmpc_basis_index(i, k, npad); };
   const double2* __restrict__ xi =
       reinterpret_cast<const double2*>(A.xi) + (size_t)(inst / A.l) * A.m * n;
   const double2* __restrict__ xis =
@@ -756,7 +787,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
         } else {
           double ps = 0.0;
 #pragma unroll
-          for (int i = 0; i < NB; ++i) ps = fma(sP[i * npad + k], A.w_cpsi[(size_t)i * L + inst], ps);
+          for (int i = 0; i < NB; ++i) ps = fma(sP[bi(i, k)], A.w_cpsi[(size_t)i * L + inst], ps);
           for (int j = 0; j < m; ++j) {
             const double2 q = __ldg(xi + j * n + k);
             const size_t row = (size_t)(j * n + k) * L + inst;
@@ -778,7 +809,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
         }
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
-          const double p = sP[i * npad + k], pd = sPd[i * npad + k], pdd = sPdd[i * npad + k];
+          const double p = sP[bi(i, k)], pd = sPd[bi(i, k)], pdd = sPdd[bi(i, k)];
           ax[i] = fma(p, gsx, ax[i]);
           ax[i] = fma(pdd, gax, ax[i]);
           ax[i] = fma(pd, gnx, ax[i]);
@@ -848,16 +879,16 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
           const double2 c = cxy[i];
+          double p[NSC], pd[NSC], pdd[NSC];
+          basis3<NSC, PAIRED, npad>(sP, sPd, sPdd, i, k, p, pd, pdd);
 #pragma unroll
           for (int s = 0; s < NSC; ++s) {
-            const double p = sP[i * npad + k[s]], pd = sPd[i * npad + k[s]],
-                         pdd = sPdd[i * npad + k[s]];
-            xx[s] = fma(p, c.x, xx[s]);
-            yy[s] = fma(p, c.y, yy[s]);
-            xd[s] = fma(pd, c.x, xd[s]);
-            yd[s] = fma(pd, c.y, yd[s]);
-            xdd[s] = fma(pdd, c.x, xdd[s]);
-            ydd[s] = fma(pdd, c.y, ydd[s]);
+            xx[s] = fma(p[s], c.x, xx[s]);
+            yy[s] = fma(p[s], c.y, yy[s]);
+            xd[s] = fma(pd[s], c.x, xd[s]);
+            yd[s] = fma(pd[s], c.y, yd[s]);
+            xdd[s] = fma(pdd[s], c.x, xdd[s]);
+            ydd[s] = fma(pdd[s], c.y, ydd[s]);
           }
         }
         double th[NSC];
@@ -892,10 +923,10 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
         }
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
+          double p[NSC];
+          basis1<NSC, PAIRED, npad>(sP, i, k, p);
 #pragma unroll
-          for (int s = 0; s < NSC; ++s) {
-            pt[i] = fma(sP[i * npad + k[s]], th[s], pt[i]);
-          }
+          for (int s = 0; s < NSC; ++s) pt[i] = fma(p[s], th[s], pt[i]);
         }
         if (__any_sync(BMPC_FULL, anyclip)) {  // clipped samples: g = a_max (cos, sin)
           double ex[NSC], ey[NSC];  // g_acc - acc
@@ -911,11 +942,12 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
           }
 #pragma unroll
           for (int i = 0; i < NB; ++i) {
+            double pdd[NSC];
+            basis1<NSC, PAIRED, npad>(sPdd, i, k, pdd);
 #pragma unroll
             for (int s = 0; s < NSC; ++s) {
-                const double pdd = sPdd[i * npad + k[s]];
-              Gx[i] = fma(pdd, ex[s], Gx[i]);
-              Gy[i] = fma(pdd, ey[s], Gy[i]);
+              Gx[i] = fma(pdd[s], ex[s], Gx[i]);
+              Gy[i] = fma(pdd[s], ey[s], Gy[i]);
             }
           }
         }
@@ -936,7 +968,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
           if (k < n) {
             const double t = ws.th[k];
 #pragma unroll
-            for (int i = 0; i < NB; ++i) pt[i] = fma(sP[i * npad + k], t, pt[i]);
+            for (int i = 0; i < NB; ++i) pt[i] = fma(sP[bi(i, k)], t, pt[i]);
           }
         }
       };
@@ -997,7 +1029,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
 #pragma unroll 1
         for (; r + TW < sl.F; r += 2 * TW) {
           const int ks[2] = {lane + 32 * r, lane + 32 * (r + TW)};
-          obstacle_block<2, NB, npad, F32, BMPC_UPAIR, XS>(T, ks, 0, 1, 0, true, true, Gx, Gy, sqo);
+          obstacle_block<2, NB, npad, F32, BMPC_UPAIR, XS, PAIRED>(T, ks, 0, 1, 0, true, true, Gx, Gy, sqo);
         }
       }
 #pragma unroll 1
@@ -1005,10 +1037,10 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
         const Slot S = slot(r, lane, sl);
         const int ks[1] = {S.k};
         if (r < sl.F)  // a full slot on its own
-          obstacle_block<1, NB, npad, F32, BMPC_USINGLE, XS>(T, ks, S.j0, S.js, 1, S.valid, S.leader,
+          obstacle_block<1, NB, npad, F32, BMPC_USINGLE, XS, false>(T, ks, S.j0, S.js, 1, S.valid, S.leader,
                                                              Gx, Gy, sqo);
         else  // the leftover samples, obstacles split over lane groups (js = g)
-          obstacle_block<1, NB, npad, F32, (NKM >= 7 ? BMPC_USPLIT_MANY : BMPC_USPLIT), XS>(
+          obstacle_block<1, NB, npad, F32, (NKM >= 7 ? BMPC_USPLIT_MANY : BMPC_USPLIT), XS, false>(
               T, ks, S.j0, S.js, sl.g, S.valid, S.leader, Gx, Gy, sqo);
       }
     }
@@ -1050,10 +1082,12 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
       for (int s = 0; s < NSC; ++s) ps1[s] = 0.0;
 #pragma unroll
       for (int i = 0; i < NB; ++i) {
+        double p[NSC];
+        basis1<NSC, PAIRED, npad>(sP, i, k, p);
 #pragma unroll
         for (int s = 0; s < NSC; ++s) {
-          if (i & 1) ps1[s] = fma(sP[i * npad + k[s]], cps_reg[i], ps1[s]);
-          else ps[s] = fma(sP[i * npad + k[s]], cps_reg[i], ps[s]);
+          if (i & 1) ps1[s] = fma(p[s], cps_reg[i], ps1[s]);
+          else ps[s] = fma(p[s], cps_reg[i], ps[s]);
         }
       }
 #pragma unroll
@@ -1096,11 +1130,12 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
       }
 #pragma unroll
       for (int i = 0; i < NB; ++i) {
+        double pd[NSC];
+        basis1<NSC, PAIRED, npad>(sPd, i, k, pd);
 #pragma unroll
         for (int s = 0; s < NSC; ++s) {
-          const double pd = sPd[i * npad + k[s]];
-          Gx[i] = fma(pd, gnx[s], Gx[i]);
-          Gy[i] = fma(pd, gny[s], Gy[i]);
+          Gx[i] = fma(pd[s], gnx[s], Gx[i]);
+          Gy[i] = fma(pd[s], gny[s], Gy[i]);
         }
       }
     };
@@ -1226,12 +1261,12 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
         x = ws.x[k];
         y = ws.y[k];
 #pragma unroll
-        for (int i = 0; i < NB; ++i) ps = __fma_rn(sP[i * npad + k], ws.cp[i], ps);
+        for (int i = 0; i < NB; ++i) ps = __fma_rn(sP[bi(i, k)], ws.cp[i], ps);
       } else {
         x = y = 0.0;
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
-          const double p = sP[i * npad + k];
+          const double p = sP[bi(i, k)];
           const double2 c = cxy2[i];
           x = __fma_rn(p, c.x, x);
           y = __fma_rn(p, c.y, y);

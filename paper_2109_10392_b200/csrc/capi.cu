@@ -277,13 +277,20 @@ int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pd
   //   Z_xy, H_xy, Z_psi, H_psi | B_xy [nb][8], B_psi [nb][4] | tau
   // followed in global memory only by the full KKT inverse / matrix pairs
   // (the step API's refined solves, csrc/steps.cu).
+  // Layout of the one allocation: the plain transposed basis PT (the ABI's
+  // bmpc_ctx_info, the stand-alone kernels), then the image, then the KKT pairs.
   const size_t nimg = bmpc_const_image_doubles(nb, npad);
-  std::vector<double> h(nimg + 2 * nKx + 2 * nKp, 0.0);
+  const size_t oI = nPT;  // image start (nPT is even: 16-byte aligned)
+  std::vector<double> h(nPT + nimg + 2 * nKx + 2 * nKp, 0.0);
   const double* mats[3] = {P, Pdot, Pddot};
   for (int q = 0; q < 3; ++q)
     for (int i = 0; i < nb; ++i)
-      for (int k = 0; k < n; ++k) h[((size_t)q * nb + i) * npad + k] = mats[q][(size_t)k * nb + i];
-  const size_t oM = nPT;
+      for (int k = 0; k < n; ++k) {
+        const double v = mats[q][(size_t)k * nb + i];
+        h[((size_t)q * nb + i) * npad + k] = v;
+        h[oI + bmpc_basis_index(q * nb + i, k, npad)] = v;
+      }
+  const size_t oM = oI + (size_t)3 * nb * npad;
   for (int i = 0; i < nb; ++i)
     for (int j = 0; j < nb; ++j) h[oM + (size_t)i * kms + j] = ftf_axis[(size_t)i * nb + j];
   // P^T P, Pddot^T Pddot, Pdot^T Pdot right after F_axis^T F_axis (the
@@ -312,7 +319,7 @@ int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pd
   const size_t otau = o;
   for (int k = 0; k < n; ++k) h[otau + k] = tau[k];
   size_t offs[4];
-  o = nimg;
+  o = oI + nimg;
   const double* blocks[4] = {kinv_axis, k_axis, kinv_psi, k_psi};
   const int dims[4] = {rx, rx, rp, rp}, strides[4] = {kxs, kxs, kps, kps};
   for (int q = 0; q < 4; ++q) {
@@ -350,6 +357,7 @@ int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pd
   c->C.kms = kms;
   c->C.rho = rho;
   c->C.PT = c->dmem;
+  c->C.IMG = c->dmem + oI;
   c->C.Kxf = c->dmem + offs[0];
   c->C.Kxa = c->dmem + offs[1];
   c->C.Kpf = c->dmem + offs[2];
