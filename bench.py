@@ -346,7 +346,10 @@ def run_ours(args, rank, world, local_rank):
                        "parallelism": f"goal/scene shards x{world}"},
             "roofline": roofline_entry(args, achieved, peak, k_ms, t_max / args.steps, n, W.m, nb),
             "e2e": {"value": e2e_value, "unit": "problems/s", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_local / args.steps},
+                    "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_local / args.steps,
+                    "path": "plan_batch -> bmpc_plan_host: page-locked inputs read in place over "
+                            "the host link by the kernels, results back in one copy into a "
+                            "pinned block"},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
