@@ -477,3 +477,24 @@ def test_plan_host_direct_block_equals_staged(cuda):
         assert np.array_equal(got, want, equal_nan=got.dtype.kind == "f")
     assert [b if b is not None else -1 for b in res.best_index] == list(idx[0])
     assert res.iterations == out.iterations == 30
+
+
+def test_plan_host_pinned_inputs_read_in_place(cuda):
+    """Page-locked inputs (read in place by the kernels) and pageable inputs
+    (copied in) give the same bits."""
+    import torch
+
+    from paper_2109_10392_b200.planner import FilterLimits, MetaCostSpec, plan_batch
+
+    z = golden("c3s")
+    solver = _solver(z)
+    S = _Scenes(z)
+    P = _Scenes(z)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).pin_memory().numpy()  # noqa: E731
+    P.xi_x, P.xi_y, P.b_xy, P.b_psi = pin(S.xi_x), pin(S.xi_y), pin(S.b_xy), pin(S.b_psi)
+    spec, limits = MetaCostSpec("cruise", v_cruise=20.0), FilterLimits()
+    a = plan_batch(solver, S, max_iter=30, tol=0.0, spec=spec, limits=limits)
+    b = plan_batch(solver, P, max_iter=30, tol=0.0, spec=spec, limits=limits)
+    for k in ("c_x", "c_y", "c_psi", "res_final", "meta_cost", "min_ratio", "heading_max", "flags"):
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
+    assert a.best_index == b.best_index
