@@ -7,16 +7,19 @@
 // KB of per-warp shared memory).  Per sweep (reference
 // /root/reference/pkg/src/batchmpc/solver.py:458-500):
 //
-//   1. xy QP     [c; mu] = K_axis^-1 [rho*G + lambda ; b], refined against K
-//                (solver.py:302-312, :164-168)
+//   1. xy QP     null-space form of [c; mu] = K_axis^-1 [rho*G + lambda ; b]
+//                (solver.py:302-312): c = B b + Z (rho*G + lambda), the boundary
+//                part B b once per solve, one refinement step against H only
+//                on ill-conditioned shapes (:164-168; capi.cu reduced_qp)
 //   2. pass A    x, y, xdot, ydot, xddot, yddot = [P; Pdot; Pddot] c;
 //                theta = unwrap(atan2(ydot, xdot)) (:474-477); acceleration
 //                block (kernels/_speedups.pyx:179-198); P^T theta, Pddot^T g_a
-//   3. psi QP    c_psi = K_psi^-1 [rho*P^T theta + lambda_psi ; b_psi], refined
+//   3. psi QP    the same for c_psi from rho*P^T theta + lambda_psi and b_psi
 //                (:322-328); lambda_psi step via (P^T P) c_psi - P^T theta
 //   4. pass B    psi = P c_psi, non-holonomic block (_speedups.pyx:200-216), Pdot^T g_n
 //   5. obstacles exact form of _speedups.pyx:150-176 (outside: g_j = x, r_j = 0),
-//                P^T sum_j g_j
+//                P^T sum_j g_j; the outside test in the ellipse frame on
+//                predictions staged in shared memory (n <= 128)
 //   6. G = F_axis^T g reduction; lambda_xy -= rho ((F_axis^T F_axis) c - G) (:491-494)
 //
 // Lanes split the horizon samples k (k = lane + 32*r); lane i owns coefficient i
@@ -183,21 +186,6 @@ __device__ __forceinline__ Slot slot(int r, int lane, const SlotLayout& sl) {
     S.leader = false;
   }
   return S;
-}
-
-// One row of a KKT apply.  The QP steps run the reference's refined solve
-// (solver.py:164-168) -- sol = K^-1 rhs; sol += K^-1 (rhs - K sol) -- with the
-// LU factors replaced by the explicit inverse; without the refinement step the
-// explicit inverse loses up to 5e-8 relative at the c4 shape (cond 3.9e6).
-template <int LEN>
-__device__ __forceinline__ double kkt_row_dot(const double* __restrict__ kr,
-                                              const double* __restrict__ v) {
-  // four interleaved partial sums: the QP steps sit on the critical path of
-  // every sweep, so their latency matters more than their (tiny) flop count
-  double s[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-  for (int j = 0; j < LEN; ++j) s[j & 3] = fma(kr[j], v[j], s[j & 3]);
-  return (s[0] + s[1]) + (s[2] + s[3]);
 }
 
 // Exact form of the same closed forms (fp64 path): outside the ellipse
