@@ -79,6 +79,7 @@ EXPORTS = {
     "bmpc_carry_doubles": ([c_void_p], c_int),
     "bmpc_ctx_info": ([c_void_p, POINTER(c_int), POINTER(c_int), POINTER(c_int), POINTER(c_void_p)], c_int),
     "bmpc_ctx_qp_info": ([c_void_p, POINTER(c_double), POINTER(c_double), POINTER(c_int)], c_int),
+    "bmpc_reduced_qp": ([c_int, c_int, _dp, _dp, _dp, POINTER(c_double)], c_int),
     "bmpc_solve": ([c_void_p, POINTER(Problem), POINTER(SolveOpts), POINTER(SolveOut), c_void_p], c_int),
     "bmpc_sweeps": ([c_void_p, POINTER(Problem), POINTER(SolveOpts), c_int, c_int, c_int, c_void_p,
                      c_int, POINTER(SolveOut), c_void_p], c_int),

@@ -380,6 +380,17 @@ int bmpc_ctx_destroy(bmpc_ctx* ctx) {
   return BMPC_OK;
 }
 
+int bmpc_reduced_qp(int nb, int rows, const double* k, double* z, double* bmap, double* cond1) {
+  if (!k || !z || !bmap || !cond1 || (rows != 4 && rows != 6) || nb < rows || nb > 16)
+    return fail(BMPC_EINVAL, "bmpc_reduced_qp: bad arguments");
+  std::vector<double> Z, B;
+  const int rc = reduced_qp(nb, rows, k, Z, B, cond1);
+  if (rc != BMPC_OK) return rc;
+  memcpy(z, Z.data(), Z.size() * sizeof(double));
+  memcpy(bmap, B.data(), B.size() * sizeof(double));
+  return BMPC_OK;
+}
+
 int bmpc_ctx_qp_info(const bmpc_ctx* ctx, double* cond_xy, double* cond_psi, int* refine) {
   if (!ctx) return fail(BMPC_EINVAL, "null ctx");
   if (cond_xy) *cond_xy = ctx->cond_xy;

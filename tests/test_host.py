@@ -183,3 +183,37 @@ def test_ctypes_arity_matches_header():
         name, params = m.group(1), m.group(2).strip()
         n = 0 if params in ("", "void") else params.count(",") + 1
         assert len(_native.EXPORTS[name][0]) == n, (name, n, len(_native.EXPORTS[name][0]))
+
+
+@pytest.mark.parametrize("n,t_f,deg,m", [(100, 5.0, 10, 10), (200, 10.0, 15, 50), (40, 2.0, 6, 2)])
+def test_null_space_qp_matches_kkt_solve(n, t_f, deg, m, rng):
+    """bmpc_reduced_qp (the persistent solve's QP form, host-only C ABI): the
+    boundary rows fix the end coefficients, c = Z rhs + B b; it must reproduce
+    the coefficient part of the reference's per-axis / heading KKT solves."""
+    lib = _native.load()
+    s = make_solver(n, t_f, deg, m)
+    nb = s.basis.n_b
+    conds = {}
+    for name, K, rows in (("xy", s.kkt.matrix_axis, 6), ("psi", s.kkt.matrix_psi, 4)):
+        K = np.ascontiguousarray(K, dtype=np.float64)
+        Z, B = np.zeros((nb, nb)), np.zeros((nb, rows))
+        cond = ctypes.c_double()
+        assert lib.bmpc_reduced_qp(nb, rows, _native.c_double_ptr(K), _native.c_double_ptr(Z),
+                                   _native.c_double_ptr(B), ctypes.byref(cond)) == 0
+        conds[name] = cond.value
+        rhs = rng.normal(0, 100.0, (nb, 32))
+        b = rng.normal(0, 10.0, (rows, 32))
+        ref = np.linalg.solve(K, np.vstack([rhs, b]))[:nb]
+        got = Z @ rhs + B @ b
+        tol = 1e-9 if cond.value < 1e4 else 1e-7
+        assert np.abs(got - ref).max() <= tol * max(1.0, np.abs(ref).max()), name
+        # boundary rows hold exactly: A c = b
+        A = K[nb:, :nb]
+        assert np.abs(A @ got - b).max() <= 1e-9 * max(1.0, np.abs(b).max())
+    if (n, deg) == (100, 10):
+        assert conds["xy"] < 1e4 and conds["psi"] < 1e4   # no refinement on c0-c3
+    if (n, deg) == (200, 15):
+        assert conds["xy"] > 1e4                           # c4 refines
+    bad = np.zeros(((nb + 6) * (nb + 6)))
+    assert lib.bmpc_reduced_qp(nb, 6, _native.c_double_ptr(bad), _native.c_double_ptr(np.zeros((nb, nb))),
+                               _native.c_double_ptr(np.zeros((nb, 6))), ctypes.byref(ctypes.c_double())) != 0
