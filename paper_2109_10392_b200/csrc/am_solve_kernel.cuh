@@ -1083,18 +1083,26 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
       // branch-free sin/cos for every slot first, so the slots interleave; the
       // full-range fallback (huge / non-finite headings) is one rare branch
       double sps[NSC], cps[NSC];
-      bool big = false;
+      bool q0 = true;
 #pragma unroll
-      for (int s = 0; s < NSC; ++s) {
-        sps[s] = 0.0;
-        cps[s] = 1.0;
-        sincos_nb(ps[s], &sps[s], &cps[s]);
-        big |= !(fabs(ps[s]) < 1.0e5);
-      }
-      if (big) {
+      for (int s = 0; s < NSC; ++s) q0 &= fabs(ps[s]) <= 0.78;
+      if (__all_sync(BMPC_FULL, q0)) {  // headings within +-45 deg (the common case)
 #pragma unroll
-        for (int s = 0; s < NSC; ++s)
-          if (!(fabs(ps[s]) < 1.0e5)) sincos(ps[s], &sps[s], &cps[s]);
+        for (int s = 0; s < NSC; ++s) sincos_q0(ps[s], &sps[s], &cps[s]);
+      } else {
+        bool big = false;
+#pragma unroll
+        for (int s = 0; s < NSC; ++s) {
+          sps[s] = 0.0;
+          cps[s] = 1.0;
+          sincos_nb(ps[s], &sps[s], &cps[s]);
+          big |= !(fabs(ps[s]) < 1.0e5);
+        }
+        if (big) {
+#pragma unroll
+          for (int s = 0; s < NSC; ++s)
+            if (!(fabs(ps[s]) < 1.0e5)) sincos(ps[s], &sps[s], &cps[s]);
+        }
       }
       double gnx[NSC], gny[NSC], vv[NSC];
 #pragma unroll
