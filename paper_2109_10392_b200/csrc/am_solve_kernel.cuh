@@ -881,11 +881,21 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
         }
         double th[NSC];
         bool clip[NSC], anyclip = false;
+        // headings within +-22.5 deg on every valid sample (the common case):
+        // the octant-0 atan2, bit-identical to the full one there
+        bool o0 = true;
+#pragma unroll
+        for (int s = 0; s < NSC; ++s) o0 &= !v[s] || atan2_is_o0(yd[s], xd[s]);
+        if (__all_sync(BMPC_FULL, o0)) {
+#pragma unroll
+          for (int s = 0; s < NSC; ++s) th[s] = atan2_o0(yd[s], xd[s]);
+        } else {
+#pragma unroll
+          for (int s = 0; s < NSC; ++s) th[s] = atan2_nb(yd[s], xd[s]);
+        }
 #pragma unroll
         for (int s = 0; s < NSC; ++s) {
-          th[s] = 0.0;
           clip[s] = false;
-          th[s] = atan2_nb(yd[s], xd[s]);
           double prev = __shfl_up_sync(BMPC_FULL, th[s], 1);
           const double last = __shfl_sync(BMPC_FULL, th[s], 31);
           if (lane == 0) prev = prev_last;

@@ -1047,7 +1047,7 @@ int bmpc_op_tail(int n, int l, int mn, const double* x, const double* y, const d
 
 int bmpc_math_check(int fn, long long n, const double* a, const double* b, double* out,
                     double* out2, void* s) {
-  if (fn < 0 || fn > 5 || !a || !out || (fn == 3 || fn == 4) && !out2)
+  if (fn < 0 || fn > 7 || !a || !out || (fn == 3 || fn == 4 || fn == 7) && !out2)
     return fail(BMPC_EINVAL, "bmpc_math_check: bad argument");
   CK(bmpc::op_math_check(fn, n, a, b, out, out2, S_(s)), "math_check");
   return BMPC_OK;

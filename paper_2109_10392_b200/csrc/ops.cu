@@ -529,6 +529,8 @@ __global__ void k_math_check(int fn, long long n, const double* __restrict__ a,
     case 3: sincos_nb(x, &s, &c); out[e] = s; out2[e] = c; break;
     case 4: sincos(x, &s, &c); out[e] = s; out2[e] = c; break;
     case 5: out[e] = div_nb(x, y); break;
+    case 6: out[e] = atan2_o0(x, y); break;
+    case 7: sincos_q0(x, &s, &c); out[e] = s; out2[e] = c; break;
     default: break;
   }
 }

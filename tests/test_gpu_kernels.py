@@ -134,3 +134,16 @@ def test_device_math(cuda):
     assert ulps(rs, 1.0 / np.sqrt(r2)).max() <= 2.0
     q, _ = run(5, t(y), t(x + 50.0))
     assert ulps(q, y / (x + 50.0)).max() <= 1.0
+    # the sweep's fast paths are bit-identical to the full functions on their domains
+    xo = rng.uniform(1e-3, 40.0, N)
+    yo = rng.uniform(-1.0, 1.0, N) * 0.41421356237309503 * xo
+    yo[:4] = [0.0, -0.0, 0.41421356237309503 * xo[2], -0.41421356237309503 * xo[3]]
+    fast, _ = run(6, t(yo), t(xo))
+    full, _ = run(0, t(yo), t(xo))
+    np.testing.assert_array_equal(fast.view(np.int64), full.view(np.int64))
+    tq = rng.uniform(-0.78, 0.78, N)
+    tq[:4] = [0.0, -0.0, 0.78, -0.78]
+    fs, fc = run(7, t(tq))
+    ns, nc = run(3, t(tq))
+    np.testing.assert_array_equal(fs.view(np.int64), ns.view(np.int64))
+    np.testing.assert_array_equal(fc.view(np.int64), nc.view(np.int64))
