@@ -20,6 +20,8 @@ SHAPES = [  # (n, t_f, degree, m, l, sweeps)
     (150, 7.5, 13, 9, 16, 25),   # npad 224, NB=14 (single-slot obstacle passes)
     (200, 10.0, 15, 40, 12, 25),  # the c4 shape, NB=16
     (256, 8.0, 9, 6, 12, 25),    # npad 256, no leftover
+    (100, 5.0, 10, 0, 20, 30),   # no obstacles (m = 0: no staged predictions)
+    (64, 4.0, 7, 3, 3, 30),      # fewer goals than a block's warps
 ]
 
 
