@@ -7,15 +7,18 @@ the reference; the work runs in one persistent sm_100a kernel per solve
 
 Differences by design (B200 formulation, SURVEY.md finding 8):
 * ``KktSystem`` holds explicit inverses of the two shared KKT matrices instead
-  of LU factors; every QP step applies the inverse and then one refinement
-  step against the matrix, as the reference's LU solve does (without it the
-  explicit inverse drifts 5e-8 relative at the c4 shape).  ``n_factorizations``
-  counts the two inversions, ``n_solves`` two refined solves per AM sweep
-  exactly as the reference's solve_xy/solve_psi calls do.
+  of LU factors (the step API applies them with one refinement step, as the
+  reference's LU solve does).  The persistent solve runs both QPs in
+  null-space form (csrc/capi.cu reduced_qp): the boundary rows fix the end
+  coefficients once per solve and each sweep applies the reduced-Hessian
+  inverse, refined only where that Hessian is ill-conditioned (c4).
+  ``n_factorizations`` counts the two inversions, ``n_solves`` two solves per
+  AM sweep exactly as the reference's solve_xy/solve_psi calls do.
 * the obstacle penalty targets are summed over obstacles before the basis
-  contraction (F_o^T g = P^T sum_j g_j) and the line-of-sight ratios use
-  rsqrt-and-multiply.  Trajectories match the reference to <= 1e-8 relative on
-  every column the reference's own 1-ulp sensitivity screen marks stable.
+  contraction (F_o^T g = P^T sum_j g_j), in exact form (an outside term gives
+  g_j = x, r_j = 0), and the line-of-sight ratios use rsqrt-and-multiply.
+  Trajectories match the reference to <= 1e-8 relative on every column the
+  reference's own 1-ulp sensitivity screen marks stable.
 """
 
 from __future__ import annotations
