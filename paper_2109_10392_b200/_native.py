@@ -85,6 +85,8 @@ EXPORTS = {
                      c_int, POINTER(SolveOut), c_void_p], c_int),
     "bmpc_score": ([c_void_p, POINTER(Problem), c_void_p, c_void_p, c_void_p, c_void_p,
                     POINTER(ScoreSpec), POINTER(ScoreOut), c_void_p], c_int),
+    "bmpc_score_samples": ([POINTER(Problem), c_int] + [c_void_p] * 5 + [POINTER(ScoreSpec),
+                                                                       POINTER(ScoreOut), c_void_p], c_int),
     "bmpc_plan_host_layout": ([c_void_p, c_int, c_int, c_int, POINTER(c_longlong), c_int], c_int),
     "bmpc_plan_host": ([c_void_p, POINTER(Problem), POINTER(SolveOpts), POINTER(SolveOut),
                         POINTER(ScoreSpec), POINTER(ScoreOut), c_void_p], c_int),

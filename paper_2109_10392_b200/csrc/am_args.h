@@ -61,6 +61,10 @@ enum {
   BMPC_F_CARRY = 4,     // write the carried state (for chunked / resumed solves)
   BMPC_F_F32 = 8,       // mixed precision: fp32 obstacle block
   BMPC_F_SCORE = 16,    // fused planner scoring after the last sweep
+  BMPC_F_POLL = 32,     // tol > 0: count finished instances per sweep and exit once an
+                        // earlier sweep is known to be globally converged
+  BMPC_F_TEAM_BUILD = 64,  // run the team instantiation (the one that carries the
+                           // early-exit poll) even with one warp per instance
 };
 
 // Planner scoring parameters and outputs for the fused epilogue.
@@ -93,10 +97,12 @@ typedef struct {
   double* hist;         // [rows][3][L]
   double* res_final;    // [3][L]
   bmpc_fused_score score;  // used with BMPC_F_SCORE
-  // global early stop (solver.py:437-439): notconv[hist_offset + t] is set to 1
-  // by every instance whose worst residual after sweep t is not <= tol
+  // global early stop (solver.py:437-439), one 64-bit word per sweep: its high
+  // half is non-zero once an instance's worst residual after sweep hist_offset
+  // + t is not <= tol; with BMPC_F_POLL its low half counts the instances that
+  // finished that sweep (so a sweep is decided converged at count L, flag 0)
   double tol;
-  int* notconv;
+  unsigned long long* notconv;
   const int* iters_dev;  // non-NULL: sweep count read on the device (0 = nothing to do)
   int team;              // warps per instance (1, 2 or 4)
 } bmpc_solve_args;

@@ -55,7 +55,9 @@ cudaError_t BMPC_CAT(launch_am_nb_, BMPC_INST_NB)(const bmpc_dev_consts& C,
                                                    const bmpc_solve_args& A, int warps,
                                                    cudaStream_t st) {
   const bool f32 = (A.flags & BMPC_F_F32) != 0;
-  if (A.team > 1) {  // teams: the small-batch latency mode, fp64, n <= 128
+  // teams: the small-batch latency mode, fp64, n <= 128; also every polling
+  // (tol > 0) solve of that shape, with teams of one warp if none was asked for
+  if (A.team > 1 || (A.flags & BMPC_F_TEAM_BUILD)) {
     if (f32) return cudaErrorNotSupported;
     switch (C.npad) {
       case 64: return launch_t<BMPC_INST_NB, 2, false, true>(C, A, warps, st);

@@ -818,8 +818,32 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
   BMPC_PROF(0);
 
   // ----------------------------------------------------------- AM sweeps ----
+  // Early exit (tol > 0, first launch of a solve): the team leader's lane 0
+  // reads the word of the earliest sweep it has not yet seen decided at the
+  // top of each sweep and evaluates it near the end (the L2 round trip hides
+  // under the sweep): flag set -> that sweep is not converged, look at the
+  // next one; flag clear with all L instances counted -> that sweep is
+  // globally converged, so every later sweep is wasted work (the host-side
+  // re-run redoes exactly that many sweeps, solver.py:437-439).
+  // The word travels by an asynchronous 16-byte copy (cp.async.cg: L2, no L1
+  // staleness) into a shared slot, so no register is held across the sweep.
+  // Nothing of it stays in registers across the sweep (the kernel sits at the
+  // register cap): the flag is re-read from the launch parameters, the sweep
+  // index to look at lives in a shared slot next to the word.  Only the team
+  // instantiation carries it (the host routes polling solves there, with one
+  // warp per instance when no team is asked for): compiled into the
+  // throughput kernels even unused it costs them ~1.5%.
+  __shared__ __align__(16) unsigned long long s_poll[BMPC_MAX_WARPS][2];
+  __shared__ int s_poll_next[BMPC_MAX_WARPS];
+#define BMPC_POLL (TEAMS && (A.flags & BMPC_F_POLL) != 0)  // the host sets it only with notconv
+  if (BMPC_POLL && lane == 0) s_poll_next[warp] = 0;
   for (int t = 0; t < iters; ++t) {
     const bool last = t == iters - 1;
+    if (BMPC_POLL && wt == 0 && lane == 0 && t > 0) {
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(&s_poll[warp][0]);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n\tcp.async.commit_group;"
+                   ::"r"(sa), "l"(A.notconv + (s_poll_next[warp] & ~1)) : "memory");
+    }
     // (1) xy QP (solver.py:302-312) in null-space form: c = cb + Z (rho G +
     //     lambda), lane i / 16+i coefficient i of x / y.  Ill-conditioned
     //     shapes add one refinement step; it starts from the previous sweep's
@@ -1181,6 +1205,25 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
       sqn = warp_sum(sqn);
     }
     __syncwarp();
+    bool stop = false;
+    if (BMPC_POLL) {
+      int dec = 0;  // 1: sweep s_poll_next not converged, 2: converged -> exit
+      if (wt == 0 && lane == 0) {
+        if (t > 0) {
+          asm volatile("cp.async.wait_all;" ::: "memory");
+          const int nx = s_poll_next[warp];
+          const unsigned long long w = s_poll[warp][nx & 1];
+          if ((w >> 32) != 0ull) {
+            dec = 1;
+            s_poll_next[warp] = nx + 1;
+          } else if ((unsigned)w == (unsigned)L) {
+            dec = 2;
+          }
+        }
+        if (TW > 1) xch[68] = dec == 2 ? 1.0 : 0.0;  // every sweep; read after the team barrier
+      }
+      stop = __shfl_sync(BMPC_FULL, dec, 0) == 2;
+    }
     if (TW > 1) {  // team: sum the warps' partials in a fixed order
       if (owner) xch[32 + lane] = gn;
       if constexpr (kSqCols) {
@@ -1191,6 +1234,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
         xch[66] = sqn;
       }
       team_sync();
+      if (BMPC_POLL) stop = xch_of(0)[68] != 0.0;  // the leader's decision, team-uniform
       gn = 0.0;
       sqo = sqa = sqn = 0.0;
       for (int w = 0; w < TW; ++w) {
@@ -1232,9 +1276,14 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
       // root stays off the sweep's critical path
       const bool ok = A.tol > 0.0 ? sqrt(sqv) <= A.tol : (A.tol == 0.0 && sqv <= 0.0);
       const bool nc = __any_sync(BMPC_FULL, is_sq_lane && !ok);
-      // a plain store: the flag only ever goes 0 -> 1, and a read-before-write
-      // would stall the warp on a coherent L2 round trip every sweep
-      if (lane == 0 && nc) A.notconv[A.hist_offset + t] = 1;
+      // a plain store into the high half: the flag only ever goes 0 -> 1, and a
+      // read-before-write would stall the warp on a coherent L2 round trip every
+      // sweep; polling solves count instead (a reduction, nothing waits on it)
+      unsigned long long* w = A.notconv + A.hist_offset + t;
+      if (lane == 0) {
+        if (BMPC_POLL) atomicAdd(w, nc ? 0x100000001ull : 1ull);
+        else if (nc) reinterpret_cast<int*>(w)[1] = 1;
+      }
     }
     if (is_sq_lane && wt == 0 && ((A.flags & BMPC_F_HISTORY) || last)) {
       const double res = sqrt(sqv);
@@ -1246,6 +1295,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
     }
     have_sol = true;
     BMPC_PROF(7);
+    if (stop) return;  // an earlier sweep converged everywhere: the re-run takes over
   }
 
   // ------------------------------------------------- fused planner scoring ----

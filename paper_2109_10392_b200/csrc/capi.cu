@@ -14,6 +14,7 @@
 
 #include "../../include/batchmpc_b200.h"
 #include "am_args.h"
+#include "score.cuh"
 
 namespace bmpc {
 cudaError_t launch_am_solve(const bmpc_dev_consts& C, const bmpc_solve_args& A, int warps,
@@ -49,12 +50,16 @@ cudaError_t op_sample(int n, int npad, int nb, int L, const double* PT, const do
                       cudaStream_t st);
 using ScoreArgs = bmpc_score_args;
 cudaError_t op_score(const ScoreArgs& S, cudaStream_t st);
+cudaError_t op_score_samples(const ScoreParams& sp, int l, int L, const double* xi2, const double* x,
+                             const double* y, const double* psi, const double* v, const double* res,
+                             double* meta, double* min_ratio, double* heading_max, uint8_t* flags,
+                             cudaStream_t st);
 cudaError_t op_argmin(int S, int l, const double* meta, const uint8_t* flags, long long* best,
                       long long* best_all, long long* best_hc, long long* nfeas, cudaStream_t st);
 cudaError_t op_pack_xi(long long total, const double* xi_x, const double* xi_y, double* out,
                        cudaStream_t st, double* scaled = nullptr, double a = 1.0, double b = 1.0,
                        int* zero = nullptr, int nzero = 0);
-cudaError_t op_early_stop(int max_iter, const int* notconv, int* rerun, int* status, int* status2,
+cudaError_t op_early_stop(int max_iter, const unsigned long long* notconv, int* rerun, int* status, int* status2,
                           cudaStream_t st);
 cudaError_t op_assemble(int S, int V, int m, int n, int l, const double* veh, const int* nveh,
                         const double* ego, const double* goals, const double* rel, double* xi_x,
@@ -438,8 +443,9 @@ static int auto_warps(const bmpc_ctx* ctx, int L, int req, int team) {
 static int launch_sweeps(bmpc_ctx* ctx, const bmpc_problem* p, const double* xi2,
                          const bmpc_solve_opts* o, int iters, int init_mode, int hist_offset,
                          double* carry, int write_carry, bmpc_solve_out* out, cudaStream_t st,
-                         const bmpc_fused_score* fsc = nullptr, int* notconv = nullptr,
-                         const int* iters_dev = nullptr) {
+                         const bmpc_fused_score* fsc = nullptr,
+                         unsigned long long* notconv = nullptr, const int* iters_dev = nullptr,
+                         int extra_flags = 0) {
   const int L = p->S * p->l;
   bmpc_solve_args A;
   memset(&A, 0, sizeof(A));
@@ -450,7 +456,7 @@ static int launch_sweeps(bmpc_ctx* ctx, const bmpc_problem* p, const double* xi2
   A.iters = iters;
   A.init_mode = init_mode;
   A.flags = (out->history ? BMPC_F_HISTORY : 0) | ((o->want_v && out->v) ? BMPC_F_V : 0) |
-            (write_carry ? BMPC_F_CARRY : 0) | (o->precision == 1 ? BMPC_F_F32 : 0);
+            (write_carry ? BMPC_F_CARRY : 0) | (o->precision == 1 ? BMPC_F_F32 : 0) | extra_flags;
   A.hist_offset = hist_offset;
   A.a = p->a;
   A.b = p->b;
@@ -615,19 +621,27 @@ static int solve_impl(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opt
   const int M = o->max_iter;
   int status[2] = {M, 0};
   // One workspace: the packed predictions (raw pairs, then the ellipse-frame
-  // pairs of the sweeps' outside test) and the scratch ints -- [0, M) the
-  // per-sweep not-converged flags, [M] the re-run sweep count, [M + 1, M + 2]
-  // {iterations, converged}.  k_pack_xi zeroes the flags (no memset call).
+  // pairs of the sweeps' outside test) and the scratch -- M 64-bit per-sweep
+  // early-stop words (not-converged flag | finished-instance count), then
+  // ints: [0] the re-run sweep count, [1, 2] {iterations, converged}.
+  // k_pack_xi zeroes the words (no memset call).
   const size_t xi_bytes = (size_t)tot * 4 * sizeof(double);
   char* wsp = nullptr;
-  CK(cudaMallocAsync(&wsp, xi_bytes + (size_t)(M + 4) * sizeof(int), st), "cudaMallocAsync");
+  CK(cudaMallocAsync(&wsp, xi_bytes + (size_t)M * 8 + 4 * sizeof(int), st), "cudaMallocAsync");
   double* xi2 = tot > 0 ? reinterpret_cast<double*>(wsp) : nullptr;
-  int* scr = L > 0 ? reinterpret_cast<int*>(wsp + xi_bytes) : nullptr;
+  unsigned long long* words = L > 0 ? reinterpret_cast<unsigned long long*>(wsp + xi_bytes) : nullptr;
+  int* scr = L > 0 ? reinterpret_cast<int*>(wsp + xi_bytes + (size_t)M * 8) : nullptr;
   if (tot > 0 || L > 0)
     CK(bmpc::op_pack_xi(tot, p->xi_x, p->xi_y, xi2, st, xi2 ? xi2 + 2 * tot : nullptr, p->a, p->b,
-                        scr, scr ? M : 0),
+                        reinterpret_cast<int*>(words), words ? 2 * M : 0),
        "pack_xi");
-  rc = launch_sweeps(ctx, p, xi2, o, M, mode, 0, nullptr, 0, out, st, fsc, scr);
+  // tol > 0 (fp64, n <= 128: the team instantiation's shapes): the first launch
+  // exits once some sweep is known to be globally converged (BMPC_F_POLL), so
+  // a solve that converges at sweep t costs about t + (t + 1) sweeps instead of
+  // max_iter + (t + 1).  The re-run uses the same instantiation, without polling.
+  const int tb = (o->tol > 0.0 && o->precision == 0 && ctx->C.npad <= 128) ? BMPC_F_TEAM_BUILD : 0;
+  const int poll = tb ? BMPC_F_POLL : 0;
+  rc = launch_sweeps(ctx, p, xi2, o, M, mode, 0, nullptr, 0, out, st, fsc, words, nullptr, tb | poll);
   if (!rc && L > 0) {
     // Global early stop (solver.py:437-439): the first sweep whose worst
     // residual over every instance is <= tol.  When it is not the last one the
@@ -635,12 +649,12 @@ static int solve_impl(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opt
     // deterministic, so the re-run reproduces the same iterates).  The decision
     // and the re-run launch stay on the device -- the second launch exits at
     // once when there is nothing to redo -- so nothing waits on the host.
-    CK(bmpc::op_early_stop(M, scr, scr + M, scr + M + 1, o->status_dev, st), "early_stop");
-    rc = launch_sweeps(ctx, p, xi2, o, M, mode, 0, nullptr, 0, out, st, fsc, scr, scr + M);
+    CK(bmpc::op_early_stop(M, words, scr, scr + 1, o->status_dev, st), "early_stop");
+    rc = launch_sweeps(ctx, p, xi2, o, M, mode, 0, nullptr, 0, out, st, fsc, words, scr, tb);
   }
   if (!rc && post) rc = post_solve(post, st);
   if (!rc && L > 0 && !o->status_dev)
-    CK(cudaMemcpyAsync(status, scr + M + 1, sizeof(status), cudaMemcpyDeviceToHost, st), "memcpy");
+    CK(cudaMemcpyAsync(status, scr + 1, sizeof(status), cudaMemcpyDeviceToHost, st), "memcpy");
   cudaFreeAsync(wsp, st);
   if (rc) return rc;
   CK(cudaGetLastError(), "bmpc_solve");
@@ -709,6 +723,38 @@ int bmpc_score(bmpc_ctx* ctx, const bmpc_problem* p, const double* c_x, const do
   if (!S.meta || !S.min_ratio || !S.heading_max || !S.flags)
     return fail(BMPC_EINVAL, "bmpc_score: per-instance outputs required");
   CK(bmpc::op_score(S, st), "score");
+  if (out->best_index && out->argmin_all && out->argmin_hc && out->n_feasible)
+    CK(bmpc::op_argmin(p->S, p->l, out->meta_cost, out->flags, out->best_index, out->argmin_all,
+                       out->argmin_hc, out->n_feasible, st),
+       "argmin");
+  if (xi2) cudaFreeAsync(xi2, st);
+  return BMPC_OK;
+}
+
+int bmpc_score_samples(const bmpc_problem* p, int n, const double* x, const double* y,
+                       const double* psi, const double* v, const double* res,
+                       const bmpc_score_spec* spec, bmpc_score_out* out, void* stream) {
+  if (!p || !spec || !out || n < 1 || p->S < 0 || p->l < 0 || p->m < 0)
+    return fail(BMPC_EINVAL, "bmpc_score_samples: bad argument");
+  if (spec->kind != 0 && spec->kind != 1) return fail(BMPC_EINVAL, "unknown meta-cost kind");
+  const int L = p->S * p->l;
+  if (L > 0 && (!x || !y || !psi || !v)) return fail(BMPC_EINVAL, "bmpc_score_samples: null samples");
+  if (L > 0 && (!out->meta_cost || !out->min_ratio || !out->heading_max || !out->flags))
+    return fail(BMPC_EINVAL, "bmpc_score_samples: per-instance outputs required");
+  cudaStream_t st = S_(stream);
+  const long long tot = (long long)p->S * p->m * n;
+  if (tot > 0 && (!p->xi_x || !p->xi_y)) return fail(BMPC_EINVAL, "bmpc_score_samples: null predictions");
+  double* xi2 = nullptr;
+  if (tot > 0) {
+    CK(cudaMallocAsync(&xi2, tot * 2 * sizeof(double), st), "cudaMallocAsync");
+    CK(bmpc::op_pack_xi(tot, p->xi_x, p->xi_y, xi2, st), "pack_xi");
+  }
+  const bmpc::ScoreParams sp{n, p->m, spec->kind, p->a, p->b, spec->v_cruise, spec->v_max,
+                             spec->y_rl, spec->w1, spec->w2, spec->heading_limit,
+                             spec->residual_tol, 1.0 - spec->collision_margin};
+  CK(bmpc::op_score_samples(sp, p->l, L, xi2, x, y, psi, v, res, out->meta_cost, out->min_ratio,
+                            out->heading_max, out->flags, st),
+     "score_samples");
   if (out->best_index && out->argmin_all && out->argmin_hc && out->n_feasible)
     CK(bmpc::op_argmin(p->S, p->l, out->meta_cost, out->flags, out->best_index, out->argmin_all,
                        out->argmin_hc, out->n_feasible, st),

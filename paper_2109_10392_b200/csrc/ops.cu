@@ -300,6 +300,38 @@ __global__ void k_score(const ScoreArgs S) {
   }
 }
 
+// Warp per instance: the same scoring from already-sampled (n, L) arrays --
+// the reference-API filter_candidates / rank, which read a RankedPlan's own
+// x, y, psi, v (planner.py:219-257).  res: (3, L) block residuals, or null
+// (the residual filter bit is then never set).
+__global__ void k_score_samples(const ScoreParams sp, int l, int L, const double2* __restrict__ xi,
+                                const double* __restrict__ x, const double* __restrict__ y,
+                                const double* __restrict__ psi, const double* __restrict__ v,
+                                const double* __restrict__ res, double* meta, double* min_ratio,
+                                double* heading_max, uint8_t* flags) {
+  const int inst = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (inst >= L) return;
+  const double2* q = xi + (size_t)(inst / l) * sp.m * sp.n;
+  auto sample = [&](int k, double& sx, double& sy, double& sv, double& sps) {
+    const size_t e = (size_t)k * L + inst;
+    sx = x[e];
+    sy = y[e];
+    sv = v[e];
+    sps = psi[e];
+  };
+  const double r0 = res ? res[inst] : NAN, r1 = res ? res[(size_t)L + inst] : NAN,
+               r2 = res ? res[2 * (size_t)L + inst] : NAN;
+  double cost, rmin, hmax;
+  unsigned char f;
+  score_samples(sp, q, sample, r0, r1, r2, cost, rmin, hmax, f);
+  if ((threadIdx.x & 31) == 0) {
+    meta[inst] = cost;
+    min_ratio[inst] = rmin;
+    heading_max[inst] = hmax;
+    flags[inst] = f;
+  }
+}
+
 // ------------------------------------------------------------------ argmin --
 // One block per scene: numpy argmin semantics (first minimum; NaN wins) over
 // where(mask, cost, inf) for three masks; -1 encodes "None".
@@ -463,6 +495,17 @@ cudaError_t op_score(const ScoreArgs& S, cudaStream_t st) {
   k_score<<<(S.L + warps - 1) / warps, warps * 32, 0, st>>>(S);
   return cudaGetLastError();
 }
+cudaError_t op_score_samples(const ScoreParams& sp, int l, int L, const double* xi2, const double* x,
+                             const double* y, const double* psi, const double* v, const double* res,
+                             double* meta, double* min_ratio, double* heading_max, uint8_t* flags,
+                             cudaStream_t st) {
+  if (L <= 0) return cudaSuccess;
+  const int warps = 8;
+  k_score_samples<<<(L + warps - 1) / warps, warps * 32, 0, st>>>(
+      sp, l, L, reinterpret_cast<const double2*>(xi2), x, y, psi, v, res, meta, min_ratio,
+      heading_max, flags);
+  return cudaGetLastError();
+}
 cudaError_t op_argmin(int S, int l, const double* meta, const uint8_t* flags, long long* best,
                       long long* best_all, long long* best_hc, long long* nfeas, cudaStream_t st) {
   if (S > 0) k_argmin<<<S, 256, 0, st>>>(l, meta, flags, best, best_all, best_hc, nfeas);
@@ -480,12 +523,12 @@ cudaError_t op_pack_xi(long long total, const double* xi_x, const double* xi_y, 
 // Early-stop decision in one launch (solver.py:437-439): t* = the first sweep no
 // instance flagged as not converged; re-run t* + 1 sweeps unless that is all
 // of them (0 = no re-run); {iterations, converged} into status (and status2).
-__global__ void k_early_stop(int max_iter, const int* __restrict__ notconv, int* rerun, int* status,
-                             int* status2) {
+__global__ void k_early_stop(int max_iter, const unsigned long long* __restrict__ notconv, int* rerun,
+                             int* status, int* status2) {
   __shared__ int wbest[8];
   int best = 0x7f7f7f7f;
   for (int t = threadIdx.x; t < max_iter; t += blockDim.x)
-    if (notconv[t] == 0) best = min(best, t);
+    if ((notconv[t] >> 32) == 0ull) best = min(best, t);
   for (int o = 16; o >= 1; o >>= 1) best = min(best, __shfl_xor_sync(BMPC_FULL, best, o));
   if ((threadIdx.x & 31) == 0) wbest[threadIdx.x >> 5] = best;
   __syncthreads();
@@ -502,7 +545,7 @@ __global__ void k_early_stop(int max_iter, const int* __restrict__ notconv, int*
   }
 }
 
-cudaError_t op_early_stop(int max_iter, const int* notconv, int* rerun, int* status, int* status2,
+cudaError_t op_early_stop(int max_iter, const unsigned long long* notconv, int* rerun, int* status, int* status2,
                           cudaStream_t st) {
   k_early_stop<<<1, 256, 0, st>>>(max_iter, notconv, rerun, status, status2);
   return cudaGetLastError();

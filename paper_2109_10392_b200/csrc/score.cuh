@@ -20,21 +20,20 @@ struct ScoreParams {
 };
 
 // Warp-cooperative: lane handles samples k = lane, lane+32, ...; `sample(k, x,
-// y, xd, yd, psi)` evaluates the basis at k.  Returns (on every lane) the meta
-// cost, min ratio, max |psi| and the filter bits (bit0 heading, bit1
+// y, v, psi)` provides sample k (v = |(xdot, ydot)|).  Returns (on every lane)
+// the meta cost, min ratio, max |psi| and the filter bits (bit0 heading, bit1
 // residual, bit2 collision) given the instance's final block residuals.
 template <class SampleFn>
-__device__ __forceinline__ void score_instance(const ScoreParams& S, const double2* __restrict__ xi,
-                                               SampleFn sample, double r0, double r1, double r2,
-                                               double& cost_out, double& rmin_out,
-                                               double& hmax_out, unsigned char& flags_out) {
+__device__ __forceinline__ void score_samples(const ScoreParams& S, const double2* __restrict__ xi,
+                                              SampleFn sample, double r0, double r1, double r2,
+                                              double& cost_out, double& rmin_out,
+                                              double& hmax_out, unsigned char& flags_out) {
   const int lane = threadIdx.x & 31;
   double hmax = 0.0, rmin = INFINITY, cost = 0.0;
   bool any_nan = false;
   for (int k = lane; k < S.n; k += 32) {
-    double x, y, xd, yd, ps;
-    sample(k, x, y, xd, yd, ps);
-    const double v = __dsqrt_rn(__dadd_rn(__dmul_rn(xd, xd), __dmul_rn(yd, yd)));
+    double x, y, v, ps;
+    sample(k, x, y, v, ps);
     const double ah = fabs(ps);
     if (ah != ah) any_nan = true;
     hmax = fmax(hmax, ah);
@@ -69,6 +68,21 @@ __device__ __forceinline__ void score_instance(const ScoreParams& S, const doubl
   rmin_out = rmin;
   hmax_out = hmax;
   flags_out = f;
+}
+
+// As score_samples, with `sample(k, x, y, xd, yd, psi)` evaluating the basis:
+// v = sqrt(xd^2 + yd^2) unclipped (planner.py:412-423).
+template <class SampleFn>
+__device__ __forceinline__ void score_instance(const ScoreParams& S, const double2* __restrict__ xi,
+                                               SampleFn sample, double r0, double r1, double r2,
+                                               double& cost_out, double& rmin_out,
+                                               double& hmax_out, unsigned char& flags_out) {
+  auto sv = [&](int k, double& x, double& y, double& v, double& ps) {
+    double xd, yd;
+    sample(k, x, y, xd, yd, ps);
+    v = __dsqrt_rn(__dadd_rn(__dmul_rn(xd, xd), __dmul_rn(yd, yd)));
+  };
+  score_samples(S, xi, sv, r0, r1, r2, cost_out, rmin_out, hmax_out, flags_out);
 }
 
 }  // namespace bmpc

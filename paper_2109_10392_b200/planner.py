@@ -156,14 +156,12 @@ def collision_ratios(x, y, xi_x, xi_y, a, b):
     return r.cpu().numpy() if host else r
 
 
-def _score_plan(plan: RankedPlan, batch: ProblemBatch, limits: FilterLimits,
-                spec: MetaCostSpec | None):
-    import torch
-
+def _score_fused(plan: RankedPlan, batch: ProblemBatch, limits: FilterLimits,
+                 spec: MetaCostSpec | None):
+    """Scoring straight from the device coefficients a Planner solve left in
+    ``plan._dev`` (bmpc_score: the fused sampling + filters + meta cost)."""
     from . import device as D
 
-    if plan._dev is None:
-        raise ValueError("RankedPlan was not produced by Planner.sample_plan of this package")
     dv = plan._dev
     solver: BatchSolver = dv["solver"]
     ctx = solver._context()
@@ -171,44 +169,91 @@ def _score_plan(plan: RankedPlan, batch: ProblemBatch, limits: FilterLimits,
     if prob is None:
         prob = solver.device_problem(batch)
         dv["prob"] = prob
-    L = prob.L
-    sc = D.alloc_score(L, prob.S, prob.b_xy.device)
+    sc = D.alloc_score(prob.L, prob.S, prob.b_xy.device)
     nat.check(nat.load().bmpc_score(ctx, ctypes.byref(prob.c_struct()), D.ptr(dv["c_x"]),
                                     D.ptr(dv["c_y"]), D.ptr(dv["c_psi"]), D.ptr(dv["res"]),
                                     ctypes.byref(_spec_struct(spec, limits)), ctypes.byref(D.score_struct(sc)),
                                     ctypes.c_void_p(D.stream_ptr())), "score")
-    del torch
+    return sc
+
+
+def _score_samples(plan: RankedPlan, xi_x, xi_y, a: float, b: float, limits: FilterLimits,
+                   spec: MetaCostSpec | None, with_residuals: bool):
+    """Scoring of the plan's OWN sampled arrays (x, y, psi, v and, for the
+    filters, plan.residuals) on the device (bmpc_score_samples): whatever the
+    caller put in the RankedPlan is what gets filtered and ranked, as in the
+    reference (planner.py:219-257)."""
+    import torch
+
+    from . import device as D
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    up = lambda t: torch.from_numpy(np.ascontiguousarray(t, dtype=np.float64)).to(dev)  # noqa: E731
+    n, l = plan.x.shape
+    xi_x, xi_y = np.asarray(xi_x, dtype=np.float64).ravel(), np.asarray(xi_y, dtype=np.float64).ravel()
+    if xi_x.size % n or xi_x.shape != xi_y.shape:
+        raise ValueError("obstacle predictions must have m*n entries")
+    gx, gy = up(xi_x), up(xi_y)
+    res = None
+    if with_residuals:
+        r = plan.residuals
+        res = up(np.stack([np.asarray(r.r_obs), np.asarray(r.r_acc), np.asarray(r.r_nonhol)]))
+    arrs = [up(t) for t in (plan.x, plan.y, plan.psi, plan.v)]
+    sc = D.alloc_score(l, 1, dev)
+    prob = nat.Problem(xi_x.size // n, l, 1, gx.data_ptr(), gy.data_ptr(), None, None, float(a), float(b),
+                       0.0, 0.0, 0.0)
+    nat.check(nat.load().bmpc_score_samples(ctypes.byref(prob), n, *[t.data_ptr() for t in arrs],
+                                            D.ptr(res), ctypes.byref(_spec_struct(spec, limits)),
+                                            ctypes.byref(D.score_struct(sc)),
+                                            ctypes.c_void_p(D.stream_ptr())), "score_samples")
     return sc
 
 
 def filter_candidates(plan: RankedPlan, batch: ProblemBatch, limits: FilterLimits) -> np.ndarray:
-    """Heading, residual and recomputed-collision filters (planner.py:233-245)."""
-    sc = _score_plan(plan, batch, limits, None)
-    flags = sc.flags.cpu().numpy()
+    """Heading, residual and recomputed-collision filters (planner.py:233-245),
+    evaluated on the plan's own x, y, psi and residuals."""
+    sc = _score_samples(plan, batch.xi_x, batch.xi_y, batch.a, batch.b, limits, None, True)
     plan.heading_max = sc.heading_max.cpu().numpy()
     plan.min_ratio = sc.min_ratio.cpu().numpy() if batch.xi_x.size else np.full(plan.l, np.inf)
-    plan.feasible = flags == 7
-    plan._dev["limits"] = limits
+    plan.feasible = sc.flags.cpu().numpy() == 7
     return plan.feasible
 
 
+def _select(feasible, meta_cost) -> int | None:
+    """The reference's selection rule (planner.py:252-256): argmin of the meta
+    cost over the feasible candidates, lowest index on ties, None when nothing
+    is feasible (numpy argmin: a NaN cost wins)."""
+    if feasible is None:
+        return None
+    feasible = np.asarray(feasible, dtype=bool)
+    if not feasible.any():
+        return None
+    return int(np.argmin(np.where(feasible, meta_cost, np.inf)))
+
+
 def rank(plan: RankedPlan, spec: MetaCostSpec) -> RankedPlan:
-    """Meta cost of every candidate and the cheapest feasible one (planner.py:248-257)."""
-    limits = plan._dev.get("limits", FilterLimits()) if plan._dev else FilterLimits()
-    batch = plan._dev.get("batch") if plan._dev else None
-    sc = _score_plan(plan, batch, limits, spec)
+    """Meta cost of every candidate from the plan's own v and y (planner.py:
+    210-216, on the device) and the cheapest candidate plan.feasible marks
+    (planner.py:248-257)."""
+    n, l = plan.x.shape
+    sc = _score_samples(plan, np.zeros(0), np.zeros(0), 1.0, 1.0, FilterLimits(), spec, False)
     plan.meta_cost = sc.meta_cost.cpu().numpy()
-    if plan.feasible is None:
-        plan.best_index = None
-    else:
-        feas = plan.feasible
-        if not feas.any():
-            plan.best_index = None
-        else:
-            # device argmin over the mask the caller's filter produced
-            b = int(sc.best_index.cpu().numpy()[0])
-            plan.best_index = b if b >= 0 else None
+    plan.best_index = _select(plan.feasible, plan.meta_cost)
     return plan
+
+
+def _filter_and_rank_fused(plan: RankedPlan, batch: ProblemBatch, limits: FilterLimits,
+                           spec: MetaCostSpec) -> None:
+    """filter_candidates + rank for a plan this package just sampled from its
+    own device solve (the MPC cycle): one fused scoring launch on the device
+    coefficients, the same bits as the two reference-API calls on the sampled
+    arrays."""
+    sc = _score_fused(plan, batch, limits, spec)
+    plan.heading_max = sc.heading_max.cpu().numpy()
+    plan.min_ratio = sc.min_ratio.cpu().numpy() if batch.xi_x.size else np.full(plan.l, np.inf)
+    plan.feasible = sc.flags.cpu().numpy() == 7
+    plan.meta_cost = sc.meta_cost.cpu().numpy()
+    plan.best_index = _select(plan.feasible, plan.meta_cost)
 
 
 @dataclass(frozen=True)
@@ -474,8 +519,7 @@ class Planner:
         history = [Residuals(r_obs=h[0].copy(), r_acc=h[1].copy(), r_nonhol=h[2].copy()) for h in hist]
         info = SolveInfo(residual_history=history, iterations=sol.iterations, converged=sol.converged)
         plan = self._sample_plan_device(sol.c_x, sol.c_y, sol.c_psi, goals, history[-1], batch)
-        filter_candidates(plan, batch, c.limits)
-        rank(plan, self.meta)
+        _filter_and_rank_fused(plan, batch, c.limits, self.meta)
         self._prev = (sol, plan.residuals)
         if plan.best_index is None:
             command, fallback = self.fallback_command(ego), True

@@ -25,6 +25,7 @@ from __future__ import annotations
 
 import ctypes
 import dataclasses
+from collections.abc import Sequence
 from dataclasses import dataclass
 
 import numpy as np
@@ -64,9 +65,85 @@ class ProblemBatch:
             raise ValueError("boundary vectors must have one column per instance")
 
 
+class _Deferred:
+    """An AmState field that still lives on the device: materialised on the host
+    the first time it is read (solver.py:440-450 builds alpha, d, alpha_a, d_a
+    eagerly; at c3/c4 batch sizes those (m*n, L) arrays are gigabytes, so here
+    they are only built when someone looks)."""
+
+    __slots__ = ("shape", "_src", "_name")
+
+    def __init__(self, src, name, shape):
+        self._src, self._name, self.shape = src, name, tuple(shape)
+
+    def device(self):
+        return self._src.device(self._name)
+
+    def host(self) -> np.ndarray:
+        return self.device().cpu().numpy()
+
+
+class _LazyAux:
+    """Device source of the deferred AmState fields of one solve: v from the
+    last sweep, and alpha, d, alpha_a, d_a re-derived from the final
+    coefficients with the closed forms (obstacle_update per scene,
+    accel_update), computed together on first use."""
+
+    def __init__(self, solver, sol, prob):
+        self.solver, self.sol, self.prob = solver, sol, prob
+        self._t = None
+
+    def device(self, name):
+        if name == "v":
+            return self.sol.v
+        if self._t is None:
+            import torch
+
+            from . import kernels
+
+            smp = self.solver.sample_device(self.sol, which=("x", "y", "xddot", "yddot"))
+            p = self.prob
+            n = self.solver.basis.grid.n
+            alpha = torch.empty(p.m * n, p.L, dtype=torch.float64, device=p.b_xy.device)
+            d = torch.empty_like(alpha)
+            for sc in range(p.S):
+                cols = slice(sc * p.l, (sc + 1) * p.l)
+                alpha[:, cols], d[:, cols] = kernels.obstacle_update(
+                    smp["x"][:, cols], smp["y"][:, cols], p.xi_x[sc], p.xi_y[sc], p.a, p.b)
+            alpha_a, d_a = kernels.accel_update(smp["xddot"], smp["yddot"], p.a_max)
+            self._t = dict(alpha=alpha, d=d, alpha_a=alpha_a, d_a=d_a)
+        return self._t[name]
+
+
+class _History(Sequence):
+    """SolveInfo.residual_history: one Residuals per sweep, read from the
+    device history on first access (the list the reference builds eagerly,
+    solver.py:432-436)."""
+
+    def __init__(self, dev_hist, iterations):
+        self._dev, self._n, self._rows = dev_hist, iterations, None
+
+    def _load(self):
+        if self._rows is None:
+            h = self._dev[: self._n].cpu().numpy()
+            self._rows = [Residuals(r_obs=r[0].copy(), r_acc=r[1].copy(), r_nonhol=r[2].copy()) for r in h]
+            self._dev = None
+        return self._rows
+
+    def __len__(self):
+        return self._n
+
+    def __getitem__(self, i):
+        return self._load()[i]
+
+    def __repr__(self):
+        return repr(self._load())
+
+
 @dataclass
 class AmState:
-    """All per-instance iterates (solver.py:62-94)."""
+    """All per-instance iterates (solver.py:62-94).  Fields a solve leaves on the
+    device (v, alpha, d, alpha_a, d_a) are materialised on first read."""
 
     c_x: np.ndarray
     c_y: np.ndarray
@@ -81,17 +158,28 @@ class AmState:
     lambda_psi: np.ndarray
     iteration: int = 0
 
+    def __getattribute__(self, name):
+        v = object.__getattribute__(self, name)
+        if type(v) is _Deferred:
+            v = v.host()
+            object.__setattr__(self, name, v)
+        return v
+
+    def _raw(self, name):
+        """The field without materialising it (ndarray or _Deferred)."""
+        return object.__getattribute__(self, name)
+
     def copy(self) -> "AmState":
         vals = {}
         for f in dataclasses.fields(self):
-            v = getattr(self, f.name)
-            vals[f.name] = v.copy() if isinstance(v, np.ndarray) else v
+            v = self._raw(f.name)
+            vals[f.name] = v.copy() if isinstance(v, np.ndarray) else v  # a _Deferred is shared
         return AmState(**vals)
 
     def shapes_match(self, other: "AmState") -> bool:
         for f in dataclasses.fields(self):
-            v = getattr(self, f.name)
-            if isinstance(v, np.ndarray) and v.shape != getattr(other, f.name).shape:
+            v = self._raw(f.name)
+            if isinstance(v, (np.ndarray, _Deferred)) and v.shape != other._raw(f.name).shape:
                 return False
         return True
 
@@ -113,10 +201,22 @@ class Residuals:
 
 @dataclass
 class SolveInfo:
-    residual_history: list[Residuals]
+    residual_history: Sequence[Residuals]
     iterations: int
     converged: bool
     iterates: list[tuple[np.ndarray, np.ndarray, np.ndarray]] | None = None
+
+
+def _default_boundary(spec) -> bool:
+    """True when ``spec`` pins the default derivative orders.  Compared field by
+    field, so a BoundarySpec of the reference's own ``batchmpc.basis`` (another
+    class; dataclass equality is per class) is accepted too."""
+    d = BoundarySpec()
+    keys = ("start_orders", "end_orders", "psi_start_orders", "psi_end_orders")
+    try:
+        return all(tuple(getattr(spec, k)) == getattr(d, k) for k in keys)
+    except AttributeError:
+        return False
 
 
 def _precision_code(precision: str) -> int:
@@ -216,7 +316,7 @@ class BatchSolver:
     def __init__(self, basis: BasisSet, mats: ConstantMatrices, rho_xy: float = 1.0):
         if mats.basis is not basis:
             raise ValueError("constant matrices were built from a different basis")
-        if mats.boundary != BoundarySpec():
+        if not _default_boundary(mats.boundary):
             raise ValueError("the device path supports the default BoundarySpec only")
         if not 6 <= basis.n_b <= 16:
             raise ValueError(f"basis size {basis.n_b} outside the supported 6..16")
@@ -400,32 +500,76 @@ class BatchSolver:
               keep_multipliers: bool = False) -> tuple[AmState, SolveInfo]:
         """Run the alternating minimization until every instance's worst residual
         is <= tol or max_iter sweeps ran (solver.py:414-456).  Host arrays in,
-        host arrays out; the returned AmState is complete (alpha/d/alpha_a/d_a
-        materialised as the reference does at the end of a solve)."""
+        host arrays out.
+
+        ``batch`` is a ProblemBatch (one scene, as in the reference) or a stacked
+        scene batch (scenes.SceneBatch: xi_x/xi_y (S, m*n), b_xy (12, S*l),
+        b_psi (4, S*l); instance s*l + i is goal i of scene s).  The returned
+        AmState's coefficients and multipliers are host arrays; v, alpha, d,
+        alpha_a and d_a stay on the device until first read (the reference
+        materialises them at the end of every solve, solver.py:440-450), and the
+        residual history is read back on first access."""
         import torch
 
         if max_iter < 1:
             raise ValueError(f"max_iter must be >= 1, got {max_iter}")
-        self._check_batch(batch)
-        prob = self.device_problem(batch)
+        prob = self._problem(batch)
         dev = prob.b_xy.device
         wd = None
         if warm is not None:
-            if not warm.shapes_match(self._zero_state(batch)):
+            if not warm.shapes_match(self._zero_shapes(prob)):
                 raise ValueError("warm state shapes do not match the batch")
-            wd = {k: torch.from_numpy(np.ascontiguousarray(getattr(warm, k), dtype=np.float64)).to(dev)
-                  for k in ("alpha", "d", "alpha_a", "d_a", "v", "c_psi",
-                            "lambda_x", "lambda_y", "lambda_psi")}
+            wd = {}
+            for k in ("alpha", "d", "alpha_a", "d_a", "v", "c_psi", "lambda_x", "lambda_y", "lambda_psi"):
+                raw = warm._raw(k)
+                wd[k] = (raw.device().contiguous() if isinstance(raw, _Deferred) else
+                         torch.from_numpy(np.ascontiguousarray(raw, dtype=np.float64)).to(dev))
         iterates = None
         if record_iterates:
             sol, iterates = self._solve_stepwise(prob, max_iter, tol, wd, keep_multipliers)
         else:
             sol = self.solve_device(prob, max_iter, tol, wd, keep_multipliers)
-        state = self._materialize(sol, prob, batch)
-        hist = sol.history[: sol.iterations].cpu().numpy()
-        history = [Residuals(r_obs=h[0].copy(), r_acc=h[1].copy(), r_nonhol=h[2].copy()) for h in hist]
-        return state, SolveInfo(residual_history=history, iterations=sol.iterations,
-                                converged=sol.converged, iterates=iterates)
+        aux = _LazyAux(self, sol, prob)
+        n, L, mn = self.basis.grid.n, prob.L, prob.m * self.basis.grid.n
+        h = lambda t: t.cpu().numpy()  # noqa: E731
+        state = AmState(c_x=h(sol.c_x), c_y=h(sol.c_y), c_psi=h(sol.c_psi),
+                        alpha=_Deferred(aux, "alpha", (mn, L)), d=_Deferred(aux, "d", (mn, L)),
+                        alpha_a=_Deferred(aux, "alpha_a", (n, L)), d_a=_Deferred(aux, "d_a", (n, L)),
+                        v=_Deferred(aux, "v", (n, L)), lambda_x=h(sol.l_x), lambda_y=h(sol.l_y),
+                        lambda_psi=h(sol.l_psi), iteration=sol.iterations)
+        return state, SolveInfo(residual_history=_History(sol.history, sol.iterations),
+                                iterations=sol.iterations, converged=sol.converged, iterates=iterates)
+
+    def _problem(self, batch):
+        """Validated DeviceProblem of a ProblemBatch or a stacked scene batch."""
+        if isinstance(batch, ProblemBatch):
+            self._check_batch(batch)
+            return self.device_problem(batch)
+        from .device import DeviceProblem
+
+        n, mn = self.basis.grid.n, self.mats.rows_obs
+        S, l = int(batch.S), int(batch.l)
+        xi_x, xi_y = np.atleast_2d(batch.xi_x), np.atleast_2d(batch.xi_y)
+        if xi_x.shape != (S, mn) or xi_y.shape != (S, mn):
+            raise ValueError(f"expected obstacle predictions of shape ({S}, {mn}), got {xi_x.shape}")
+        if np.shape(batch.b_xy) != (self.mats.A.shape[0], S * l):
+            raise ValueError(f"b_xy must have shape ({self.mats.A.shape[0]}, {S * l})")
+        if np.shape(batch.b_psi) != (self.mats.A_psi.shape[0], S * l):
+            raise ValueError(f"b_psi must have shape ({self.mats.A_psi.shape[0]}, {S * l})")
+        if getattr(batch, "rho", self.rho_xy) != self.rho_xy:
+            raise ValueError("batch rho differs from the rho the KKT inverses were built with")
+        ProblemBatch(l=S * l, xi_x=xi_x[0], xi_y=xi_y[0], a=batch.a, b=batch.b, v_min=batch.v_min,
+                     v_max=batch.v_max, a_max=batch.a_max, b_xy=batch.b_xy, b_psi=batch.b_psi)
+        return DeviceProblem.from_host(n, xi_x, xi_y, batch.b_xy, batch.b_psi, l, batch.a, batch.b,
+                                       batch.v_min, batch.v_max, batch.a_max)
+
+    def _zero_shapes(self, prob) -> AmState:
+        """Shape-only AmState of a problem (no allocation)."""
+        nb, n, L, mn = self.basis.n_b, self.basis.grid.n, prob.L, prob.m * self.basis.grid.n
+        z = lambda *sh: _Deferred(None, "", sh)  # noqa: E731
+        return AmState(c_x=z(nb, L), c_y=z(nb, L), c_psi=z(nb, L), alpha=z(mn, L), d=z(mn, L),
+                       alpha_a=z(n, L), d_a=z(n, L), v=z(n, L), lambda_x=z(nb, L), lambda_y=z(nb, L),
+                       lambda_psi=z(nb, L))
 
     def _solve_stepwise(self, prob, max_iter, tol, wd, keep_multipliers):
         """One launch per sweep through the carried-state API, so every
@@ -464,19 +608,6 @@ class BatchSolver:
         sol.iterations, sol.converged = it, converged
         self.kkt.n_solves += 2 * it
         return sol, iterates
-
-    def _materialize(self, sol, prob, batch) -> AmState:
-        """Complete AmState on the host (solver.py:440-450)."""
-        from . import kernels
-
-        smp = self.sample_device(sol, which=("x", "y", "xddot", "yddot"))
-        alpha, d = kernels.obstacle_update(smp["x"], smp["y"], prob.xi_x[0], prob.xi_y[0],
-                                           batch.a, batch.b)
-        alpha_a, d_a = kernels.accel_update(smp["xddot"], smp["yddot"], batch.a_max)
-        h = lambda t: t.cpu().numpy()  # noqa: E731
-        return AmState(c_x=h(sol.c_x), c_y=h(sol.c_y), c_psi=h(sol.c_psi), alpha=h(alpha), d=h(d),
-                       alpha_a=h(alpha_a), d_a=h(d_a), v=h(sol.v), lambda_x=h(sol.l_x),
-                       lambda_y=h(sol.l_y), lambda_psi=h(sol.l_psi), iteration=sol.iterations)
 
     # -- step-wise API (solver.py:288-410) --------------------------------------
     # The same math as the fused sweep, one reference step at a time, on host
@@ -646,6 +777,34 @@ class BatchSolver:
         th = self._heading(dc(state.c_x), dc(state.c_y))
         psi = self._samples(state, ("psi",))["psi"]
         state.lambda_psi = state.lambda_psi - rho * self._project(psi - th, 1, 0).cpu().numpy()
+
+    def _iterate(self, state: AmState, batch: ProblemBatch, g_x, g_y):
+        """One full sweep on a host AmState through the device step operators
+        (solver.py:458-500): xy QP, sampling, unwrap(atan2) heading target, psi
+        QP, the fused tail (d, d_a, v, residual vectors, next targets) and the
+        multiplier steps.  ``g_x``/``g_y`` are the incoming targets (as
+        ``_g_parts`` returns them, device arrays); returns (Residuals, next
+        g_x, next g_y).  The persistent kernel fuses all of this for solve()."""
+        from . import kernels
+
+        self._apply_xy(state, batch, g_x, g_y)
+        d = self._dev
+        cx, cy = d(state.c_x), d(state.c_y)
+        s = self._samples(state, ("x", "y", "xdot", "ydot", "xddot", "yddot"))
+        theta = self._heading(cx, cy)
+        self._apply_psi(state, batch, theta)
+        psi = self._samples(state, ("psi",))["psi"]
+        (dd, d_a, v, r_x, r_y, g_x2, g_y2, sq_obs, sq_acc, sq_nonhol) = kernels.tail_core(
+            s["x"], s["y"], s["xdot"], s["ydot"], s["xddot"], s["yddot"], psi, d(batch.xi_x),
+            d(batch.xi_y), batch.v_min, batch.v_max, batch.a_max, batch.a, batch.b)
+        state.d, state.d_a, state.v = dd.cpu().numpy(), d_a.cpu().numpy(), v.cpu().numpy()
+        m, rho = self.mats.m, batch.rho_xy
+        state.lambda_x = state.lambda_x - rho * self._project(r_x, 0, m).cpu().numpy()
+        state.lambda_y = state.lambda_y - rho * self._project(r_y, 0, m).cpu().numpy()
+        state.lambda_psi = state.lambda_psi - rho * self._project(psi - theta, 1, 0).cpu().numpy()
+        state.iteration += 1
+        h = lambda t: np.sqrt(t.cpu().numpy())  # noqa: E731
+        return Residuals(r_obs=h(sq_obs), r_acc=h(sq_acc), r_nonhol=h(sq_nonhol)), g_x2, g_y2
 
     def compute_residuals(self, state: AmState, batch: ProblemBatch) -> Residuals:
         """Block L2 norms of the residual vectors (solver.py:392-410)."""

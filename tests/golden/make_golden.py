@@ -20,6 +20,18 @@ Fixtures (float64 unless noted):
   c4s.npz         2 scenes x 32 goals of the c4 generator (n=200, n_b=16, m=50), 100 sweeps
   reverse.npz     goals behind a reversing ego: headings cross +-pi so the
                   np.unwrap corrections are non-zero (40 sweeps)
+  c2s.npz         1 scene x 256 goals of the c2 generator (m=30, x~U(-50,200)),
+                  200 sweeps -- the one BASELINE config at 200 sweeps
+  c2f.npz, c3f.npz, c4f.npz  scenes of the c3 / c4 generators with FEASIBLE candidates,
+                  so best_index is a real index on both sides (seeds found by
+                  tests/golden/seed_search.py); each holds every feasible column
+                  of its scene (c2f: of a 1024-goal batch) plus the lowest-index
+                  other columns up to l
+  mpc_kat.npz     also stores, per cycle, the set of best indices the reference
+                  itself picks when the same solve (same batch, same warm state)
+                  is re-run with its columns permuted or one column at a time:
+                  the evidence that the reference's pick inside a tie class is
+                  a column-position (BLAS rounding) artefact
 """
 
 from __future__ import annotations
@@ -226,6 +238,95 @@ def reverse_case():
     workload_fixture("reverse", W, 40, screen=True)
 
 
+def _permuted(obj, perm):
+    """Copy of a reference ProblemBatch / AmState with its columns permuted."""
+    import dataclasses
+
+    vals = {}
+    for f in dataclasses.fields(obj):
+        v = getattr(obj, f.name)
+        vals[f.name] = np.ascontiguousarray(v[:, perm]) if isinstance(v, np.ndarray) and v.ndim == 2 else v
+    if "l" in vals:
+        vals["l"] = len(perm)
+    return type(obj)(**vals)
+
+
+def _ref_best(planner, batch, warm, perm, max_iter, tol):
+    """The reference's own solve + sample_plan/filter/rank on the permuted
+    columns; returns the best index in the ORIGINAL column numbering."""
+    st, info = planner.solver.solve(_permuted(batch, perm), max_iter=max_iter, tol=tol,
+                                    warm=None if warm is None else _permuted(warm, perm),
+                                    keep_multipliers=True)
+    plan = planner.sample_plan(st, [None] * len(perm), info.residual_history[-1])
+    filter_candidates(plan, _permuted(batch, perm), planner.cfg.limits)
+    rank(plan, planner.meta)
+    return None if plan.best_index is None else int(np.asarray(perm)[plan.best_index])
+
+
+def _ref_best_sequential(planner, batch, warm, max_iter, tol):
+    """Column-at-a-time reference solves (l = 1 batches) under the batch's
+    global tol rule: all columns run the same sweep count as the batch solve
+    would, so each is solved for that count with tol disabled."""
+    from batchmpc.solver import Residuals
+
+    full_st, full_info = planner.solver.solve(batch, max_iter=max_iter, tol=tol, warm=warm,
+                                              keep_multipliers=True)
+    iters = full_info.iterations
+    cols = []
+    for i in range(batch.l):
+        st, info = planner.solver.solve(_permuted(batch, [i]), max_iter=iters, tol=-1.0,
+                                        warm=None if warm is None else _permuted(warm, [i]),
+                                        keep_multipliers=True)
+        cols.append((st, info.residual_history[-1]))
+    cat = lambda k: np.concatenate([getattr(c[0], k) for c in cols], axis=1)  # noqa: E731
+    st = full_st
+    st.c_x, st.c_y, st.c_psi = cat("c_x"), cat("c_y"), cat("c_psi")
+    res = Residuals(*(np.concatenate([getattr(c[1], k) for c in cols]) for k in ("r_obs", "r_acc", "r_nonhol")))
+    plan = planner.sample_plan(st, [None] * batch.l, res)
+    filter_candidates(plan, batch, planner.cfg.limits)
+    rank(plan, planner.meta)
+    return None if plan.best_index is None else int(plan.best_index)
+
+
+class SequentialSolver:
+    """The reference's BatchSolver run one column at a time (l = 1 batches, the
+    reference's own batch-vs-sequential oracle, oracles.py:270-293), keeping the
+    batch's global tol rule: every column is solved with tol disabled, the first
+    sweep t at which the max over all columns is <= tol is found from the
+    per-column histories, and the columns are re-solved for exactly t sweeps.
+    Column arithmetic then never depends on a column's position in the batch."""
+
+    def __init__(self, ref):
+        self.ref = ref
+        self.basis, self.mats, self.kkt = ref.basis, ref.mats, ref.kkt
+
+    def __getattr__(self, k):
+        return getattr(self.ref, k)
+
+    def solve(self, batch, max_iter=150, tol=1e-3, warm=None, record_iterates=False,
+              keep_multipliers=False):
+        from batchmpc.solver import Residuals, SolveInfo
+
+        def run(i, iters):
+            return self.ref.solve(_permuted(batch, [i]), max_iter=iters, tol=-1.0,
+                                  warm=None if warm is None else _permuted(warm, [i]),
+                                  keep_multipliers=keep_multipliers)
+
+        cols = [run(i, max_iter) for i in range(batch.l)]
+        worst = np.max([[h.max_per_instance()[0] for h in info.residual_history] for _, info in cols], axis=0)
+        hit = np.nonzero(worst <= tol)[0]
+        iters = int(hit[0]) + 1 if hit.size else max_iter
+        if iters != max_iter:
+            cols = [run(i, iters) for i in range(batch.l)]
+        st = cols[0][0].copy()
+        for f in ("c_x", "c_y", "c_psi", "alpha", "d", "alpha_a", "d_a", "v", "lambda_x", "lambda_y",
+                  "lambda_psi"):
+            setattr(st, f, np.concatenate([getattr(c[0], f) for c in cols], axis=1))
+        hist = [Residuals(*(np.concatenate([getattr(c[1].residual_history[t], k) for c in cols])
+                            for k in ("r_obs", "r_acc", "r_nonhol"))) for t in range(iters)]
+        return st, SolveInfo(residual_history=hist, iterations=iters, converged=bool(hit.size))
+
+
 def mpc_kat(cycles: int = 3):
     """Closed-loop cruise_idm replay (seed 7, l=11, warm starts, tol=1e-3,
     200 sweeps) through the reference's own harness objects, full precision.
@@ -245,6 +346,18 @@ def mpc_kat(cycles: int = 3):
     ego = EgoState(x=cfg.ego_x, y=float(lanes.centers[cfg.ego_lane]), psi=0.0, psidot=0.0,
                    vx=cfg.ego_v, vy=0.0, ax=0.0, ay=0.0)
     kat = [json.loads(s) for s in open("/root/reference/pkg/frontend/testdata/run.jsonl")][1:]
+    seen = {}
+    solve0 = planner.solver.solve
+
+    def spy(batch, max_iter=150, tol=1e-3, warm=None, record_iterates=False, keep_multipliers=False):
+        seen["batch"] = batch
+        seen["warm"] = None if warm is None else warm.copy()
+        return solve0(batch, max_iter=max_iter, tol=tol, warm=warm, record_iterates=record_iterates,
+                      keep_multipliers=keep_multipliers)
+
+    planner.solver.solve = spy
+    seq_planner = Planner(pc, lanes, cfg.meta_spec)
+    seq_planner.solver = SequentialSolver(seq_planner.solver)
     out = dict(l=pc.l, n=pc.n, t_f=pc.t_f, degree=pc.degree, rho=pc.rho_xy, max_iter=pc.max_iter,
                tol=pc.tol, m=pc.m, a=pc.a, b=pc.b, v_min=pc.v_min, v_max=pc.v_max, a_max=pc.a_max,
                h=pc.h, dt_cycle=pc.dt_cycle, warm_residual_cap=pc.warm_residual_cap,
@@ -257,6 +370,7 @@ def mpc_kat(cycles: int = 3):
         states = world.states()
         res = planner.mpc_cycle(ego, states)
         plan = res.plan
+        sres = seq_planner.mpc_cycle(ego, states)
         hist = np.stack([[r.r_obs, r.r_acc, r.r_nonhol] for r in res.info.residual_history])
         # the reference's own recorded run (rounded by its log writer) must agree
         rec = kat[c]
@@ -276,6 +390,25 @@ def mpc_kat(cycles: int = 3):
         out[p + "iterations"] = np.int64(res.info.iterations)
         out[p + "converged"] = np.int64(res.info.converged)
         out[p + "history"] = hist
+        # the same closed loop with column-independent reference arithmetic
+        out[p + "seq_best_index"] = np.int64(-1 if sres.plan.best_index is None else sres.plan.best_index)
+        out[p + "seq_meta_cost"] = sres.plan.meta_cost
+        out[p + "seq_feasible"] = sres.plan.feasible.astype(np.uint8)
+        out[p + "seq_iterations"] = np.int64(sres.info.iterations)
+        out[p + "seq_command"] = np.array([sres.command.accel, sres.command.steering])
+        print(f"cycle {c}: sequential-arithmetic reference best {sres.plan.best_index}")
+        # the reference's pick under column permutations / sequential solves
+        planner.solver.solve = solve0
+        b, w, l = seen["batch"], seen["warm"], seen["batch"].l
+        prng = np.random.default_rng(100 + c)
+        perms = [np.arange(l), np.arange(l)[::-1]] + [np.roll(np.arange(l), k) for k in range(1, l)]
+        perms += [prng.permutation(l) for _ in range(8)]
+        picks = {_ref_best(planner, b, w, pm, pc.max_iter, pc.tol) for pm in perms}
+        picks.add(_ref_best_sequential(planner, b, w, pc.max_iter, pc.tol))
+        assert plan.best_index in picks
+        out[p + "ref_best_set"] = np.array(sorted(-1 if q is None else q for q in picks), dtype=np.int64)
+        print(f"cycle {c}: reference best {plan.best_index}, picks under permutation {sorted(picks, key=str)}")
+        planner.solver.solve = spy
         for k in ("x", "y", "psi", "psidot", "v"):
             out[p + k] = getattr(plan, k)
         ego = H._apply_command(ego, res.command, cfg.dt, cfg.h)
@@ -285,8 +418,46 @@ def mpc_kat(cycles: int = 3):
     print("mpc_kat", cycles, "cycles; matches testdata/run.jsonl")
 
 
+def subset_fixture(name, cfg_name, seeds, l, iters, l_full=None):
+    """Scenes with feasible candidates: each seed's full goal batch is solved by
+    the reference, then the fixture keeps every feasible column plus the
+    lowest-index others up to l and is re-solved (and screened) on that subset."""
+    from paper_2109_10392_b200.scenes import CONFIGS, make_workload
+
+    cfg = CONFIGS[cfg_name]
+    parts = []
+    for seed in seeds:
+        Wf = make_workload(cfg_name, scenes=1, l=l_full, seed0=seed)
+        solver = ref_solver(Wf.n, Wf.t_f, Wf.degree, Wf.m)
+        batch = ProblemBatch(l=Wf.l, xi_x=Wf.xi_x[0], xi_y=Wf.xi_y[0], a=Wf.a, b=Wf.b, v_min=Wf.v_min,
+                             v_max=Wf.v_max, a_max=Wf.a_max, b_xy=Wf.b_xy, b_psi=Wf.b_psi)
+        st, info = solver.solve(batch, max_iter=cfg.iters, tol=0.0)
+        sc = score(solver, st, info, batch, MetaCostSpec("cruise", v_cruise=20.0))
+        feas = list(np.nonzero(sc["feasible"])[0])
+        assert feas, f"{cfg_name} seed {seed} has no feasible candidate"
+        others = [i for i in range(Wf.l) if i not in feas][: max(0, l - len(feas))]
+        cols = np.array(sorted(feas[:l] + others))
+        parts.append((Wf, cols))
+    W = make_workload(cfg_name, scenes=len(seeds), l=l, seed0=0)
+    for s, (Wf, cols) in enumerate(parts):
+        W.xi_x[s], W.xi_y[s] = Wf.xi_x[0], Wf.xi_y[0]
+        W.b_xy[:, s * l:(s + 1) * l] = Wf.b_xy[:, cols]
+        W.b_psi[:, s * l:(s + 1) * l] = Wf.b_psi[:, cols]
+
+    def check(o, info):
+        assert o["cruise_best_index"] >= 0
+
+    workload_fixture(name, W, iters, extra=check)
+
+
 def main():
     t = time.time()
+    only = set(sys.argv[1:])
+    if only:
+        for f in only:
+            FIXTURES[f]()
+        print(f"done in {time.time() - t:.1f}s")
+        return
     mpc_kat()
     tail_case()
     demo()
@@ -295,8 +466,23 @@ def main():
     workload_fixture("c3s", make_workload("c3", scenes=4, l=64), 100)
     workload_fixture("c4s", make_workload("c4", scenes=2, l=32), 100)
     reverse_case()
+    for f in ("c2s", "c2f", "c3f", "c4f"):
+        FIXTURES[f]()
     print(f"done in {time.time() - t:.1f}s; reference version {batchmpc.__version__}")
 
+
+FIXTURES = {
+    "mpc_kat": mpc_kat,
+    "tail_case": tail_case,
+    "demo": demo,
+    "reverse": reverse_case,
+    "c2s": lambda: workload_fixture("c2s", make_workload("c2", l=256), 200),
+    "c2f": lambda: subset_fixture("c2f", "c2", [4], 256, 200, l_full=1024),
+    # seeds and l chosen from tests/golden/seed_search.py output
+    "c3f": lambda: subset_fixture("c3f", "c3", [2, 4, 6, 10], 64, 100),
+    "c4f": lambda: subset_fixture("c4f", "c4", C4F_SEEDS, 32, 100),
+}
+C4F_SEEDS = [2, 10]
 
 if __name__ == "__main__":
     main()

@@ -54,7 +54,13 @@ def _plan(z, kind="cruise"):
     return solver, res
 
 
-@pytest.mark.parametrize("name", ["c0", "c1", "c3s", "c4s", "reverse"])
+PARITY = ["c0", "c1", "c2s", "c2f", "c3s", "c3f", "c4s", "c4f", "reverse"]
+# fixtures whose every scene has a feasible candidate: best_index is a real
+# index on both sides (c2f / c3f / c4f, tests/golden/seed_search.py)
+FEASIBLE = ["c2f", "c3f", "c4f"]
+
+
+@pytest.mark.parametrize("name", PARITY)
 def test_solve_and_score_parity(cuda, name):
     z = golden(name)
     solver, res = _plan(z)
@@ -77,13 +83,15 @@ def test_solve_and_score_parity(cuda, name):
     np.testing.assert_allclose(res.min_ratio[stable], z["cruise_min_ratio"][stable], rtol=1e-8)
     np.testing.assert_allclose(res.heading_max[stable], z["cruise_heading_max"][stable], rtol=1e-7,
                                atol=1e-12)
+    if name in FEASIBLE:
+        assert all(b is not None for b in res.best_index), res.best_index
     del l
 
 
 FP32_TOL = 1e-5  # measured: see DESIGN.md (fp32 mode)
 
 
-@pytest.mark.parametrize("name", ["c0", "c1", "c3s", "c4s"])
+@pytest.mark.parametrize("name", ["c0", "c1", "c2f", "c3s", "c3f", "c4s", "c4f"])
 def test_fp32_mode_tolerance(cuda, name):
     """Mixed-precision mode (fp32 obstacle block) against the reference: the
     stated tolerance on stable columns; reported, not bit-compatible."""
@@ -100,10 +108,12 @@ def test_fp32_mode_tolerance(cuda, name):
     assert err[stable].max() <= FP32_TOL
 
 
-@pytest.mark.parametrize("name", ["c0", "c3s"])
+@pytest.mark.parametrize("name", ["c0", "c2f", "c3s", "c3f", "c4f"])
 def test_highspeed_scoring_parity(cuda, name):
     z = golden(name)
     _, res = _plan(z, "highspeed")
+    if name in FEASIBLE:
+        assert all(b is not None for b in res.best_index)
     for s in range(int(z["S"])):
         assert (res.best_index[s] if res.best_index[s] is not None else -1) == int(z["highspeed_best_index"][s])
         assert int(res.argmin_all[s]) == int(z["highspeed_argmin_all"][s])
@@ -498,3 +508,77 @@ def test_plan_host_pinned_inputs_read_in_place(cuda):
     for k in ("c_x", "c_y", "c_psi", "res_final", "meta_cost", "min_ratio", "heading_max", "flags"):
         assert np.array_equal(getattr(a, k), getattr(b, k)), k
     assert a.best_index == b.best_index
+
+
+@pytest.mark.parametrize("team", [1, 4])
+def test_tol_early_exit(cuda, team):
+    """tol > 0: the first launch exits once some sweep is globally converged
+    (BMPC_F_POLL), the re-run reproduces exactly t* sweeps (solver.py:437-439).
+    Same bits as a fixed t*-sweep solve, and far cheaper than max_iter sweeps."""
+    import time
+
+    z = golden("demo")
+    solver = _solver(z)
+    b = _batch(z)
+    prob = solver.device_problem(b)
+    ref = solver.solve_device(prob, max_iter=60, tol=0.0, team_warps=team)
+    worst = ref.history[:60].amax(dim=(1, 2)).cpu().numpy()
+    tol = float(worst[20]) * (1 + 1e-9)
+    expect = int(np.argmax(worst <= tol)) + 1
+    got = solver.solve_device(prob, max_iter=3000, tol=tol, team_warps=team)
+    assert got.converged and got.iterations == expect
+    exact = solver.solve_device(prob, max_iter=expect, tol=0.0, team_warps=team)
+    for k in ("c_x", "c_y", "c_psi", "l_x", "l_y", "l_psi", "res_final"):
+        assert cuda.equal(getattr(got, k), getattr(exact, k)), k
+    assert cuda.equal(got.history[:expect], exact.history[:expect])
+
+    def timed(max_iter, t):
+        cuda.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(3):
+            solver.solve_device(prob, max_iter=max_iter, tol=t, team_warps=team)
+        cuda.cuda.synchronize()
+        return (time.perf_counter() - t0) / 3
+
+    timed(3000, tol)
+    t_tol, t_full = timed(3000, tol), timed(3000, 0.0)
+    print(f"team {team}: converged at {expect}; tol solve {1e3 * t_tol:.2f} ms vs 3000 sweeps {1e3 * t_full:.2f} ms")
+    assert t_tol < 0.2 * t_full
+
+
+def test_solve_stacked_scenes_lazy_state(cuda):
+    """BatchSolver.solve on a stacked scene batch (the c3/c4 form): v, alpha, d,
+    alpha_a, d_a stay on the device until read, the history is read back on
+    first access; results equal plan_batch and per-scene solves bit for bit,
+    and a lazy state warm-starts the next solve without a host round trip."""
+    from paper_2109_10392_b200.planner import plan_batch
+
+    z = golden("c3s")
+    solver = _solver(z)
+    S = _Scenes(z)
+    state, info = solver.solve(S, max_iter=50, tol=0.0)
+    for k in ("v", "alpha", "d", "alpha_a", "d_a"):
+        assert type(state._raw(k)).__name__ == "_Deferred", k
+    assert state._raw("alpha").shape == (int(z["m"]) * int(z["n"]), S.S * S.l)
+    pb = plan_batch(solver, S, max_iter=50, tol=0.0)
+    np.testing.assert_array_equal(state.c_x, pb.c_x)
+    np.testing.assert_array_equal(state.c_psi, pb.c_psi)
+    assert len(info.residual_history) == 50
+    last = info.residual_history[-1]
+    np.testing.assert_array_equal(np.stack([last.r_obs, last.r_acc, last.r_nonhol]), pb.res_final)
+    l = S.l
+    one, _ = solver.solve(_batch(z, s=2), max_iter=50, tol=0.0)
+    cols = slice(2 * l, 3 * l)
+    for k in ("c_x", "lambda_y", "v", "alpha", "d", "alpha_a", "d_a"):
+        np.testing.assert_array_equal(getattr(one, k), getattr(state, k)[:, cols], err_msg=k)
+    # warm start from a lazy state (device fields used in place) == from host arrays
+    state2, _ = solver.solve(S, max_iter=50, tol=0.0)
+    w_lazy, _ = solver.solve(S, max_iter=7, tol=0.0, warm=state2, keep_multipliers=True)
+    host = state2.copy()
+    for k in ("v", "alpha", "d", "alpha_a", "d_a"):
+        getattr(host, k)  # materialise
+    w_host, _ = solver.solve(S, max_iter=7, tol=0.0, warm=host, keep_multipliers=True)
+    np.testing.assert_array_equal(w_lazy.c_x, w_host.c_x)
+    np.testing.assert_array_equal(w_lazy.lambda_psi, w_host.lambda_psi)
+    with pytest.raises(ValueError):
+        solver.solve(_batch(z, s=0), max_iter=3, warm=state2)  # L columns vs l

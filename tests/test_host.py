@@ -217,3 +217,45 @@ def test_null_space_qp_matches_kkt_solve(n, t_f, deg, m, rng):
     bad = np.zeros(((nb + 6) * (nb + 6)))
     assert lib.bmpc_reduced_qp(nb, 6, _native.c_double_ptr(bad), _native.c_double_ptr(np.zeros((nb, nb))),
                                _native.c_double_ptr(np.zeros((nb, 6))), ctypes.byref(ctypes.c_double())) != 0
+
+
+REF_SRC = Path("/root/reference/pkg/src")
+
+
+def test_solver_accepts_foreign_boundary_spec():
+    """The solver swap of INTEGRATION.md passes the reference's own basis and
+    constant-matrix objects: a BoundarySpec of another class with the default
+    orders is accepted, non-default orders are refused."""
+    import dataclasses
+
+    @dataclasses.dataclass(frozen=True)
+    class OtherSpec:
+        start_orders: tuple = (0, 1, 2)
+        end_orders: tuple = (0, 1, 2)
+        psi_start_orders: tuple = (0, 1)
+        psi_end_orders: tuple = (0, 1)
+
+    b = build_basis(build_time_grid(0.0, 5.0, 100), 10)
+    mats = build_constant_matrices(b, 10)
+    BatchSolver(b, dataclasses.replace(mats, boundary=OtherSpec()))
+    with pytest.raises(ValueError, match="BoundarySpec"):
+        BatchSolver(b, dataclasses.replace(mats, boundary=OtherSpec(end_orders=(0, 1))))
+
+
+@pytest.mark.skipif(not REF_SRC.exists(), reason="reference tree not present (GPU box)")
+def test_solver_from_reference_basis_and_matrices():
+    """BatchSolver(ref_basis, ref_mats): built from the reference's batchmpc.basis
+    objects, with KKT matrices bitwise equal to ours."""
+    import sys
+
+    sys.path.insert(0, str(REF_SRC))
+    try:
+        import batchmpc.basis as RB
+    finally:
+        sys.path.remove(str(REF_SRC))
+    rb = RB.build_basis(RB.build_time_grid(0.0, 5.0, 100), 10)
+    rm = RB.build_constant_matrices(rb, 10)
+    s = BatchSolver(rb, rm, 1.0)
+    ours = make_solver(100, 5.0, 10, 10)
+    np.testing.assert_array_equal(s.kkt.matrix_xy, ours.kkt.matrix_xy)
+    np.testing.assert_array_equal(s.kkt.matrix_psi, ours.kkt.matrix_psi)

@@ -52,7 +52,7 @@ def _oracle_solve(z, s=0, kernel="c", iters=None):
     return osol, r, cols
 
 
-@pytest.mark.parametrize("name", ["demo", "c0", "reverse"])
+@pytest.mark.parametrize("name", ["demo", "c0", "reverse", "c2f"])
 def test_oracle_solver_matches_reference(name):
     z = golden(name)
     _, r, cols = _oracle_solve(z)
@@ -62,15 +62,21 @@ def test_oracle_solver_matches_reference(name):
         assert np.abs(r[k] - ref).max() <= 1e-12 * scale, k
 
 
-def test_oracle_scoring_matches_reference():
-    z = golden("c0")
-    osol, r, _ = _oracle_solve(z)
-    sc = osol.score(r, z["xi_x"][0], z["xi_y"][0], float(z["a"]), float(z["b"]), kind="cruise",
+@pytest.mark.parametrize("name,s", [("c0", 0), ("c3f", 0), ("c3f", 2)])
+def test_oracle_scoring_matches_reference(name, s):
+    """Scene s of a golden: the oracle's solve + scoring reproduce the
+    reference's meta costs, feasibility and indices (c3f: real best indices)."""
+    z = golden(name)
+    osol, r, cols = _oracle_solve(z, s=s)
+    sc = osol.score(r, z["xi_x"][s], z["xi_y"][s], float(z["a"]), float(z["b"]), kind="cruise",
                     v_cruise=20.0)
-    np.testing.assert_allclose(sc["meta_cost"], z["cruise_meta_cost"], rtol=1e-12)
-    np.testing.assert_array_equal(sc["feasible"], z["cruise_feasible"].astype(bool))
-    assert sc["best_index"] == int(z["cruise_best_index"][0])
-    assert sc["argmin_all"] == int(z["cruise_argmin_all"][0])
+    np.testing.assert_allclose(sc["meta_cost"], z["cruise_meta_cost"][cols], rtol=1e-12)
+    np.testing.assert_array_equal(sc["feasible"], z["cruise_feasible"][cols].astype(bool))
+    best = int(z["cruise_best_index"][s])
+    assert (sc["best_index"] if sc["best_index"] is not None else -1) == best
+    assert sc["argmin_all"] == int(z["cruise_argmin_all"][s])
+    if name == "c3f":
+        assert best >= 0
 
 
 def test_oracle_demo_history_and_aux():
