@@ -13,9 +13,11 @@ tol=0 as the reference's bench-kernels uses) + fused scoring/argmin.
 * roofline: algorithmic fp64 work of the persistent AM kernel
   (W(n,m,nb) slots per instance per sweep; 2 flops per
   slot) / its CUDA-event duration, against the DFMA peak measured live.
-Multi-GPU (torchrun): weak scaling, each rank solves its own contiguous block
-of l goal columns of one shared scene; the per-shard winners are all-gathered
-(the only collective) to form the global argmin.
+Multi-GPU (torchrun): --scaling weak (default; each rank a whole config: its
+own block of l goal columns of one shared scene, or its own scenes) or strong
+(the BASELINE config split over the ranks as dist.plan_sharded does); the
+shards' results are all-gathered inside the timed step (the only collective),
+and e2e runs dist.plan_sharded.
 --impl reference: the CPU oracle port of the reference (oracle/am_oracle.py +
 oracle/am_oracle.c, the reference's algorithm op for op) on all host cores.
 """
@@ -112,19 +114,31 @@ def _coll_device(dev):
 
 
 # ------------------------------------------------------------- workloads ----
-def make_step_workload(cfg_name: str, world: int, rank: int):
+def make_step_workload(cfg_name: str, world: int, rank: int, scaling: str = "weak"):
+    """(config, this rank's SceneBatch, global column offset, the full job).
+
+    weak: every rank a whole config's worth -- one scene of world*l goals with
+    rank owning a contiguous block of l columns, or its own set of scenes;
+    strong: the BASELINE config itself split over the ranks -- contiguous goal
+    columns of its one scene (c1/c2) or contiguous scene blocks (c3/c4),
+    exactly as dist.plan_sharded partitions it."""
+    from paper_2109_10392_b200.dist import shard_range
     from paper_2109_10392_b200.scenes import CONFIGS, make_workload
 
     cfg = CONFIGS[cfg_name]
+    if scaling == "strong":
+        full = make_workload(cfg_name)
+        if cfg.scenes == 1:
+            lo, hi = shard_range(cfg.l, rank, world)
+            return cfg, full.columns(lo, hi), lo, full
+        lo, hi = shard_range(cfg.scenes, rank, world)
+        return cfg, full.scenes(lo, hi), 0, full
     if cfg.scenes == 1:
         # one scene, world * l goals; rank owns a contiguous block of l columns
-        W = make_workload(cfg_name, l=cfg.l * world)
-        W = W.columns(rank * cfg.l, (rank + 1) * cfg.l)
-        offset = rank * cfg.l
-    else:
-        W = make_workload(cfg_name, seed0=rank * cfg.scenes)
-        offset = 0
-    return cfg, W, offset
+        full = make_workload(cfg_name, l=cfg.l * world)
+        return cfg, full.columns(rank * cfg.l, (rank + 1) * cfg.l), rank * cfg.l, full
+    W = make_workload(cfg_name, seed0=rank * cfg.scenes)
+    return cfg, W, 0, None
 
 
 # ------------------------------------------------------------ CPU oracle ----
@@ -196,7 +210,7 @@ def run_ours(args, rank, world, local_rank):
     local_rank = local_rank % max(1, torch.cuda.device_count())  # see main(): gloo smoke test
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    cfg, W, offset = make_step_workload(args.config, world, rank)
+    cfg, W, offset, full = make_step_workload(args.config, world, rank, args.scaling)
     iters = args.iters or cfg.iters
     solver = make_solver(W.n, W.t_f, W.degree, W.m)
     ctx = solver._context()
@@ -225,12 +239,43 @@ def run_ours(args, rank, world, local_rank):
     # exits at once when there is none), argmin
     launches_per_step = 5
 
+    # N > 1: the step ends with the shards' result exchange (dist.plan_sharded's
+    # collective, here on device tensors so nothing waits on the host): one
+    # scene -> (cost, global index, n_feasible) of each rank's feasible winner;
+    # scenes -> every scene's (best, argmin_all, argmin_hc, n_feasible) row.
+    # The {iterations, converged} status rides along (the cross-shard early-stop
+    # rule: at tol = 0 no rank converges, checked after the timed loop).
+    gathered = None
+    if world > 1:
+        import torch.distributed as dist
+
+        cdev = _coll_device(dev)
+        rec_len = 5 if W.S == 1 else 4 * W.S + 2
+        gathered = torch.empty(world, rec_len, dtype=torch.float64, device=cdev)
+
+    def exchange():
+        if W.S == 1:
+            b = sc.best_index[0]
+            bc = sc.meta_cost[b.clamp(min=0)]
+            rec = torch.stack([torch.where(b >= 0, bc, torch.full_like(bc, float("inf"))),
+                               torch.where(b >= 0, (b + offset).double(), torch.full_like(bc, -1.0)),
+                               sc.n_feasible[0].double(), status_dev[0].double(), status_dev[1].double()])
+        else:
+            rec = torch.cat([torch.stack([sc.best_index, sc.argmin_all, sc.argmin_hc, sc.n_feasible]).double().ravel(),
+                             status_dev.double()])
+        if gathered.device.type == "cuda":
+            dist.all_gather_into_tensor(gathered, rec)
+        else:
+            dist.all_gather(list(gathered.unbind(0)), rec.cpu())
+
     def step():
         # the residual history is not requested (plan_batch does not return it)
         out = D.solution_struct(sol)
         out.history = None
         nat.check(lib.bmpc_plan(ctx, ctypes.byref(pstruct), ctypes.byref(opts_async), ctypes.byref(out),
                                 ctypes.byref(sspec), ctypes.byref(D.score_struct(sc)), sp))
+        if world > 1:
+            exchange()
         return out
 
     def kernel_only():
@@ -260,19 +305,23 @@ def run_ours(args, rank, world, local_rank):
             torch.distributed.barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     t_local = sum(step_ms)
-    # global argmin across shards (the only collective): exercised once, outside timing
-    best_local = None
+    best_global = None
+    total_L = L
     if world > 1:
-        from paper_2109_10392_b200.dist import allgather_winner, local_winner
+        from paper_2109_10392_b200.dist import merge_winners
 
-        rec = local_winner(sc.meta_cost.cpu().numpy(), sc.flags.cpu().numpy() == 7, offset)
-        best_local, _ = allgather_winner(rec)
-        tt = torch.tensor([t_local], dtype=torch.float64, device=_coll_device(dev))
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        t_max = float(tt.item())
+        g = gathered.cpu().numpy()
+        assert (g[:, -1] == 0).all(), "a shard converged at tol = 0: the step would need the re-run"
+        if W.S == 1:
+            best_global, _ = merge_winners(g[:, :3])
+        tt = torch.tensor([t_local, float(L)], dtype=torch.float64, device=_coll_device(dev))
+        tl = [torch.empty_like(tt) for _ in range(world)]
+        torch.distributed.all_gather(tl, tt)
+        t_max = max(float(x[0]) for x in tl)
+        total_L = int(sum(float(x[1]) for x in tl))
     else:
         t_max = t_local
-    total_problems = L * world * args.steps
+    total_problems = total_L * args.steps
     value = total_problems / (t_max / 1e3)
 
     # roofline: the persistent AM kernel alone
@@ -290,7 +339,7 @@ def run_ours(args, rank, world, local_rank):
     peak = D.peak_fp64_tflops(5)
     achieved = flops / (k_ms * 1e-3) / 1e12
 
-    # e2e through the public API from pinned host buffers
+    # e2e through the public API from host buffers
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
 
     class _H:
@@ -299,20 +348,40 @@ def run_ours(args, rank, world, local_rank):
     H = _H()
     H.xi_x, H.xi_y, H.b_xy, H.b_psi = pin(W.xi_x), pin(W.xi_y), pin(W.b_xy), pin(W.b_psi)
     H.l, H.S, H.a, H.b, H.v_min, H.v_max, H.a_max = W.l, W.S, W.a, W.b, W.v_min, W.v_max, W.a_max
-    res = None
-    for _ in range(args.warmup):  # as the timed loop: the previous result stays alive
-        res = plan_batch(solver, H, max_iter=iters, tol=0.0, spec=spec, limits=limits,
-                         precision=args.precision)
-    e2e_ms = []
-    best_e2e = None
-    for i in range(args.steps):
-        flush.fill_(float(i))
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        res = plan_batch(solver, H, max_iter=iters, tol=0.0, spec=spec, limits=limits,
-                         precision=args.precision)
-        e2e_ms.append((time.perf_counter() - t0) * 1e3)
-        best_e2e = res.best_index[0]
+    job = None
+    if world > 1:
+        from paper_2109_10392_b200.dist import plan_sharded
+
+        # the whole job every rank passes to plan_sharded (weak c3/c4: the
+        # ranks' consecutive seed blocks are one stacked batch)
+        from paper_2109_10392_b200.scenes import make_workload
+
+        job = full if full is not None else make_workload(args.config, scenes=cfg.scenes * world)
+
+    def e2e_call(src):
+        if job is not None:
+            return plan_sharded(solver, job, max_iter=iters, tol=0.0, spec=spec, limits=limits,
+                                precision=args.precision)
+        return plan_batch(solver, src, max_iter=iters, tol=0.0, spec=spec, limits=limits,
+                          precision=args.precision)
+
+    def timed_e2e(src, steps):
+        r = None
+        for _ in range(args.warmup):  # as the timed loop: the previous result stays alive
+            r = e2e_call(src)
+        ms = []
+        for i in range(steps):
+            flush.fill_(float(i))
+            torch.cuda.synchronize()
+            if world > 1:
+                torch.distributed.barrier()
+            t0 = time.perf_counter()
+            r = e2e_call(src)
+            ms.append((time.perf_counter() - t0) * 1e3)
+        return ms, r
+
+    e2e_ms, res = timed_e2e(H, args.steps)
+    best_e2e = res.best_index[0]
     e2e_local = sum(e2e_ms)
     if world > 1:
         tt = torch.tensor([e2e_local], dtype=torch.float64, device=_coll_device(dev))
@@ -321,6 +390,35 @@ def run_ours(args, rank, world, local_rank):
     e2e_value = total_problems / (e2e_local / 1e3)
     h2d = sum(a.nbytes for a in (H.xi_x, H.xi_y, H.b_xy, H.b_psi))
     d2h = 3 * nb * L * 8 + 3 * L * 8 + 3 * L * 8 + L + 4 * W.S * 8
+    # the same call from ordinary (pageable) numpy arrays, as the reference API
+    # passes them, and BatchSolver.solve end to end (reference-shaped: host
+    # arrays in, AmState + SolveInfo out)
+    extra = {}
+    if world == 1:
+        pg_ms, _ = timed_e2e(W, args.steps)
+        extra["e2e_pageable"] = {"value": L * args.steps / (sum(pg_ms) / 1e3), "unit": "problems/s",
+                                 "ms_per_step": sum(pg_ms) / args.steps,
+                                 "path": "plan_batch from pageable numpy inputs (staged copies in)"}
+        from paper_2109_10392_b200.solver import ProblemBatch
+
+        src = (ProblemBatch(l=W.l, xi_x=W.xi_x[0], xi_y=W.xi_y[0], a=W.a, b=W.b, v_min=W.v_min,
+                            v_max=W.v_max, a_max=W.a_max, b_xy=W.b_xy, b_psi=W.b_psi)
+               if W.S == 1 else W)
+        sv_ms = []
+        for i in range(args.warmup + min(args.steps, 5)):
+            flush.fill_(float(i))
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            st, info = solver.solve(src, max_iter=iters, tol=0.0)
+            _ = (st.c_x, info.residual_history[-1])
+            if i >= args.warmup:
+                sv_ms.append((time.perf_counter() - t0) * 1e3)
+        extra["e2e_solve"] = {"value": L * len(sv_ms) / (sum(sv_ms) / 1e3), "unit": "problems/s",
+                              "ms_per_step": sum(sv_ms) / len(sv_ms),
+                              "path": "BatchSolver.solve(batch, max_iter, tol=0) from pageable numpy: "
+                                      "coefficients, multipliers and the final residuals on the host; "
+                                      "v / alpha / d / alpha_a / d_a left on the device until read; "
+                                      "no scoring"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -337,23 +435,26 @@ def run_ours(args, rank, world, local_rank):
         line = {
             "metric": METRIC, "value": value, "unit": "problems/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "f64" if prec == 0 else "f64+f32 (fp32 obstacle block)",
             "data": "synthetic (seeded scene generator, paper_2109_10392_b200/scenes.py)",
-            "config": {"workload": args.config, "problems_per_gpu": L, "iters": iters, "n": n,
+            "config": {"workload": args.config, "problems_per_step": total_L,
+                       "problems_per_gpu": L, "iters": iters, "n": n,
                        "m": W.m, "n_b": nb, "scenes_per_gpu": W.S, "tol": 0.0,
                        "l2": "flushed between steps (256 MiB write)",
-                       "parallelism": f"goal/scene shards x{world}"},
+                       "parallelism": f"{'goal-column' if W.S == 1 else 'scene'} shards x{world} "
+                                      f"({args.scaling} scaling)"},
             "roofline": roofline_entry(args, achieved, peak, k_ms, t_max / args.steps, n, W.m, nb),
             "e2e": {"value": e2e_value, "unit": "problems/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_local / args.steps,
                     "path": "plan_batch -> bmpc_plan_host: page-locked inputs read in place over "
                             "the host link by the kernels, results back in one copy into a "
                             "pinned block"},
+            **extra,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
-            "best_index_scene0": best_local if world > 1 else best_e2e,
+            "best_index_scene0": best_global if world > 1 and W.S == 1 else best_e2e,
         }
         print(json.dumps(line))
 
@@ -440,6 +541,8 @@ def main():
     ap.add_argument("--iters", type=int, default=0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: a whole config per GPU; strong: the BASELINE config split over the GPUs")
     ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"],
                     help="fp32: mixed precision, fp32 obstacle block (tolerance in DESIGN.md)")
     args = ap.parse_args()

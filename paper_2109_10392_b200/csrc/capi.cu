@@ -87,6 +87,9 @@ struct bmpc_ctx {
   double cond_xy = 0.0, cond_psi = 0.0;  // 1-norm condition numbers of the reduced Hessians
   int sms = 148;
   int smem_optin = 227 * 1024;
+  // private stream-ordered pool for the per-call workspaces: freed blocks stay
+  // cached (release threshold = max) without touching the device's default pool
+  cudaMemPool_t pool = nullptr;
   // pinned staging for bmpc_plan_host's results (grown on demand)
   std::mutex stage_mu;
   void* stage = nullptr;
@@ -113,10 +116,16 @@ static int cuda_fail(cudaError_t e, const char* where) {
 static inline cudaStream_t S_(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 // ------------------------------------------------------------ host e2e ----
+// Stream-ordered workspace from the context's private pool.
+static inline cudaError_t ws_alloc(const bmpc_ctx* c, void** p, size_t bytes, cudaStream_t st) {
+  return c->pool ? cudaMallocFromPoolAsync(p, bytes, c->pool, st) : cudaMallocAsync(p, bytes, st);
+}
+
 struct DevBuf {
   std::vector<void*> ptrs;
+  const bmpc_ctx* ctx;
   cudaStream_t st;
-  explicit DevBuf(cudaStream_t s) : st(s) {}
+  DevBuf(const bmpc_ctx* c, cudaStream_t s) : ctx(c), st(s) {}
   ~DevBuf() {
     for (void* p : ptrs) cudaFreeAsync(p, st);
   }
@@ -124,7 +133,7 @@ struct DevBuf {
   T* alloc(size_t count) {
     void* p = nullptr;
     if (count == 0) count = 1;
-    if (cudaMallocAsync(&p, count * sizeof(T), st) != cudaSuccess) return nullptr;
+    if (ws_alloc(ctx, &p, count * sizeof(T), st) != cudaSuccess) return nullptr;
     ptrs.push_back(p);
     return static_cast<T*>(p);
   }
@@ -347,12 +356,20 @@ int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pd
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&c->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  // Per-call workspaces come from the stream-ordered pool; keep freed blocks
-  // cached instead of trimming them back to the OS at every synchronisation.
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+  // Per-call workspaces come from a private stream-ordered pool that keeps
+  // freed blocks cached instead of trimming them back to the OS at every
+  // synchronisation (the device's default pool is left as the caller set it).
+  cudaMemPoolProps props;
+  memset(&props, 0, sizeof(props));
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  if (cudaMemPoolCreate(&c->pool, &props) == cudaSuccess) {
     unsigned long long keep = ~0ull;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  } else {
+    c->pool = nullptr;
+    cudaGetLastError();
   }
   c->C.n = n;
   c->C.npad = npad;
@@ -381,6 +398,7 @@ int bmpc_ctx_destroy(bmpc_ctx* ctx) {
   if (!ctx) return BMPC_OK;
   cudaFree(ctx->dmem);
   if (ctx->stage) cudaFreeHost(ctx->stage);
+  if (ctx->pool) cudaMemPoolDestroy(ctx->pool);  // released once outstanding blocks are freed
   delete ctx;
   return BMPC_OK;
 }
@@ -529,7 +547,7 @@ int bmpc_sweeps(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opts* o, 
   double* xi2 = nullptr;
   if (tot > 0) {
     // raw pairs, then the ellipse-frame pairs for the sweeps' outside test
-    CK(cudaMallocAsync(&xi2, tot * 4 * sizeof(double), st), "cudaMallocAsync");
+    CK(ws_alloc(ctx, (void**)&xi2, tot * 4 * sizeof(double), st), "workspace allocation");
     CK(bmpc::op_pack_xi(tot, p->xi_x, p->xi_y, xi2, st, xi2 + 2 * tot, p->a, p->b), "pack_xi");
   }
   const int mode = resume ? BMPC_INIT_RESUME : (is_warm(o) ? BMPC_INIT_WARM : BMPC_INIT_COLD);
@@ -627,7 +645,7 @@ static int solve_impl(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opt
   // k_pack_xi zeroes the words (no memset call).
   const size_t xi_bytes = (size_t)tot * 4 * sizeof(double);
   char* wsp = nullptr;
-  CK(cudaMallocAsync(&wsp, xi_bytes + (size_t)M * 8 + 4 * sizeof(int), st), "cudaMallocAsync");
+  CK(ws_alloc(ctx, (void**)&wsp, xi_bytes + (size_t)M * 8 + 4 * sizeof(int), st), "workspace allocation");
   double* xi2 = tot > 0 ? reinterpret_cast<double*>(wsp) : nullptr;
   unsigned long long* words = L > 0 ? reinterpret_cast<unsigned long long*>(wsp + xi_bytes) : nullptr;
   int* scr = L > 0 ? reinterpret_cast<int*>(wsp + xi_bytes + (size_t)M * 8) : nullptr;
@@ -688,7 +706,7 @@ int bmpc_score(bmpc_ctx* ctx, const bmpc_problem* p, const double* c_x, const do
   const long long tot = (long long)p->S * p->m * ctx->C.n;
   double* xi2 = nullptr;
   if (tot > 0) {
-    CK(cudaMallocAsync(&xi2, tot * 2 * sizeof(double), st), "cudaMallocAsync");
+    CK(ws_alloc(ctx, (void**)&xi2, tot * 2 * sizeof(double), st), "workspace allocation");
     CK(bmpc::op_pack_xi(tot, p->xi_x, p->xi_y, xi2, st), "pack_xi");
   }
   bmpc::ScoreArgs S;
@@ -905,7 +923,7 @@ int bmpc_plan_host(bmpc_ctx* ctx, const bmpc_problem* hp, const bmpc_solve_opts*
         cudaGetLastError();  // clear a sticky "invalid value" from pageable memory
     }
   }
-  DevBuf B(st);
+  DevBuf B(ctx, st);
   char* arena = B.alloc<char>(off);
   if (!arena) return fail(BMPC_ECUDA, "device allocation failed");
   double* xix = (double*)(arena + o_xix);

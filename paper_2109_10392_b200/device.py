@@ -101,6 +101,7 @@ class DeviceSolution:
     v: "object"          # (n, L) or None
     iterations: int
     converged: bool
+    coef: "object" = None  # (6, nb, L): c_x, c_y, c_psi, l_x, l_y, l_psi are its rows
 
 
 @dataclass
@@ -120,7 +121,7 @@ def alloc_solution(nb: int, n: int, L: int, max_iter: int, want_v: bool, device)
     z = lambda *s: torch.empty(*s, dtype=torch.float64, device=device)  # noqa: E731
     coef = z(6, nb, L)
     return DeviceSolution(coef[0], coef[1], coef[2], coef[3], coef[4], coef[5],
-                          z(max_iter, 3, L), z(3, L), z(n, L) if want_v else None, 0, False)
+                          z(max_iter, 3, L), z(3, L), z(n, L) if want_v else None, 0, False, coef)
 
 
 def solution_struct(sol: DeviceSolution) -> nat.SolveOut:

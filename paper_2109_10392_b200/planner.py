@@ -593,18 +593,12 @@ def plan_batch(solver: BatchSolver, scenes, max_iter: int = 100, tol: float = 0.
     from .device import stream_ptr
 
     limits = limits or FilterLimits()
-    if isinstance(scenes, ProblemBatch):
-        solver._check_batch(scenes)
-        xi_x, xi_y, S = scenes.xi_x[None, :], scenes.xi_y[None, :], 1
-    else:
-        xi_x, xi_y, S = scenes.xi_x, scenes.xi_y, scenes.S
-    l = scenes.l
+    # every shape is checked before the C ABI reads (or copies) the host buffers
+    xi_x, xi_y, S, l = solver.check_scenes(scenes)
     L = S * l
     nb, n = solver.basis.n_b, solver.basis.grid.n
     c = lambda a: np.ascontiguousarray(a, dtype=np.float64)  # noqa: E731
     xi_x, xi_y, b_xy, b_psi = c(xi_x), c(xi_y), c(scenes.b_xy), c(scenes.b_psi)
-    if xi_x.shape[1] % n:
-        raise ValueError("obstacle predictions must have m*n entries per scene")
     ctx = solver._context()
     prob = nat.Problem(xi_x.shape[1] // n, l, S, xi_x.ctypes.data, xi_y.ctypes.data,
                        b_xy.ctypes.data, b_psi.ctypes.data, scenes.a, scenes.b, scenes.v_min,

@@ -330,18 +330,19 @@ class BatchSolver:
         self._sample_all = np.vstack([basis.P, basis.Pdot, basis.Pddot])
         g = basis.grid
         self._tau = np.ascontiguousarray((g.times - g.t0) / (g.tf - g.t0))
-        self._ctx = None
-        self._ctx_device = None
+        self._ctxs = {}  # device index -> bmpc_ctx (constants uploaded once per device)
 
     # -- device context ------------------------------------------------------
     def _context(self):
+        """The C-ABI context of the current CUDA device (created on first use)."""
         import torch
 
-        if self._ctx is not None and self._ctx_device == torch._C._cuda_getDevice():
-            return self._ctx
         if not torch.cuda.is_available():
             raise RuntimeError("BatchSolver needs a CUDA device (sm_100a); there is no CPU fallback")
-        dev = torch.cuda.current_device()
+        dev = torch._C._cuda_getDevice()
+        c = self._ctxs.get(dev)
+        if c is not None:
+            return c
         lib = nat.load()
         c = ctypes.c_void_p()
         b = self.basis
@@ -351,7 +352,7 @@ class BatchSolver:
         nat.check(lib.bmpc_ctx_create(b.grid.n, b.n_b, float(self.rho_xy),
                                       *[nat.c_double_ptr(a) for a in arrs], ctypes.byref(c)),
                   "bmpc_ctx_create")
-        self._ctx, self._ctx_device = c, dev
+        self._ctxs[dev] = c
         return c
 
     def qp_info(self) -> dict:
@@ -366,10 +367,20 @@ class BatchSolver:
 
     def __del__(self):
         try:
-            if self._ctx is not None:
-                nat.load().bmpc_ctx_destroy(self._ctx)
+            lib = nat.load()
+            for c in self.__dict__.get("_ctxs", {}).values():
+                lib.bmpc_ctx_destroy(c)
         except Exception:
             pass
+
+    @staticmethod
+    def _on_current_device(t, what="problem"):
+        import torch
+
+        cur = torch._C._cuda_getDevice()
+        if t.device.type != "cuda" or t.device.index != cur:
+            raise ValueError(f"the {what} lives on {t.device} but the current device is cuda:{cur}; "
+                             "select it with torch.cuda.set_device / torch.cuda.device first")
 
     # -- validation ---------------------------------------------------------
     def _check_batch(self, batch: ProblemBatch):
@@ -420,6 +431,7 @@ class BatchSolver:
 
         if max_iter < 1:
             raise ValueError(f"max_iter must be >= 1, got {max_iter}")
+        self._on_current_device(prob.b_xy)
         ctx = self._context()
         dev = prob.b_xy.device
         sol = D.alloc_solution(self.basis.n_b, self.basis.grid.n, prob.L, max_iter, want_v, dev)
@@ -531,14 +543,43 @@ class BatchSolver:
             sol = self.solve_device(prob, max_iter, tol, wd, keep_multipliers)
         aux = _LazyAux(self, sol, prob)
         n, L, mn = self.basis.grid.n, prob.L, prob.m * self.basis.grid.n
-        h = lambda t: t.cpu().numpy()  # noqa: E731
-        state = AmState(c_x=h(sol.c_x), c_y=h(sol.c_y), c_psi=h(sol.c_psi),
+        coef = sol.coef.cpu().numpy()  # c_x, c_y, c_psi, l_x, l_y, l_psi in one copy
+        state = AmState(c_x=coef[0], c_y=coef[1], c_psi=coef[2],
                         alpha=_Deferred(aux, "alpha", (mn, L)), d=_Deferred(aux, "d", (mn, L)),
                         alpha_a=_Deferred(aux, "alpha_a", (n, L)), d_a=_Deferred(aux, "d_a", (n, L)),
-                        v=_Deferred(aux, "v", (n, L)), lambda_x=h(sol.l_x), lambda_y=h(sol.l_y),
-                        lambda_psi=h(sol.l_psi), iteration=sol.iterations)
+                        v=_Deferred(aux, "v", (n, L)), lambda_x=coef[3], lambda_y=coef[4],
+                        lambda_psi=coef[5], iteration=sol.iterations)
         return state, SolveInfo(residual_history=_History(sol.history, sol.iterations),
                                 iterations=sol.iterations, converged=sol.converged, iterates=iterates)
+
+    def check_scenes(self, batch):
+        """Validate a ProblemBatch or a stacked scene batch against this solver's
+        shapes (the reference's checks, solver.py:47-59, :266-277, applied per
+        scene); returns (xi_x (S, m*n), xi_y, S, l)."""
+        if isinstance(batch, ProblemBatch):
+            self._check_batch(batch)
+            return batch.xi_x[None, :], batch.xi_y[None, :], 1, batch.l
+        mn = self.mats.rows_obs
+        S, l = int(batch.S), int(batch.l)
+        xi_x, xi_y = np.atleast_2d(batch.xi_x), np.atleast_2d(batch.xi_y)
+        if S < 1 or l < 0:
+            raise ValueError(f"need S >= 1 scenes and l >= 0 goals, got S={S}, l={l}")
+        if xi_x.shape != (S, mn) or xi_y.shape != (S, mn):
+            raise ValueError(f"expected obstacle predictions of shape ({S}, {mn}), got {xi_x.shape} "
+                             f"and {xi_y.shape}")
+        if np.shape(batch.b_xy) != (self.mats.A.shape[0], S * l):
+            raise ValueError(f"b_xy must have shape ({self.mats.A.shape[0]}, {S * l}), got "
+                             f"{np.shape(batch.b_xy)}")
+        if np.shape(batch.b_psi) != (self.mats.A_psi.shape[0], S * l):
+            raise ValueError(f"b_psi must have shape ({self.mats.A_psi.shape[0]}, {S * l}), got "
+                             f"{np.shape(batch.b_psi)}")
+        rho = getattr(batch, "rho", getattr(batch, "rho_xy", self.rho_xy))
+        if rho != self.rho_xy:
+            raise ValueError("batch rho differs from the rho the KKT inverses were built with")
+        ProblemBatch(l=S * l, xi_x=xi_x[0], xi_y=xi_y[0], a=batch.a, b=batch.b, v_min=batch.v_min,
+                     v_max=batch.v_max, a_max=batch.a_max, b_xy=np.asarray(batch.b_xy),
+                     b_psi=np.asarray(batch.b_psi))  # scalar checks
+        return xi_x, xi_y, S, l
 
     def _problem(self, batch):
         """Validated DeviceProblem of a ProblemBatch or a stacked scene batch."""
@@ -547,21 +588,9 @@ class BatchSolver:
             return self.device_problem(batch)
         from .device import DeviceProblem
 
-        n, mn = self.basis.grid.n, self.mats.rows_obs
-        S, l = int(batch.S), int(batch.l)
-        xi_x, xi_y = np.atleast_2d(batch.xi_x), np.atleast_2d(batch.xi_y)
-        if xi_x.shape != (S, mn) or xi_y.shape != (S, mn):
-            raise ValueError(f"expected obstacle predictions of shape ({S}, {mn}), got {xi_x.shape}")
-        if np.shape(batch.b_xy) != (self.mats.A.shape[0], S * l):
-            raise ValueError(f"b_xy must have shape ({self.mats.A.shape[0]}, {S * l})")
-        if np.shape(batch.b_psi) != (self.mats.A_psi.shape[0], S * l):
-            raise ValueError(f"b_psi must have shape ({self.mats.A_psi.shape[0]}, {S * l})")
-        if getattr(batch, "rho", self.rho_xy) != self.rho_xy:
-            raise ValueError("batch rho differs from the rho the KKT inverses were built with")
-        ProblemBatch(l=S * l, xi_x=xi_x[0], xi_y=xi_y[0], a=batch.a, b=batch.b, v_min=batch.v_min,
-                     v_max=batch.v_max, a_max=batch.a_max, b_xy=batch.b_xy, b_psi=batch.b_psi)
-        return DeviceProblem.from_host(n, xi_x, xi_y, batch.b_xy, batch.b_psi, l, batch.a, batch.b,
-                                       batch.v_min, batch.v_max, batch.a_max)
+        xi_x, xi_y, S, l = self.check_scenes(batch)
+        return DeviceProblem.from_host(self.basis.grid.n, xi_x, xi_y, batch.b_xy, batch.b_psi, l, batch.a,
+                                       batch.b, batch.v_min, batch.v_max, batch.a_max)
 
     def _zero_shapes(self, prob) -> AmState:
         """Shape-only AmState of a problem (no allocation)."""

@@ -122,3 +122,36 @@ def test_gloo_world2_global_early_stop(case):
     assert out[0] == out[1] == expect
     if case == "global_later":
         assert expect[0] == 20  # rank 0 alone would stop at 10
+
+
+def test_goal_and_scene_record_merges():
+    """plan_sharded's record builders and merges (CPU): the three scoring masks
+    with numpy's tie / NaN rules across shards, and scene-block padding."""
+    from types import SimpleNamespace
+
+    from paper_2109_10392_b200.dist import goal_records, merge_goal_records, scene_records, shard_range
+
+    rng = np.random.default_rng(11)
+    L, nb = 300, 4
+    meta = np.round(rng.normal(50.0, 5.0, L))  # many exact ties
+    meta[17] = np.nan
+    flags = rng.integers(0, 8, L).astype(np.uint8)
+    coef = rng.normal(size=(3 * nb, L))
+    for world in (1, 2, 3, 7):
+        rows = []
+        for r in range(world):
+            lo, hi = shard_range(L, r, world)
+            rows.append(goal_records(meta[lo:hi], flags[lo:hi], coef[:, lo:hi], lo))
+        best, a_all, a_hc, nf, cost, c = merge_goal_records(np.stack(rows))
+        feas, hc = flags == 7, (flags & 5) == 5
+        assert best == int(np.argmin(np.where(feas, meta, np.inf)))
+        assert a_all == int(np.argmin(meta)) == 17  # NaN wins, as numpy's argmin
+        assert a_hc == int(np.argmin(np.where(hc, meta, np.inf)))
+        assert nf == int(feas.sum()) and cost == meta[best]
+        np.testing.assert_array_equal(c, coef[:, best])
+    res = SimpleNamespace(best_index=[3, None], argmin_all=np.array([1, 2]), argmin_hc=np.array([3, -1]),
+                          n_feasible=np.array([5, 0]), meta_cost=np.arange(20.0),
+                          c_x=np.ones((nb, 20)), c_y=2 * np.ones((nb, 20)), c_psi=3 * np.ones((nb, 20)))
+    rec = scene_records(res, nb, 2, 3, 10).reshape(3, -1)
+    assert rec[0, :5].tolist() == [3, 1, 3, 5, 3.0] and rec[1, 0] == -1 and rec[1, 4] == np.inf
+    assert rec[2, 0] == -1 and rec[0, 5:].tolist() == [1] * nb + [2] * nb + [3] * nb

@@ -259,3 +259,24 @@ def test_solver_from_reference_basis_and_matrices():
     ours = make_solver(100, 5.0, 10, 10)
     np.testing.assert_array_equal(s.kkt.matrix_xy, ours.kkt.matrix_xy)
     np.testing.assert_array_equal(s.kkt.matrix_psi, ours.kkt.matrix_psi)
+
+
+def test_check_scenes_validation():
+    """plan_batch / solve validate stacked scene batches before any host buffer
+    is handed to the C ABI (shapes against S, l, m, n; rho; the scalars)."""
+    import dataclasses
+
+    s = make_solver(100, 5.0, 10, 20)
+    W = make_workload("c3", scenes=2, l=8)
+    xi_x, xi_y, S, l = s.check_scenes(W)
+    assert (S, l) == (2, 8) and xi_x.shape == (2, 2000)
+    bad = [dataclasses.replace(W, b_xy=W.b_xy[:, :-1]), dataclasses.replace(W, b_psi=W.b_psi[:3]),
+           dataclasses.replace(W, xi_x=W.xi_x[:1]), dataclasses.replace(W, xi_y=W.xi_y[:, :-100]),
+           dataclasses.replace(W, rho=2.0), dataclasses.replace(W, v_min=0.0),
+           dataclasses.replace(W, S=3)]
+    for b in bad:
+        with pytest.raises(ValueError):
+            s.check_scenes(b)
+    m10 = make_workload("c1", scenes=1, l=4)  # m = 10 predictions for an m = 20 solver
+    with pytest.raises(ValueError):
+        s.check_scenes(m10)
