@@ -85,6 +85,8 @@ typedef struct {
   double a, b, v_min, v_max, a_max;
   const double* xi;     // [S][m][n] interleaved (xi_x, xi_y) pairs
   const double* xis;    // the same pairs in the ellipse frame: (b xi_x, a xi_y)
+  const float* xs32;    // those pairs rounded to fp32 (NaN beyond the prefilter bound)
+  const float* boxes;   // [S][ceil(n/32)][m] float4 obstacle boxes per sample slot, or NULL
   const double* b_xy;   // [12][L]
   const double* b_psi;  // [4][L]
   // warm start (BMPC_INIT_WARM), reference AmState layouts (rows, L)

@@ -8,11 +8,11 @@ namespace bmpc {
 
 size_t am_solve_smem_bytes(int nb, int npad, int kxs, int kps, int warps, int team);
 
-template <int NB, int NKM, bool F32, bool TEAMS = false, bool XS = false>
+template <int NB, int NKM, bool F32, bool TEAMS = false, bool XS = false, bool CULL = false>
 static cudaError_t launch_t(const bmpc_dev_consts& C, const bmpc_solve_args& A, int warps,
                             cudaStream_t st, size_t xs_bytes = 0) {
   const size_t smem = am_solve_smem_bytes(NB, C.npad, C.kxs, C.kps, warps, A.team) + xs_bytes;
-  auto kfn = am_solve_kernel<NB, NKM, F32, TEAMS, XS>;
+  auto kfn = am_solve_kernel<NB, NKM, F32, TEAMS, XS, CULL>;
   // raise the dynamic shared-memory limit once per device and size (a driver
   // call per launch costs microseconds of host time on the critical path)
   static std::atomic<int> granted[16];
@@ -69,24 +69,31 @@ cudaError_t BMPC_CAT(launch_am_nb_, BMPC_INST_NB)(const bmpc_dev_consts& C,
   // constants) when the scene(s) of a block fit next to the scratch: n <= 128,
   // fp64; a block spans at most two scenes when l >= its instance count.
   const size_t xs = xs_stage_bytes(C, A, warps);
+  // obstacle culling by bounding boxes (host decides: A.boxes set for many
+  // obstacles, where it pays): a separate instantiation of every throughput kernel
+  const bool cull = A.boxes != nullptr;
   if (!f32 && xs > 0) {
     switch (C.npad) {
-      case 64: return launch_t<BMPC_INST_NB, 2, false, false, true>(C, A, warps, st, xs);
-      case 128: return launch_t<BMPC_INST_NB, 4, false, false, true>(C, A, warps, st, xs);
+      case 64: return cull ? launch_t<BMPC_INST_NB, 2, false, false, true, true>(C, A, warps, st, xs)
+                           : launch_t<BMPC_INST_NB, 2, false, false, true>(C, A, warps, st, xs);
+      case 128: return cull ? launch_t<BMPC_INST_NB, 4, false, false, true, true>(C, A, warps, st, xs)
+                            : launch_t<BMPC_INST_NB, 4, false, false, true>(C, A, warps, st, xs);
       default: break;
     }
   }
+#define BMPC_LAUNCH(NK)                                                                            \
+  (f32 ? (cull ? launch_t<BMPC_INST_NB, NK, true, false, false, true>(C, A, warps, st)              \
+               : launch_t<BMPC_INST_NB, NK, true>(C, A, warps, st))                                \
+       : (cull ? launch_t<BMPC_INST_NB, NK, false, false, false, true>(C, A, warps, st)             \
+               : launch_t<BMPC_INST_NB, NK, false>(C, A, warps, st)))
   switch (C.npad) {  // the host pads n to 64, 128, 224 or 256 samples
-    case 64: return f32 ? launch_t<BMPC_INST_NB, 2, true>(C, A, warps, st)
-                                 : launch_t<BMPC_INST_NB, 2, false>(C, A, warps, st);
-    case 128: return f32 ? launch_t<BMPC_INST_NB, 4, true>(C, A, warps, st)
-                                 : launch_t<BMPC_INST_NB, 4, false>(C, A, warps, st);
-    case 224: return f32 ? launch_t<BMPC_INST_NB, 7, true>(C, A, warps, st)
-                                 : launch_t<BMPC_INST_NB, 7, false>(C, A, warps, st);
-    case 256: return f32 ? launch_t<BMPC_INST_NB, 8, true>(C, A, warps, st)
-                                 : launch_t<BMPC_INST_NB, 8, false>(C, A, warps, st);
+    case 64: return BMPC_LAUNCH(2);
+    case 128: return BMPC_LAUNCH(4);
+    case 224: return BMPC_LAUNCH(7);
+    case 256: return BMPC_LAUNCH(8);
     default: return cudaErrorInvalidValue;
   }
+#undef BMPC_LAUNCH
 }
 
 #ifdef BMPC_PHASE_PROF

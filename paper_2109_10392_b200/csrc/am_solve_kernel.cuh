@@ -261,11 +261,16 @@ constexpr bool kPairSlots = NB <= 12;
 struct TailArgs {
   const double* P;
   const double2* cxy;
-  const double2* xi;  // predictions in the ellipse frame (b qx, a qy)
+  const double2* xi;  // predictions in the ellipse frame (b qx, a qy), fp64 (shared memory when staged)
+  const float2* xf;   // the same rounded to fp32, for the prefilter (global)
   const double *xs, *ys;  // sampled positions (pass A) or nullptr: recompute from c
   int n, m;
   double a, b;
   double ia, ib;  // 1 / a, 1 / b
+  float t32;      // prefilter threshold round_up(1.02 (ab)^2) (common.cuh prefilter_lim)
+  float lim32;    // largest coordinate magnitude the prefilter may decide
+  const float4* box;  // [slot][m] obstacle bounding boxes (k_obstacle_boxes) or nullptr
+  float tc;           // culling threshold round_up((ab)^2 (1 + 1e-4)) on the squared box gap
 };
 
 // fp32 mode inside term (the outside test runs in fp64 in both modes): with
@@ -323,15 +328,18 @@ __device__ __forceinline__ void basis3(const double* B0, const double* B1, const
 
 // Prediction loads: shared memory when the block staged its scene(s), else
 // the read-only global path.
-template <bool XS>
-__device__ __forceinline__ double2 ldq(const double2* p) {
+template <bool XS, class T>
+__device__ __forceinline__ T ldq(const T* p) {
   if constexpr (XS)
     return *p;
   else
     return __ldg(p);
 }
 
-template <int NS, int NB, int NPAD, bool F32, int U, bool XS, bool PAIRED>
+#ifndef BMPC_PF_SCALE
+#define BMPC_PF_SCALE 1  // obstacles in flight with the prefilter, relative to U (2, 3: slower at c4)
+#endif
+template <int NS, int NB, int NPAD, bool F32, int U, bool XS, bool PAIRED, bool CULL>
 __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)[NS], int j0, int js,
                                                int group, bool valid, bool leader,
                                                double (&Gx)[NB], double (&Gy)[NB], double& sqo) {
@@ -359,28 +367,115 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
         }
       }
     }
-    // into the ellipse frame
+    // into the ellipse frame, rounded here (an explicit product: left to the
+    // compiler it may fuse into the outside test's subtraction in one loop
+    // variant and not in another, and the variants would differ in the last bit)
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
-      x[s] *= T.b;
-      y[s] *= T.a;
+      x[s] = __dmul_rn(x[s], T.b);
+      y[s] = __dmul_rn(y[s], T.a);
     }
-    const double ia = T.ia, ib = T.ib;
-    BMPC_PROF_NS(10);
-    const int qstep = js * T.n;
-
-    // U obstacles in flight per sample (NS * U terms per group)
+  }
+  const double ia = T.ia, ib = T.ib;
+  constexpr int UF = U * BMPC_PF_SCALE;
+  BMPC_PROF_NS(10);
+  const int qstep = js * T.n;
+  float srx[NS], sry[NS], sqf[NS];  // fp32 mode: sum_j r_j and sum_j |r_j|^2
+#pragma unroll
+  for (int s = 0; s < NS; ++s) srx[s] = sry[s] = sqf[s] = 0.f;
+  const float af = (float)T.a, bf = (float)T.b, ab2 = (float)(T.a * T.b * T.a * T.b);
+  const double abd2 = (T.a * T.b) * (T.a * T.b);
+  // CULL is a separate instantiation: the culling code compiled into the other
+  // kernels costs them registers even unused (c1 +13%)
+  if (CULL && js == 1) {
+    // Whole (or partial, unsplit) slots: cull obstacles by bounding boxes first.
+    // The warp's samples of the slot span a box (fp32, rounded outward; NaN
+    // samples make it unbounded); each obstacle's samples over the same slot
+    // span a precomputed box (k_obstacle_boxes, rounded outward).  When the
+    // gap between the two boxes is at least ab, every term of that obstacle
+    // is outside (r >= gap >= ab), contributes nothing (exact form), and is
+    // skipped; the survivors take the fp64 test in increasing j, so the inside
+    // terms accumulate in the same order as the full loop -- same bits.
+    constexpr int UC = NS == 2 ? 2 : 4;  // surviving obstacles in flight
+    float bx0[NS], bx1[NS], by0[NS], by1[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      float lx = INFINITY, hx = -INFINITY, ly = INFINITY, hy = -INFINITY;
+      if (valid) {
+        const bool nan = x[s] != x[s] || y[s] != y[s];
+        lx = nan ? -INFINITY : __double2float_rd(x[s]);
+        hx = nan ? INFINITY : __double2float_ru(x[s]);
+        ly = nan ? -INFINITY : __double2float_rd(y[s]);
+        hy = nan ? INFINITY : __double2float_ru(y[s]);
+      }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        lx = fminf(lx, __shfl_xor_sync(BMPC_FULL, lx, o));
+        hx = fmaxf(hx, __shfl_xor_sync(BMPC_FULL, hx, o));
+        ly = fminf(ly, __shfl_xor_sync(BMPC_FULL, ly, o));
+        hy = fmaxf(hy, __shfl_xor_sync(BMPC_FULL, hy, o));
+      }
+      bx0[s] = lx, bx1[s] = hx, by0[s] = ly, by1[s] = hy;
+    }
+    const float tc = T.tc;
+    const int lane = threadIdx.x & 31;
+    for (int c0 = 0; c0 < T.m; c0 += 32) {
+      const int jl = c0 + lane;
+      bool keep = false;
+      if (jl < T.m) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          const float4 bo = __ldg(T.box + (k[s] >> 5) * T.m + jl);
+          const float gx = fmaxf(fmaxf(bo.x - bx1[s], bx0[s] - bo.y), 0.f);
+          const float gy = fmaxf(fmaxf(bo.z - by1[s], by0[s] - bo.w), 0.f);
+          keep |= !(fmaf(gx, gx, gy * gy) >= tc);
+        }
+      }
+      unsigned bits = __ballot_sync(BMPC_FULL, keep);
+      while (bits) {
+        int jj[UC];
+        bool on[UC];
+#pragma unroll
+        for (int u = 0; u < UC; ++u) {
+          on[u] = bits != 0u;
+          jj[u] = on[u] ? c0 + __ffs(bits) - 1 : 0;
+          bits &= bits - 1u;
+        }
+        double2 q[NS][UC];
+#pragma unroll
+        for (int u = 0; u < UC; ++u)
+#pragma unroll
+          for (int s = 0; s < NS; ++s)
+            q[s][u] = (on[u] && valid) ? ldq<XS>(T.xi + jj[u] * T.n + k[s]) : make_double2(0.0, 0.0);
+        if (valid) {
+#pragma unroll
+          for (int u = 0; u < UC; ++u)
+#pragma unroll
+            for (int s = 0; s < NS; ++s)
+              if (on[u] && obstacle_inside_s(x[s], y[s], q[s][u], abd2)) {
+                if constexpr (F32)
+                  obstacle_term_f32(x[s], y[s], q[s][u], af, bf, ab2, ia, ib, srx[s], sry[s], sqf[s],
+                                    cin[s]);
+                else
+                  obstacle_inside_res_s(x[s], y[s], q[s][u], T.a, T.b, ia, ib, gsx[s], gsy[s], sq[s],
+                                        cin[s]);
+              }
+        }
+      }
+    }
+  } else if (valid) {
+#ifdef BMPC_NO_PREFILTER
+    constexpr bool kFp64Loop = true;
+#else
+    constexpr bool kFp64Loop = XS;
+#endif
+    if constexpr (kFp64Loop) {
+    // predictions staged in shared memory: the fp64 test straight away (LDS
+    // latency; the prefilter measured slower here)
     const double2* qp[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) qp[s] = T.xi + j0 * T.n + k[s];
-    float srx[NS], sry[NS], sqf[NS];  // fp32 mode: sum_j r_j and sum_j |r_j|^2
-#pragma unroll
-    for (int s = 0; s < NS; ++s) srx[s] = sry[s] = sqf[s] = 0.f;
-    const float af = (float)T.a, bf = (float)T.b, ab2 = (float)(T.a * T.b * T.a * T.b);
-    const double abd2 = (T.a * T.b) * (T.a * T.b);
     int j = j0;
-    // software pipeline: the next group's predictions are in flight while the
-    // current group computes (xi comes from L2 once it outgrows L1, e.g. c4)
     double2 qn[NS][U];
     if (j + (U - 1) * js < T.m) {
 #pragma unroll
@@ -388,11 +483,7 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
 #pragma unroll
         for (int u = 0; u < U; ++u) qn[s][u] = ldq<XS>(qp[s] + u * qstep);
     }
-#ifndef BMPC_OBST_UNROLL
-#define BMPC_OBST_UNROLL 1
-#endif
-    constexpr int kObstUnroll = BMPC_OBST_UNROLL;
-#pragma unroll kObstUnroll
+#pragma unroll 1
     for (; j + (U - 1) * js < T.m; j += U * js) {
       double2 q[NS][U];
 #pragma unroll
@@ -447,6 +538,111 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
         qp[s] += qstep;
       }
     }
+    } else {
+    // Predictions from L2 (not staged): an exact fp32 prefilter (common.cuh prefilter_lim): a term is decided
+    // "outside" from the fp32 pairs when r2f >= t32 and the sample's
+    // coordinates are within the bound; every other term (the boundary band,
+    // the inside terms, large or non-finite coordinates) loads its fp64 pair
+    // and takes the fp64 test, so the decisions -- and the order the inside
+    // terms accumulate in -- are those of the fp64 loop.
+    float xf[NS], yf[NS];
+    const float lim = T.lim32, t32 = T.t32;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const bool ok = fabs(x[s]) <= (double)lim && fabs(y[s]) <= (double)lim;
+      xf[s] = ok ? __double2float_rn(x[s]) : __int_as_float(0x7fc00000);  // NaN: never decides
+      yf[s] = __double2float_rn(y[s]);
+    }
+    // UF obstacles in flight per sample (the fp32 pairs take half the registers)
+    const float2* qp[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) qp[s] = T.xf + j0 * T.n + k[s];
+    // the fp64 test of one undecided term (obstacle jj of sample s)
+    auto slow = [&](int s, int jj) {
+      const double2 q = __ldg(T.xi + jj * T.n + k[s]);
+#ifdef BMPC_PF_DEBUG
+      if (obstacle_inside_s(x[s], y[s], q, abd2) && blockIdx.x == 0 && threadIdx.x < 32)
+        printf("PF inside blk0 lane=%d k=%d j=%d\n", threadIdx.x, k[s], jj);
+#endif
+      if (obstacle_inside_s(x[s], y[s], q, abd2)) {
+        if constexpr (F32)
+          obstacle_term_f32(x[s], y[s], q, af, bf, ab2, ia, ib, srx[s], sry[s], sqf[s], cin[s]);
+        else
+          obstacle_inside_res_s(x[s], y[s], q, T.a, T.b, ia, ib, gsx[s], gsy[s], sq[s], cin[s]);
+      }
+    };
+    int j = j0;
+    // software pipeline: the next group's predictions are in flight while the
+    // current group computes (xi comes from L2 once it outgrows L1, e.g. c4)
+    float2 qn[NS][UF];
+    if (j + (UF - 1) * js < T.m) {
+#pragma unroll
+      for (int s = 0; s < NS; ++s)
+#pragma unroll
+        for (int u = 0; u < UF; ++u) qn[s][u] = ldq<XS>(qp[s] + u * qstep);
+    }
+#pragma unroll 1
+    for (; j + (UF - 1) * js < T.m; j += UF * js) {
+      float2 q[NS][UF];
+#pragma unroll
+      for (int s = 0; s < NS; ++s)
+#pragma unroll
+        for (int u = 0; u < UF; ++u) q[s][u] = qn[s][u];
+      if (j + (2 * UF - 1) * js < T.m) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+#pragma unroll
+          for (int u = 0; u < UF; ++u) qn[s][u] = ldq<XS>(qp[s] + (UF + u) * qstep);
+      }
+      {
+        bool und[NS][UF], any = false;
+#pragma unroll
+        for (int u = 0; u < UF; ++u)
+#pragma unroll
+          for (int s = 0; s < NS; ++s) {
+            const float dx = xf[s] - q[s][u].x, dy = yf[s] - q[s][u].y;
+            und[s][u] = !(fmaf(dx, dx, dy * dy) >= t32);
+            any |= und[s][u];
+#ifdef BMPC_PF_DEBUG
+            {
+              const int jj = j + u * js;
+              const double2 q64 = __ldg(T.xi + jj * T.n + k[s]);
+              if (!und[s][u] && obstacle_inside_s(x[s], y[s], q64, abd2))
+                printf("PF mismatch k=%d j=%d x=%.17g y=%.17g q=(%.17g,%.17g) qf=(%.9g,%.9g) xf=(%.9g,%.9g)\n",
+                       k[s], jj, x[s], y[s], q64.x, q64.y, q[s][u].x, q[s][u].y, xf[s], yf[s]);
+            }
+#endif
+          }
+        if (any) {
+#pragma unroll
+          for (int u = 0; u < UF; ++u)
+#pragma unroll
+            for (int s = 0; s < NS; ++s)
+              if (und[s][u]) slow(s, j + u * js);
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < NS; ++s) qp[s] += UF * qstep;
+    }
+    for (; j < T.m; j += js) {
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const float2 q = ldq<XS>(qp[s]);
+        const float dx = xf[s] - q.x, dy = yf[s] - q.y;
+#ifdef BMPC_PF_DEBUG
+        {
+          const double2 q64 = __ldg(T.xi + j * T.n + k[s]);
+          if ((fmaf(dx, dx, dy * dy) >= t32) && obstacle_inside_s(x[s], y[s], q64, abd2))
+            printf("PF tail mismatch k=%d j=%d\n", k[s], j);
+        }
+#endif
+        if (!(fmaf(dx, dx, dy * dy) >= t32)) slow(s, j);
+        qp[s] += qstep;
+      }
+    }
+    }
+  }
+  if (valid) {
     if constexpr (F32) {
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
@@ -455,7 +651,7 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
         sq[s] = (double)sqf[s];
       }
     }
-  }
+    }
   BMPC_PROF_NS(11);
   if (NS == 1 && group > 1) {  // split slot: combine the group's partial sums
     for (int o = 1; o < group; o <<= 1) {
@@ -492,7 +688,7 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
   BMPC_PROF_NS(13);
 }
 
-template <int NB, int NKM, bool F32, bool TEAMS, bool XS>
+template <int NB, int NKM, bool F32, bool TEAMS, bool XS, bool CULL>
 #ifndef BMPC_MINB
 #define BMPC_MINB 1
 #endif
@@ -634,6 +830,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
   const double2* __restrict__ xis =
       XS ? reinterpret_cast<const double2*>(sXi) + (size_t)(inst / A.l - scene0) * A.m * n
          : reinterpret_cast<const double2*>(A.xis) + (size_t)(inst / A.l) * A.m * n;
+  const float2* __restrict__ xf = reinterpret_cast<const float2*>(A.xs32) + (size_t)(inst / A.l) * A.m * n;
   const int m = A.m;
   const double a = A.a, b = A.b, rho = C.rho;
   const double inv_a = 1.0 / a, inv_b = 1.0 / b;
@@ -1044,14 +1241,18 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
     //     slot(): full slots two at a time, the n % 32 leftover samples split
     //     over lane groups.
     {
-      TailArgs T{sP, cxy, xis, kStoreXY ? ws.x : nullptr, kStoreXY ? ws.y : nullptr, n, m, a, b,
-                 inv_a, inv_b};
+      TailArgs T{sP, cxy, xis, xf, kStoreXY ? ws.x : nullptr, kStoreXY ? ws.y : nullptr, n, m, a, b,
+                 inv_a, inv_b, __double2float_ru((a * b) * (a * b) * 1.02),
+                 __double2float_rd(prefilter_lim(a, b)),
+                 CULL ? reinterpret_cast<const float4*>(A.boxes) + (size_t)(inst / A.l) * ((n + 31) >> 5) * m
+                      : nullptr,
+                 __double2float_ru((a * b) * (a * b) * (1.0 + 1e-4))};
       int r = wt;  // this warp's slots r = wt, wt + TW, ...
       if (kPairSlots<NB>) {
 #pragma unroll 1
         for (; r + TW < sl.F; r += 2 * TW) {
           const int ks[2] = {lane + 32 * r, lane + 32 * (r + TW)};
-          obstacle_block<2, NB, npad, F32, BMPC_UPAIR, XS, PAIRED>(T, ks, 0, 1, 0, true, true, Gx, Gy, sqo);
+          obstacle_block<2, NB, npad, F32, BMPC_UPAIR, XS, PAIRED, CULL>(T, ks, 0, 1, 0, true, true, Gx, Gy, sqo);
         }
       }
 #pragma unroll 1
@@ -1059,10 +1260,10 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
         const Slot S = slot(r, lane, sl);
         const int ks[1] = {S.k};
         if (r < sl.F)  // a full slot on its own
-          obstacle_block<1, NB, npad, F32, BMPC_USINGLE, XS, false>(T, ks, S.j0, S.js, 1, S.valid, S.leader,
+          obstacle_block<1, NB, npad, F32, BMPC_USINGLE, XS, false, CULL>(T, ks, S.j0, S.js, 1, S.valid, S.leader,
                                                              Gx, Gy, sqo);
         else  // the leftover samples, obstacles split over lane groups (js = g)
-          obstacle_block<1, NB, npad, F32, (NKM >= 7 ? BMPC_USPLIT_MANY : BMPC_USPLIT), XS, false>(
+          obstacle_block<1, NB, npad, F32, (NKM >= 7 ? BMPC_USPLIT_MANY : BMPC_USPLIT), XS, false, false>(
               T, ks, S.j0, S.js, sl.g, S.valid, S.leader, Gx, Gy, sqo);
       }
     }

@@ -56,6 +56,7 @@ cudaError_t op_score_samples(const ScoreParams& sp, int l, int L, const double* 
                              cudaStream_t st);
 cudaError_t op_argmin(int S, int l, const double* meta, const uint8_t* flags, long long* best,
                       long long* best_all, long long* best_hc, long long* nfeas, cudaStream_t st);
+cudaError_t op_obstacle_boxes(int S, int m, int n, const double* xis, float* boxes, cudaStream_t st);
 cudaError_t op_pack_xi(long long total, const double* xi_x, const double* xi_y, double* out,
                        cudaStream_t st, double* scaled = nullptr, double a = 1.0, double b = 1.0,
                        int* zero = nullptr, int nzero = 0);
@@ -457,6 +458,15 @@ static int auto_warps(const bmpc_ctx* ctx, int L, int req, int team) {
   return ipb * team;
 }
 
+// Offset (doubles) of the boxes: after the fp32 pairs, 16-byte aligned.
+static inline size_t box_offset(size_t tot) { return (5 * tot + 1) & ~(size_t)1; }
+// Bytes of the packed predictions: raw pairs (2 tot doubles), ellipse-frame
+// pairs (2 tot), their fp32 copy (tot), the per-slot obstacle boxes.
+static size_t xi_work_bytes(const bmpc_problem* p, int n) {
+  const size_t tot = (size_t)p->S * p->m * n;
+  return tot == 0 ? 0 : (box_offset(tot) + 2 * (size_t)p->S * ((n + 31) / 32) * p->m) * sizeof(double);
+}
+
 // Launch `iters` sweeps; xi2 is the packed (S, m, n) double2 buffer.
 static int launch_sweeps(bmpc_ctx* ctx, const bmpc_problem* p, const double* xi2,
                          const bmpc_solve_opts* o, int iters, int init_mode, int hist_offset,
@@ -483,6 +493,13 @@ static int launch_sweeps(bmpc_ctx* ctx, const bmpc_problem* p, const double* xi2
   A.a_max = p->a_max;
   A.xi = xi2;
   A.xis = xi2 ? xi2 + 2 * (size_t)p->S * p->m * ctx->C.n : nullptr;
+  A.xs32 = xi2 ? reinterpret_cast<const float*>(xi2 + 4 * (size_t)p->S * p->m * ctx->C.n) : nullptr;
+  // culling by bounding boxes pays from about two dozen obstacles (c2 m = 30:
+  // -6%, c4 m = 50: -17%; c1 m = 10 / c3 m = 20: +4% / +3%); not in teams
+  static const int cull_min_m = getenv("BMPC_CULL_MIN_M") ? atoi(getenv("BMPC_CULL_MIN_M")) : 24;
+  A.boxes = (xi2 && p->m >= cull_min_m && o->team_warps <= 1 && !(extra_flags & BMPC_F_TEAM_BUILD))
+                ? reinterpret_cast<const float*>(xi2 + box_offset((size_t)p->S * p->m * ctx->C.n))
+                : nullptr;
   A.b_xy = p->b_xy;
   A.b_psi = p->b_psi;
   A.w_alpha = o->w_alpha;
@@ -546,9 +563,11 @@ int bmpc_sweeps(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opts* o, 
   const long long tot = (long long)p->S * p->m * ctx->C.n;
   double* xi2 = nullptr;
   if (tot > 0) {
-    // raw pairs, then the ellipse-frame pairs for the sweeps' outside test
-    CK(ws_alloc(ctx, (void**)&xi2, tot * 4 * sizeof(double), st), "workspace allocation");
+    // raw pairs, then the ellipse-frame pairs for the sweeps' outside test (fp64
+    // and the fp32 prefilter copy), then the obstacle boxes of the culling
+    CK(ws_alloc(ctx, (void**)&xi2, xi_work_bytes(p, ctx->C.n), st), "workspace allocation");
     CK(bmpc::op_pack_xi(tot, p->xi_x, p->xi_y, xi2, st, xi2 + 2 * tot, p->a, p->b), "pack_xi");
+    CK(bmpc::op_obstacle_boxes(p->S, p->m, ctx->C.n, xi2 + 2 * tot, (float*)(xi2 + box_offset(tot)), st), "boxes");
   }
   const int mode = resume ? BMPC_INIT_RESUME : (is_warm(o) ? BMPC_INIT_WARM : BMPC_INIT_COLD);
   rc = launch_sweeps(ctx, p, xi2, o, iters, mode, hist_offset, carry, write_carry, out, st);
@@ -639,11 +658,11 @@ static int solve_impl(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opt
   const int M = o->max_iter;
   int status[2] = {M, 0};
   // One workspace: the packed predictions (raw pairs, then the ellipse-frame
-  // pairs of the sweeps' outside test) and the scratch -- M 64-bit per-sweep
+  // pairs of the sweeps' outside test, fp64 and fp32) and the scratch -- M 64-bit per-sweep
   // early-stop words (not-converged flag | finished-instance count), then
   // ints: [0] the re-run sweep count, [1, 2] {iterations, converged}.
   // k_pack_xi zeroes the words (no memset call).
-  const size_t xi_bytes = (size_t)tot * 4 * sizeof(double);
+  const size_t xi_bytes = (xi_work_bytes(p, ctx->C.n) + 15) & ~(size_t)15;
   char* wsp = nullptr;
   CK(ws_alloc(ctx, (void**)&wsp, xi_bytes + (size_t)M * 8 + 4 * sizeof(int), st), "workspace allocation");
   double* xi2 = tot > 0 ? reinterpret_cast<double*>(wsp) : nullptr;
@@ -653,6 +672,7 @@ static int solve_impl(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opt
     CK(bmpc::op_pack_xi(tot, p->xi_x, p->xi_y, xi2, st, xi2 ? xi2 + 2 * tot : nullptr, p->a, p->b,
                         reinterpret_cast<int*>(words), words ? 2 * M : 0),
        "pack_xi");
+  if (tot > 0) CK(bmpc::op_obstacle_boxes(p->S, p->m, ctx->C.n, xi2 + 2 * tot, (float*)(xi2 + box_offset(tot)), st), "boxes");
   // tol > 0 (fp64, n <= 128: the team instantiation's shapes): the first launch
   // exits once some sweep is known to be globally converged (BMPC_F_POLL), so
   // a solve that converges at sweep t costs about t + (t + 1) sweeps instead of

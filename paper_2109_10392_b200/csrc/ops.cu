@@ -409,6 +409,10 @@ __global__ void k_argmin(int l, const double* __restrict__ meta, const uint8_t* 
 // ------------------------------------------------------------------- misc --
 // (xi_x, xi_y) pairs, and optionally the pairs scaled to the ellipse frame
 // (b xi_x, a xi_y) that the sweep's outside test reads.
+// With `scaled`, also the fp32 copy of the ellipse-frame pairs the sweep's
+// prefilter reads (am_solve_kernel.cuh obstacle_block): rounded to nearest, and
+// NaN when a coordinate exceeds the prefilter's magnitude bound (the fp32 test
+// then never decides that term, the fp64 test does).
 __global__ void k_pack_xi(long long total, const double* __restrict__ xi_x,
                           const double* __restrict__ xi_y, double2* __restrict__ out,
                           double2* __restrict__ scaled, double a, double b, int* zero,
@@ -418,7 +422,43 @@ __global__ void k_pack_xi(long long total, const double* __restrict__ xi_x,
   if (e >= total) return;
   const double x = xi_x[e], y = xi_y[e];
   out[e] = make_double2(x, y);
-  if (scaled) scaled[e] = make_double2(b * x, a * y);
+  if (scaled) {
+    const double sx = b * x, sy = a * y;
+    scaled[e] = make_double2(sx, sy);
+    const double lim = prefilter_lim(a, b);
+    const bool ok = fabs(sx) <= lim && fabs(sy) <= lim;
+    reinterpret_cast<float2*>(scaled + total)[e] =
+        ok ? make_float2(__double2float_rn(sx), __double2float_rn(sy)) : make_float2(NAN, NAN);
+  }
+}
+
+// Bounding box of every obstacle's ellipse-frame predictions over every
+// 32-sample slot (the sweep's culling, am_solve_kernel.cuh obstacle_block):
+// (min x, max x, min y, max y) rounded outward to fp32; unbounded when a
+// prediction is NaN.  Entry (scene * nslots + slot) * m + j.
+__global__ void k_obstacle_boxes(long long count, int m, int n, int nslots,
+                                 const double2* __restrict__ xis, float4* __restrict__ box) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= count) return;
+  const int j = (int)(e % m);
+  const long long r = e / m;
+  const int sl = (int)(r % nslots);
+  const long long sc = r / nslots;
+  const double2* q = xis + ((size_t)sc * m + j) * n;
+  double lx = INFINITY, hx = -INFINITY, ly = INFINITY, hy = -INFINITY;
+  bool nan = false;
+  const int k1 = min(n, 32 * sl + 32);
+  for (int k = 32 * sl; k < k1; ++k) {
+    const double2 v = q[k];
+    nan |= v.x != v.x || v.y != v.y;
+    lx = fmin(lx, v.x);
+    hx = fmax(hx, v.x);
+    ly = fmin(ly, v.y);
+    hy = fmax(hy, v.y);
+  }
+  box[e] = nan ? make_float4(-INFINITY, INFINITY, -INFINITY, INFINITY)
+               : make_float4(__double2float_rd(lx), __double2float_ru(hx), __double2float_rd(ly),
+                             __double2float_ru(hy));
 }
 
 // ---------------------------------------------------------------- launchers --
@@ -509,6 +549,14 @@ cudaError_t op_score_samples(const ScoreParams& sp, int l, int L, const double* 
 cudaError_t op_argmin(int S, int l, const double* meta, const uint8_t* flags, long long* best,
                       long long* best_all, long long* best_hc, long long* nfeas, cudaStream_t st) {
   if (S > 0) k_argmin<<<S, 256, 0, st>>>(l, meta, flags, best, best_all, best_hc, nfeas);
+  return cudaGetLastError();
+}
+cudaError_t op_obstacle_boxes(int S, int m, int n, const double* xis, float* boxes, cudaStream_t st) {
+  const int nslots = (n + 31) / 32;
+  const long long count = (long long)S * nslots * m;
+  if (count > 0)
+    k_obstacle_boxes<<<nblk(count), kTB, 0, st>>>(count, m, n, nslots, reinterpret_cast<const double2*>(xis),
+                                                  reinterpret_cast<float4*>(boxes));
   return cudaGetLastError();
 }
 cudaError_t op_pack_xi(long long total, const double* xi_x, const double* xi_y, double* out,

@@ -33,5 +33,30 @@ d = {
     "grid": get("launch__grid_size", False), "block": get("launch__block_size", False),
     "inst_executed": get("smsp__inst_executed.sum", False),
 }
+
+
+def opt(k):
+    return get(k, False) if k in hdr else None
+
+
+# executed fp64 work, per elapsed cycle over the whole GPU (thread-level SASS
+# counts; clock independent): the fraction of the DFMA lanes' peak the kernel
+# keeps busy (slots: one DFMA, DMUL or DADD each) and its flop-weighted twin
+# (a DFMA is 2 flops; peak = 2 x 64 DFMA lanes x SMs per cycle)
+ops = {op: opt(f"smsp__sass_thread_inst_executed_op_{op}_pred_on.sum.per_cycle_elapsed")
+       for op in ("dfma", "dmul", "dadd")}
+peak = opt("sm__sass_thread_inst_executed_op_dfma_pred_on.sum.peak_sustained")
+if all(v is not None for v in ops.values()) and peak:
+    d["fp64_thread_ops_per_cycle"] = ops
+    d["fp64_peak_thread_ops_per_cycle"] = peak
+    d["fp64_slot_frac_executed"] = (ops["dfma"] + ops["dmul"] + ops["dadd"]) / peak
+    d["fp64_flop_frac_executed"] = (2 * ops["dfma"] + ops["dmul"] + ops["dadd"]) / (2 * peak)
+for k in ("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+          "smsp__pcsamp_warps_issue_stalled_long_scoreboard"):
+    v = opt(k)
+    if v is not None:
+        d[k] = v
+if len(sys.argv) > 5:
+    d["note"] = sys.argv[5]
 json.dump(d, open(out, "w"), indent=1)
 print(json.dumps(d, indent=1))

@@ -9,8 +9,8 @@ def parse(path):
         m = re.search(r"Compiling entry function '(\S+)'", line)
         if m:
             cur = m.group(1)
-            k = re.search(r"am_solve_kernelIL(i\d+)ELi(\d+)ELb(\d)ELb(\d)ELb(\d)E", cur)
-            cur = "am<%s,%s,%s,%s,%s>" % tuple(g.lstrip("i") for g in k.groups()) if k else cur[:40]
+            k = re.search(r"am_solve_kernelIL(i\d+)ELi(\d+)ELb(\d)ELb(\d)ELb(\d)E(?:Lb(\d)E)?", cur)
+            cur = ("am<" + ",".join(g.lstrip("i") for g in k.groups() if g is not None) + ">") if k else cur[:40]
             out[cur] = [None, 0, 0]
             continue
         if cur is None:
