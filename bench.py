@@ -18,8 +18,9 @@ own block of l goal columns of one shared scene, or its own scenes) or strong
 (the BASELINE config split over the ranks as dist.plan_sharded does); the
 shards' results are all-gathered inside the timed step (the only collective),
 and e2e runs dist.plan_sharded.
---impl reference: the CPU oracle port of the reference (oracle/am_oracle.py +
-oracle/am_oracle.c, the reference's algorithm op for op) on all host cores.
+--impl reference: the reference's own CPU path -- its batchmpc package (build-time
+copy, oracle/_ref/pkg) with its compiled Cython kernels, BatchSolver.solve +
+planner scoring -- on all host cores, one BLAS thread per process.
 """
 
 from __future__ import annotations
@@ -141,59 +142,110 @@ def make_step_workload(cfg_name: str, world: int, rank: int, scaling: str = "wea
     return cfg, W, 0, None
 
 
-# ------------------------------------------------------------ CPU oracle ----
-def _oracle_kind() -> str:
-    """"ref": the reference's own compiled Cython kernels (oracle/_ref, built from
-    /root/reference by build() and shipped with the tree) under the oracle's
-    restatement of solver.py; "c": the oracle's C restatement of those kernels."""
-    return "ref" if any((ROOT / "oracle" / "_ref").glob("_speedups*.so")) else "c"
+# ------------------------------------------------------------ CPU baseline ----
+# The reference's own CPU path: its batchmpc package (build-time copy in
+# oracle/_ref/pkg, with its Cython kernels compiled from /root/reference) running
+# BatchSolver.solve(tol=0) + its planner scoring (sample_plan / filter_candidates
+# / rank) over disjoint goal blocks of one scene, one process per host core, one
+# BLAS thread each.  Each worker builds the scene and the
+# solver (KKT factorisation) once, outside the timed region.  When the package
+# copy is absent the oracle's restatement (oracle/am_oracle.py + its C kernels)
+# stands in.
+REF_PKG = ROOT / "oracle" / "_ref" / "pkg"
+
+
+def _cpu_kind() -> str:
+    if (REF_PKG / "batchmpc" / "solver.py").exists() and any((REF_PKG / "batchmpc" / "kernels").glob("_speedups*.so")):
+        return "refpkg"
+    return "c"
 
 
 def _cpu_sample_text(kind: str) -> str:
-    return ("oracle/am_oracle.py (solver.py restated op for op in numpy) + the reference's compiled "
-            "Cython kernels (oracle/_ref)" if kind == "ref" else "oracle/am_oracle.py + am_oracle.c")
+    return ("the reference's own batchmpc.BatchSolver.solve + planner scoring (oracle/_ref/pkg: its sources, its "
+            "Cython kernels compiled from /root/reference)" if kind == "refpkg"
+            else "oracle/am_oracle.py (solver.py restated op for op) + am_oracle.c kernels")
 
 
-def _cpu_worker(args):
-    cfg_name, l_lo, l_hi, iters, world_l = args[:5]
-    kind = args[5] if len(args) > 5 else "c"
+_W = {}
+
+
+def _cpu_init(cfg_name, goals, kind):
     from threadpoolctl import threadpool_limits
-
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import am_oracle as O
 
     from paper_2109_10392_b200.scenes import CONFIGS, make_workload
 
     cfg = CONFIGS[cfg_name]
-    with threadpool_limits(1):
-        W = make_workload(cfg_name, l=world_l, scenes=1)
-        o = O.OracleSolver(cfg.n, cfg.t_f, cfg.degree, cfg.m)
-        t = time.perf_counter()
-        r = o.solve(W.xi_x[0], W.xi_y[0], W.b_xy[:, l_lo:l_hi], W.b_psi[:, l_lo:l_hi], W.a, W.b,
-                    W.v_min, W.v_max, W.a_max, iters, kernel=kind)
-        sc = o.score(r, W.xi_x[0], W.xi_y[0], W.a, W.b, kind="cruise", v_cruise=20.0)
-        return time.perf_counter() - t, l_hi - l_lo, sc["best_index"]
+    W = make_workload(cfg_name, l=goals, scenes=1)
+    _W.update(cfg=cfg, W=W, kind=kind)
+    if kind == "refpkg":
+        sys.path.insert(0, str(REF_PKG))
+        import batchmpc as B
+        from batchmpc import planner as RP
+        from batchmpc.solver import BatchSolver, ProblemBatch
+
+        grid = B.build_time_grid(0.0, cfg.t_f, cfg.n)
+        basis = B.build_basis(grid, cfg.degree)
+        _W.update(solver=BatchSolver(basis, B.build_constant_matrices(basis, cfg.m), 1.0), PB=ProblemBatch,
+                  RP=RP)
+    else:
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import am_oracle as O
+
+        _W["solver"] = O.OracleSolver(cfg.n, cfg.t_f, cfg.degree, cfg.m)
+    # after every BLAS is loaded (numpy's and scipy's own OpenBLAS), kept for the
+    # worker's lifetime: one thread per process
+    _W["limits"] = threadpool_limits(1)
 
 
-def cpu_oracle_rate(cfg_name: str, goals: int, iters: int, procs: int, reps: int = 3,
-                    kind: str = "c"):
-    """Aggregate problems/s of the CPU path: `procs` processes, 1 BLAS thread each,
-    disjoint goal blocks of one scene, best of `reps` (SURVEY.md 8d CPU-baseline recipe)."""
+def _cpu_job(args):
+    lo, hi, iters = args
+    W, solver = _W["W"], _W["solver"]
+    t = time.perf_counter()
+    if _W["kind"] == "refpkg":
+        RP = _W["RP"]
+        batch = _W["PB"](l=hi - lo, xi_x=W.xi_x[0], xi_y=W.xi_y[0], a=W.a, b=W.b, v_min=W.v_min,
+                         v_max=W.v_max, a_max=W.a_max, b_xy=np.ascontiguousarray(W.b_xy[:, lo:hi]),
+                         b_psi=np.ascontiguousarray(W.b_psi[:, lo:hi]))
+        st, info = solver.solve(batch, max_iter=iters, tol=0.0)
+        bs = solver.basis
+        xd, yd = bs.Pdot @ st.c_x, bs.Pdot @ st.c_y
+        plan = RP.RankedPlan(goals=[None] * batch.l, x=bs.P @ st.c_x, y=bs.P @ st.c_y, psi=bs.P @ st.c_psi,
+                             psidot=bs.Pdot @ st.c_psi, v=np.sqrt(xd ** 2 + yd ** 2),
+                             xddot=bs.Pddot @ st.c_x, yddot=bs.Pddot @ st.c_y,
+                             residuals=info.residual_history[-1])
+        RP.filter_candidates(plan, batch, RP.FilterLimits())
+        RP.rank(plan, RP.MetaCostSpec("cruise", v_cruise=20.0))
+        best = plan.best_index
+    else:
+        r = solver.solve(W.xi_x[0], W.xi_y[0], W.b_xy[:, lo:hi], W.b_psi[:, lo:hi], W.a, W.b, W.v_min,
+                         W.v_max, W.a_max, iters, kernel="c")
+        best = solver.score(r, W.xi_x[0], W.xi_y[0], W.a, W.b, kind="cruise", v_cruise=20.0)["best_index"]
+    return time.perf_counter() - t, hi - lo, best
+
+
+def cpu_reference_rate(cfg_name: str, goals: int, iters: int, steps: int, warmup: int):
+    """Problems/s of the reference CPU path on `goals` goal columns of scene 0
+    split over every host core: mean over `steps` timed passes (wall clock
+    around the pool map) after `warmup` passes.  Returns (rate, per-step
+    seconds, processes, kind)."""
     import multiprocessing as mp
 
+    kind = _cpu_kind()
+    procs = min(os.cpu_count() or 1, goals)
     per = int(math.ceil(goals / procs))
-    jobs = [(cfg_name, i * per, min(goals, (i + 1) * per), iters, goals, kind) for i in range(procs)
-            if i * per < goals]
-    ctx = mp.get_context("spawn")
-    best = None
-    with ctx.Pool(len(jobs)) as pool:
-        pool.map(_cpu_worker, [(cfg_name, 0, 1, 1, goals, kind)] * len(jobs))  # warm-up imports
-        for _ in range(reps):
+    jobs = [(i * per, min(goals, (i + 1) * per), iters) for i in range(procs) if i * per < goals]
+    times = []
+    for v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[v] = "1"  # inherited by the spawned workers
+    with mp.get_context("spawn").Pool(len(jobs), initializer=_cpu_init, initargs=(cfg_name, goals, kind)) as pool:
+        pool.map(_cpu_job, [(0, 1, 1)] * len(jobs))  # imports, first-touch
+        for _ in range(warmup):
+            pool.map(_cpu_job, jobs)
+        for _ in range(steps):
             t0 = time.perf_counter()
-            pool.map(_cpu_worker, jobs)
-            dt = time.perf_counter() - t0
-            best = dt if best is None else min(best, dt)
-    return goals / best, best, len(jobs)
+            pool.map(_cpu_job, jobs)
+            times.append(time.perf_counter() - t0)
+    return goals * len(times) / sum(times), times, len(jobs), kind
 
 
 # ---------------------------------------------------------------- our arm ----
@@ -422,15 +474,13 @@ def run_ours(args, rank, world, local_rank):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        procs = os.cpu_count() or 1
         goals = min(cfg.l, 1024)  # bounded sample: scene 0, at most 1024 goals of this config
-        kind = _oracle_kind()
-        rate, secs, used = cpu_oracle_rate(args.config, goals, iters, procs, kind=kind)
+        rate, times, used, kind = cpu_reference_rate(args.config, goals, iters, steps=3, warmup=1)
         cpu = {"value": rate, "unit": "problems/s", "cores": used,
-               "kind": "reference" if kind == "ref" else "port",
-               "sample": f"{args.config} scene 0, {goals} goals x {iters} sweeps + scoring, split "
-                         f"over {used} processes (1 BLAS thread each), best of 3, {secs:.2f}s wall; "
-                         + _cpu_sample_text(kind)}
+               "kind": "reference" if kind == "refpkg" else "port",
+               "sample": f"{args.config} scene 0, {goals} goals x {iters} sweeps + scoring per pass, split "
+                         f"over {used} processes (1 BLAS thread each), mean of {len(times)} passes "
+                         f"({statistics.mean(times):.2f}s each); " + _cpu_sample_text(kind)}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "problems/s", "n_gpus": world,
@@ -474,22 +524,34 @@ def roofline_entry(args, achieved, peak, k_ms, step_ms, n, m, nb):
          "peak_source": "measured live: DFMA microbenchmark (csrc/peak.cu)",
          "note": "frac = canonical algorithmic work per second over the FP64 peak; the kernel "
                  "executes less than W (exact-form obstacle/acceleration blocks: an outside test "
-                 "per obstacle term), so frac can exceed 1 on obstacle-heavy configs; the executed "
-                 "FP64-pipe utilisation is ncu.fp64_pipe_active_pct"}
+                 "per obstacle term; obstacles culled by bounding boxes when m >= 24), so frac "
+                 "can exceed 1 on obstacle-heavy configs; frac_executed is the executed fp64 "
+                 "flops over the peak (ncu capture of the same config, profiles/ncu_<config>_"
+                 "<precision>.json)"}
     prof = ROOT / "profiles" / f"ncu_{args.config}_{args.precision}.json"
     if prof.exists():
         d = json.loads(prof.read_text())
         r["traffic"] = d["dram_read_bytes"] + d["dram_write_bytes"]
         r["traffic_unit"] = "bytes per launch (ncu dram__bytes_read+write)"
-        r["ncu"] = {"report": d["report"], "fp64_pipe_active_pct": d["fp64_pipe_active_pct"],
-                    "issue_active_per_cycle": d["issue_active_per_cycle"],
-                    "warps_active_per_cycle": d["warps_active_per_cycle"],
-                    "duration_ms": d["duration_ms"]}
+        r["ncu"] = {k: d[k] for k in ("report", "kernel", "fp64_pipe_active_pct", "issue_active_per_cycle",
+                                        "warps_active_per_cycle", "duration_ms", "registers_per_thread",
+                                        "fp64_thread_ops_per_cycle", "fp64_slot_frac_executed",
+                                        "fp64_flop_frac_executed", "note") if k in d}
+        if "fp64_flop_frac_executed" in d:
+            # executed fp64 work (ncu SASS counts of DFMA x2 + DMUL + DADD per elapsed
+            # cycle, over the DFMA lanes' peak): the pipe's real utilisation, next to
+            # the canonical-W fraction above (which credits the work the exact-form
+            # obstacle block and the culling never execute)
+            r["frac_executed"] = d["fp64_flop_frac_executed"]
+            r["achieved_executed"] = d["fp64_flop_frac_executed"] * peak
     return r
 
 
 # ---------------------------------------------------------- reference arm ----
 def run_reference(args, rank, world):
+    """--impl reference: the reference's own CPU path (see cpu_reference_rate) on
+    this host's cores, on a bounded sample of the same workload per step; rank 0
+    only under torchrun."""
     if rank != 0:
         return
     from paper_2109_10392_b200.scenes import CONFIGS
@@ -497,36 +559,19 @@ def run_reference(args, rank, world):
     cfg = CONFIGS[args.config]
     iters = args.iters or cfg.iters
     goals = min(cfg.l, 1024)  # bounded sample of the workload per step: scene 0
-    procs = os.cpu_count() or 1
-    times = []
-    import multiprocessing as mp
-
-    per = int(math.ceil(goals / procs))
-    cfg_name = args.config
-    kind = _oracle_kind()
-    jobs = [(cfg_name, i * per, min(goals, (i + 1) * per), iters, goals, kind) for i in range(procs)
-            if i * per < goals]
-    with mp.get_context("spawn").Pool(len(jobs)) as pool:
-        pool.map(_cpu_worker, [(cfg_name, 0, 1, 1, goals, kind)] * len(jobs))
-        for _ in range(args.warmup):
-            pool.map(_cpu_worker, jobs)
-        for _ in range(args.steps):
-            t0 = time.perf_counter()
-            pool.map(_cpu_worker, jobs)
-            times.append(time.perf_counter() - t0)
-    value = goals * args.steps / sum(times)
+    value, times, used, kind = cpu_reference_rate(args.config, goals, iters, args.steps, args.warmup)
+    n, m, nb = cfg.n, cfg.m, cfg.degree + 1
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "problems/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * sum(times) / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config, "problems_per_step": goals, "iters": iters,
-                   "tol": 0.0},
-        "cpu_baseline": {"value": value, "unit": "problems/s", "cores": len(jobs),
-                         "kind": "reference" if kind == "ref" else "port",
-                         "sample": f"{cfg_name} scene 0, {goals} goals x {iters} sweeps + scoring per "
-                                   f"step over {len(jobs)} processes (1 BLAS thread each); "
-                                   + _cpu_sample_text(kind)},
+        "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True, "scaling": args.scaling,
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded scene generator, paper_2109_10392_b200/scenes.py)",
+        "config": {"workload": args.config, "problems_per_step": goals, "problems_per_gpu": goals, "iters": iters,
+                   "n": n, "m": m, "n_b": nb, "scenes_per_gpu": 1, "tol": 0.0},
+        "cpu_baseline": {"value": value, "unit": "problems/s", "cores": used,
+                         "kind": "reference" if kind == "refpkg" else "port",
+                         "sample": f"{args.config} scene 0, {goals} goals x {iters} sweeps + scoring per "
+                                   f"step over {used} processes (1 BLAS thread each); " + _cpu_sample_text(kind)},
         "e2e": {"value": value, "unit": "problems/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
