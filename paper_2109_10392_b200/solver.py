@@ -207,6 +207,12 @@ class SolveInfo:
     iterates: list[tuple[np.ndarray, np.ndarray, np.ndarray]] | None = None
 
 
+def _single_scene(batch) -> bool:
+    """A one-scene batch: this package's ProblemBatch or any object with its
+    fields (the reference's own batchmpc.solver.ProblemBatch: 1-D predictions)."""
+    return isinstance(batch, ProblemBatch) or np.ndim(batch.xi_x) == 1
+
+
 def _default_boundary(spec) -> bool:
     """True when ``spec`` pins the default derivative orders.  Compared field by
     field, so a BoundarySpec of the reference's own ``batchmpc.basis`` (another
@@ -556,9 +562,9 @@ class BatchSolver:
         """Validate a ProblemBatch or a stacked scene batch against this solver's
         shapes (the reference's checks, solver.py:47-59, :266-277, applied per
         scene); returns (xi_x (S, m*n), xi_y, S, l)."""
-        if isinstance(batch, ProblemBatch):
+        if _single_scene(batch):
             self._check_batch(batch)
-            return batch.xi_x[None, :], batch.xi_y[None, :], 1, batch.l
+            return np.asarray(batch.xi_x)[None, :], np.asarray(batch.xi_y)[None, :], 1, batch.l
         mn = self.mats.rows_obs
         S, l = int(batch.S), int(batch.l)
         xi_x, xi_y = np.atleast_2d(batch.xi_x), np.atleast_2d(batch.xi_y)
@@ -583,7 +589,7 @@ class BatchSolver:
 
     def _problem(self, batch):
         """Validated DeviceProblem of a ProblemBatch or a stacked scene batch."""
-        if isinstance(batch, ProblemBatch):
+        if _single_scene(batch):
             self._check_batch(batch)
             return self.device_problem(batch)
         from .device import DeviceProblem

@@ -582,3 +582,27 @@ def test_solve_stacked_scenes_lazy_state(cuda):
     np.testing.assert_array_equal(w_lazy.lambda_psi, w_host.lambda_psi)
     with pytest.raises(ValueError):
         solver.solve(_batch(z, s=0), max_iter=3, warm=state2)  # L columns vs l
+
+
+@pytest.mark.parametrize("name,team", [("c0", 4), ("c0", 2), ("c1", 0), ("c2f", 0), ("c4f", 0)])
+def test_repeat_runs_bitwise_deterministic(cuda, name, team):
+    """Race / barrier-misuse canary (compute-sanitizer is closed on this GPU
+    pool): the persistent kernel's shared-memory exchanges (transpose buffer,
+    team exchange slots, staged predictions, the polled early exit) would
+    show up as run-to-run differences; 12 repeated solves of every kernel
+    variant must agree bit for bit."""
+    from paper_2109_10392_b200 import device as D
+
+    z = golden(name)
+    solver = _solver(z)
+    S = _Scenes(z)
+    prob = D.DeviceProblem.from_host(int(z["n"]), S.xi_x, S.xi_y, S.b_xy, S.b_psi, S.l, S.a, S.b,
+                                     S.v_min, S.v_max, S.a_max)
+    ref = solver.solve_device(prob, max_iter=30, tol=0.0, team_warps=team)
+    tol_ref = solver.solve_device(prob, max_iter=30, tol=1e-9, team_warps=team)
+    for _ in range(12):
+        again = solver.solve_device(prob, max_iter=30, tol=0.0, team_warps=team)
+        for k in ("c_x", "c_y", "c_psi", "l_x", "l_psi", "res_final"):
+            assert cuda.equal(getattr(again, k), getattr(ref, k)), k
+    again = solver.solve_device(prob, max_iter=30, tol=1e-9, team_warps=team)
+    assert again.iterations == tol_ref.iterations and cuda.equal(again.c_x, tol_ref.c_x)
