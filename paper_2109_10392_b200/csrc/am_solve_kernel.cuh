@@ -372,8 +372,13 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
     // variant and not in another, and the variants would differ in the last bit)
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
+#ifdef BMPC_FRAME_CONTRACT
+      x[s] *= T.b;
+      y[s] *= T.a;
+#else
       x[s] = __dmul_rn(x[s], T.b);
       y[s] = __dmul_rn(y[s], T.a);
+#endif
     }
   }
   const double ia = T.ia, ib = T.ib;
