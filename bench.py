@@ -287,9 +287,9 @@ def run_ours(args, rank, world, local_rank):
     status_dev = torch.zeros(2, dtype=torch.int32, device=dev)
     opts_async = nat.SolveOpts(max_iter=iters, tol=0.0, precision=prec, status_dev=status_dev.data_ptr())
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    # pack_xi, am_solve (+ fused scoring), early_stop, am_solve (early-stop re-run:
-    # exits at once when there is none), argmin
-    launches_per_step = 5
+    # pack_xi, [obstacle_boxes when culling: m >= 24], am_solve (+ fused scoring),
+    # early_stop, am_solve (early-stop re-run: exits at once when there is none), argmin
+    launches_per_step = 5 + (1 if W.m >= int(os.environ.get("BMPC_CULL_MIN_M", "24")) else 0)
 
     # N > 1: the step ends with the shards' result exchange (dist.plan_sharded's
     # collective, here on device tensors so nothing waits on the host): one

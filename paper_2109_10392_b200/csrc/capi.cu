@@ -467,6 +467,13 @@ static size_t xi_work_bytes(const bmpc_problem* p, int n) {
   return tot == 0 ? 0 : (box_offset(tot) + 2 * (size_t)p->S * ((n + 31) / 32) * p->m) * sizeof(double);
 }
 
+// Obstacle culling by bounding boxes pays from about two dozen obstacles (c2
+// m = 30: -5%, c4 m = 50: -18%; c1 m = 10 / c3 m = 20: +7% / +3%); not in teams.
+static bool use_cull(const bmpc_problem* p, const bmpc_solve_opts* o, int extra_flags) {
+  static const int cull_min_m = getenv("BMPC_CULL_MIN_M") ? atoi(getenv("BMPC_CULL_MIN_M")) : 24;
+  return p->m >= cull_min_m && o->team_warps <= 1 && !(extra_flags & BMPC_F_TEAM_BUILD);
+}
+
 // Launch `iters` sweeps; xi2 is the packed (S, m, n) double2 buffer.
 static int launch_sweeps(bmpc_ctx* ctx, const bmpc_problem* p, const double* xi2,
                          const bmpc_solve_opts* o, int iters, int init_mode, int hist_offset,
@@ -494,10 +501,7 @@ static int launch_sweeps(bmpc_ctx* ctx, const bmpc_problem* p, const double* xi2
   A.xi = xi2;
   A.xis = xi2 ? xi2 + 2 * (size_t)p->S * p->m * ctx->C.n : nullptr;
   A.xs32 = xi2 ? reinterpret_cast<const float*>(xi2 + 4 * (size_t)p->S * p->m * ctx->C.n) : nullptr;
-  // culling by bounding boxes pays from about two dozen obstacles (c2 m = 30:
-  // -6%, c4 m = 50: -17%; c1 m = 10 / c3 m = 20: +4% / +3%); not in teams
-  static const int cull_min_m = getenv("BMPC_CULL_MIN_M") ? atoi(getenv("BMPC_CULL_MIN_M")) : 24;
-  A.boxes = (xi2 && p->m >= cull_min_m && o->team_warps <= 1 && !(extra_flags & BMPC_F_TEAM_BUILD))
+  A.boxes = (xi2 && use_cull(p, o, extra_flags))
                 ? reinterpret_cast<const float*>(xi2 + box_offset((size_t)p->S * p->m * ctx->C.n))
                 : nullptr;
   A.b_xy = p->b_xy;
@@ -567,7 +571,9 @@ int bmpc_sweeps(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opts* o, 
     // and the fp32 prefilter copy), then the obstacle boxes of the culling
     CK(ws_alloc(ctx, (void**)&xi2, xi_work_bytes(p, ctx->C.n), st), "workspace allocation");
     CK(bmpc::op_pack_xi(tot, p->xi_x, p->xi_y, xi2, st, xi2 + 2 * tot, p->a, p->b), "pack_xi");
-    CK(bmpc::op_obstacle_boxes(p->S, p->m, ctx->C.n, xi2 + 2 * tot, (float*)(xi2 + box_offset(tot)), st), "boxes");
+    if (use_cull(p, o, 0))
+      CK(bmpc::op_obstacle_boxes(p->S, p->m, ctx->C.n, xi2 + 2 * tot, (float*)(xi2 + box_offset(tot)), st),
+         "boxes");
   }
   const int mode = resume ? BMPC_INIT_RESUME : (is_warm(o) ? BMPC_INIT_WARM : BMPC_INIT_COLD);
   rc = launch_sweeps(ctx, p, xi2, o, iters, mode, hist_offset, carry, write_carry, out, st);
@@ -672,12 +678,15 @@ static int solve_impl(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opt
     CK(bmpc::op_pack_xi(tot, p->xi_x, p->xi_y, xi2, st, xi2 ? xi2 + 2 * tot : nullptr, p->a, p->b,
                         reinterpret_cast<int*>(words), words ? 2 * M : 0),
        "pack_xi");
-  if (tot > 0) CK(bmpc::op_obstacle_boxes(p->S, p->m, ctx->C.n, xi2 + 2 * tot, (float*)(xi2 + box_offset(tot)), st), "boxes");
+  // tol > 0 (fp64, n <= 128) runs on the team instantiation (see below)
+  const int tb = (o->tol > 0.0 && o->precision == 0 && ctx->C.npad <= 128) ? BMPC_F_TEAM_BUILD : 0;
+  if (tot > 0 && use_cull(p, o, tb))
+    CK(bmpc::op_obstacle_boxes(p->S, p->m, ctx->C.n, xi2 + 2 * tot, (float*)(xi2 + box_offset(tot)), st),
+       "boxes");
   // tol > 0 (fp64, n <= 128: the team instantiation's shapes): the first launch
   // exits once some sweep is known to be globally converged (BMPC_F_POLL), so
   // a solve that converges at sweep t costs about t + (t + 1) sweeps instead of
   // max_iter + (t + 1).  The re-run uses the same instantiation, without polling.
-  const int tb = (o->tol > 0.0 && o->precision == 0 && ctx->C.npad <= 128) ? BMPC_F_TEAM_BUILD : 0;
   const int poll = tb ? BMPC_F_POLL : 0;
   rc = launch_sweeps(ctx, p, xi2, o, M, mode, 0, nullptr, 0, out, st, fsc, words, nullptr, tb | poll);
   if (!rc && L > 0) {

@@ -16,6 +16,11 @@ for spec in "c1::" "c2::" "c3::" "c4:--scenes 128:subset: 128 of the 1024 c4 sce
       -o gpurun_out/prof_${TAG}_${cfg} python tools/profile_solve.py --config $base $args > gpurun_out/ncu_${TAG}_${cfg}.log 2>&1
   python tools/ncu_json.py gpurun_out/prof_${TAG}_${cfg}.ncu-rep $base $prec profiles/ncu_${base}_${prec}.json "$note" > /dev/null \
     && cp profiles/ncu_${base}_${prec}.json gpurun_out/ && echo "ncu $cfg ok"
+  # small text summaries travel back; the reports themselves only for c1 (the
+  # merge back is capped at 64 MiB)
+  ncu -i gpurun_out/prof_${TAG}_${cfg}.ncu-rep --page details > gpurun_out/${TAG}_${cfg}_ncu.txt 2>&1
+  python tools/ncu_srclines.py gpurun_out/prof_${TAG}_${cfg}.ncu-rep 60 > gpurun_out/${TAG}_${cfg}_ncu_lines.txt 2>&1
+  [ "$cfg" != "c1" ] && rm -f gpurun_out/prof_${TAG}_${cfg}.ncu-rep
 done
 timeout 600 python bench.py --steps 20 --warmup 3 > gpurun_out/bench_${TAG}_c1.log 2>&1
 for cfg in c2 c3 c4; do
@@ -25,3 +30,4 @@ timeout 1200 python bench.py --config c4 --precision fp32 --steps 3 --warmup 3 >
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_${TAG}_ref.log 2>&1
 bash tools/launch_list.sh ${TAG}
 for f in gpurun_out/bench_${TAG}_*.log; do tail -1 $f | cut -c1-160; done
+du -sh gpurun_out
