@@ -27,6 +27,8 @@ typedef struct {
                       // B_xy [nb][8], B_psi [nb][4] (capi.cu: reduced_qp)
   int const_doubles;  // size of the whole constant image starting at PT (even; the
                       // kernel's shared-memory layout, copied in one bulk transfer)
+  const float* IMGF;  // fp32 copy of the image's basis part (same bmpc_basis_index
+                      // order): the fp32 mode's shared-memory basis
   int refine;         // QP refinement step: bit 0 xy, bit 1 psi
 } bmpc_dev_consts;
 
@@ -59,7 +61,8 @@ enum {
   BMPC_F_HISTORY = 1,   // write residual history rows
   BMPC_F_V = 2,         // write the last tail's clipped speed v (n, L)
   BMPC_F_CARRY = 4,     // write the carried state (for chunked / resumed solves)
-  BMPC_F_F32 = 8,       // mixed precision: fp32 obstacle block
+  BMPC_F_F32 = 8,       // mixed precision: fp32 sample passes and obstacle block, fp64
+                        // QP steps, Gram terms, G and multipliers
   BMPC_F_SCORE = 16,    // fused planner scoring after the last sweep
   BMPC_F_POLL = 32,     // tol > 0: count finished instances per sweep and exit once an
                         // earlier sweep is known to be globally converged
@@ -150,6 +153,16 @@ typedef struct {
 #define BMPC_MAX_WARPS 8  // warps (instances) per CTA; the kernel's launch bound is 32x this
 #endif
 BMPC_HD constexpr bool bmpc_stores_xy(int npad) { return npad <= BMPC_XY_NPAD_MAX; }
+// Doubles of the image's basis part in shared memory: P^T, Pdot^T, Pddot^T in
+// fp64, or in fp32 (the fp32 mode; npad is a multiple of 32, so this is whole).
+BMPC_HD constexpr int bmpc_basis_doubles(int nb, int npad, bool f32) {
+  return f32 ? 3 * nb * npad / 2 : 3 * nb * npad;
+}
+// fp32 mode per-sample arrays (floats, in the team's sample-array region):
+// theta, xdot, ydot, and the ellipse-frame positions (b x, a y), then the fp32
+// copies of the coefficients (32 c_xy pair slots, 16 c_psi).  They fit the
+// fp64 region for every npad (224: 584 of 672 doubles).
+BMPC_HD constexpr int bmpc_f32_sample_doubles(int npad) { return (5 * npad + 48) / 2; }
 BMPC_HD constexpr int bmpc_sample_arrays(int npad) { return bmpc_stores_xy(npad) ? 5 : 3; }
 // Team layout (team = the TW warps sharing one instance): per warp 64 QP
 // doubles + the 32 x 33 transpose buffer + 72 exchange doubles; per team the

@@ -6,12 +6,12 @@
 
 namespace bmpc {
 
-size_t am_solve_smem_bytes(int nb, int npad, int kxs, int kps, int warps, int team);
+size_t am_solve_smem_bytes(int nb, int npad, int kxs, int kps, int warps, int team, bool f32);
 
 template <int NB, int NKM, bool F32, bool TEAMS = false, bool XS = false, bool CULL = false>
 static cudaError_t launch_t(const bmpc_dev_consts& C, const bmpc_solve_args& A, int warps,
                             cudaStream_t st, size_t xs_bytes = 0) {
-  const size_t smem = am_solve_smem_bytes(NB, C.npad, C.kxs, C.kps, warps, A.team) + xs_bytes;
+  const size_t smem = am_solve_smem_bytes(NB, C.npad, C.kxs, C.kps, warps, A.team, F32) + xs_bytes;
   auto kfn = am_solve_kernel<NB, NKM, F32, TEAMS, XS, CULL>;
   // raise the dynamic shared-memory limit once per device and size (a driver
   // call per launch costs microseconds of host time on the critical path)
@@ -44,7 +44,7 @@ static size_t xs_stage_bytes(const bmpc_dev_consts& C, const bmpc_solve_args& A,
   int dev = 0;
   cudaGetDevice(&dev);
   if (!optin[dev & 15]) cudaDeviceGetAttribute(&optin[dev & 15], cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const size_t base = am_solve_smem_bytes(C.nb, C.npad, C.kxs, C.kps, warps, 1);
+  const size_t base = am_solve_smem_bytes(C.nb, C.npad, C.kxs, C.kps, warps, 1, false);
   return base + xs <= (size_t)optin[dev & 15] ? xs : 0;
 }
 

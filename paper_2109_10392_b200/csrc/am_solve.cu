@@ -7,12 +7,17 @@
 
 namespace bmpc {
 
-size_t am_solve_smem_bytes(int nb, int npad, int kxs, int kps, int warps, int team) {
-  // the constant image (am_args.h) and the per-team scratch
+size_t am_solve_smem_bytes(int nb, int npad, int kxs, int kps, int warps, int team, bool f32) {
+  // the constant image (am_args.h; the fp32 mode holds its basis in fp32) and
+  // the per-team scratch
   (void)kxs;
   (void)kps;
-  return sizeof(double) *
-         (bmpc_const_image_doubles(nb, npad) + (size_t)(warps / team) * bmpc_team_doubles(npad, team));
+  static_assert(bmpc_f32_sample_doubles(64) <= 5 * 64 && bmpc_f32_sample_doubles(128) <= 5 * 128 &&
+                    bmpc_f32_sample_doubles(224) <= 3 * 224 && bmpc_f32_sample_doubles(256) <= 3 * 256,
+                "fp32 sample arrays must fit the fp64 region");
+  return sizeof(double) * (bmpc_const_image_doubles(nb, npad) - bmpc_basis_doubles(nb, npad, false) +
+                           bmpc_basis_doubles(nb, npad, f32) +
+                           (size_t)(warps / team) * bmpc_team_doubles(npad, team));
 }
 
 #define BMPC_DECL(NB)                                                                      \

@@ -306,10 +306,13 @@ __device__ __forceinline__ void obstacle_term_f32(double xs, double ys, double2 
 // Basis rows at the slots of a chunk: with PAIRED the NS == 2 slots are an even
 // slot pair (samples k and k + 32), adjacent in the paired-slot image, so one
 // 16-byte load returns both; otherwise one load per slot.
-template <int NS, bool PAIRED, int NPAD>
-__device__ __forceinline__ void basis1(const double* B, int i, const int (&k)[NS], double (&v)[NS]) {
+// (T = double, or float for the fp32 mode's basis: the same index order)
+template <class T> struct vec2_of { using type = double2; };
+template <> struct vec2_of<float> { using type = float2; };
+template <int NS, bool PAIRED, int NPAD, class T>
+__device__ __forceinline__ void basis1(const T* B, int i, const int (&k)[NS], T (&v)[NS]) {
   if constexpr (PAIRED && NS == 2) {
-    const double2 w = *reinterpret_cast<const double2*>(B + bmpc_basis_index(i, k[0], NPAD));
+    const auto w = *reinterpret_cast<const typename vec2_of<T>::type*>(B + bmpc_basis_index(i, k[0], NPAD));
     v[0] = w.x;
     v[1] = w.y;
   } else {
@@ -317,10 +320,10 @@ __device__ __forceinline__ void basis1(const double* B, int i, const int (&k)[NS
     for (int s = 0; s < NS; ++s) v[s] = B[bmpc_basis_index(i, k[s], NPAD)];
   }
 }
-template <int NS, bool PAIRED, int NPAD>
-__device__ __forceinline__ void basis3(const double* B0, const double* B1, const double* B2, int i,
-                                       const int (&k)[NS], double (&v0)[NS], double (&v1)[NS],
-                                       double (&v2)[NS]) {
+template <int NS, bool PAIRED, int NPAD, class T>
+__device__ __forceinline__ void basis3(const T* B0, const T* B1, const T* B2, int i,
+                                       const int (&k)[NS], T (&v0)[NS], T (&v1)[NS],
+                                       T (&v2)[NS]) {
   basis1<NS, PAIRED, NPAD>(B0, i, k, v0);
   basis1<NS, PAIRED, NPAD>(B1, i, k, v1);
   basis1<NS, PAIRED, NPAD>(B2, i, k, v2);
@@ -732,6 +735,221 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
   BMPC_PROF_NS(13);
 }
 
+// ---------------------------------------------------------------------------
+// fp32 mode obstacle block (BMPC_F_F32): the exact form of the fp64 block in
+// single precision.  Positions come from pass A's fp32 ellipse-frame samples,
+// predictions from the fp32 ellipse-frame copy (xs32, NaN past the prefilter
+// bound); a term whose fp32 r^2 is NaN (that bound, or a NaN input) takes the
+// fp64 test on the fp64 pair, so non-finite values propagate as in fp64 mode
+// and far predictions never decide in fp32.  The inside residuals r_j =
+// w - (a cos, b sin) and their squares accumulate in fp32 per lane.
+struct TailArgs32 {
+  const float* P;            // fp32 basis (shared memory)
+  const float *xs, *ys;      // pass A's ellipse-frame samples (b x, a y)
+  const float2* xf;          // fp32 ellipse-frame predictions (global)
+  const double2* xi;         // fp64 ellipse-frame predictions (NaN fallback)
+  int n, m;
+  float a, b, ia, ib, ab2;   // ab2 = (ab)^2 rounded to fp32
+  double da, db, dia, dib, dab2;
+  const float4* box;         // [slot][m] obstacle boxes (culling) or nullptr
+  float tc;
+};
+
+template <int NS>
+__device__ __forceinline__ void obstacle_term32(const TailArgs32& T, float px, float py, float r2,
+                                                float& srx, float& sry, float& sq) {
+  const float ri = rsqrtf(r2);
+  const bool pos = r2 > 0.f;  // r = 0 -> (cos, sin) = (1, 0) (_speedups.pyx:158-166)
+  const float ca = pos ? px * ri : 1.f, sa = pos ? py * ri : 0.f;
+  const float rx = fmaf(px, T.ib, -T.a * ca), ry = fmaf(py, T.ia, -T.b * sa);
+  sq = fmaf(rx, rx, fmaf(ry, ry, sq));
+  srx += rx;
+  sry += ry;
+}
+
+template <int NS, int NB, int NPAD, int U, bool PAIRED, bool CULL>
+__device__ __forceinline__ void obstacle_block_f32(const TailArgs32& T, const int (&k)[NS], int j0, int js,
+                                                   int group, bool valid, bool leader, float (&Gx)[NB],
+                                                   float (&Gy)[NB], float& sqo) {
+  float x[NS], y[NS], srx[NS], sry[NS], sq[NS];
+  bool hit[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    x[s] = valid ? T.xs[k[s]] : 0.f;
+    y[s] = valid ? T.ys[k[s]] : 0.f;
+    srx[s] = sry[s] = sq[s] = 0.f;
+    hit[s] = false;
+  }
+  // one term of obstacle jj at sample s, prediction q
+  auto term = [&](int s, float2 q, int jj) {
+    const float px = x[s] - q.x, py = y[s] - q.y;
+    const float r2 = fmaf(px, px, py * py);
+    if (!(r2 >= T.ab2)) {  // inside, or NaN
+      if (r2 == r2) {
+        obstacle_term32<NS>(T, px, py, r2, srx[s], sry[s], sq[s]);
+        hit[s] = true;
+      } else {  // rare: the fp64 test and term on the fp64 pair
+        const double2 q64 = __ldg(T.xi + jj * T.n + k[s]);
+        const double dx = (double)x[s] - q64.x, dy = (double)y[s] - q64.y;
+        const double d2 = fma(dx, dx, dy * dy);
+        if (!(d2 >= T.dab2)) {
+          const double ri = rsqrt_nb(d2);
+          const double ca = d2 > 0.0 ? dx * ri : 1.0, sa = dy * ri;
+          const double rx = fma(dx, T.dib, -T.da * ca), ry = fma(dy, T.dia, -T.db * sa);
+          sq[s] = (float)fma(rx, rx, fma(ry, ry, (double)sq[s]));
+          srx[s] += (float)rx;
+          sry[s] += (float)ry;
+          hit[s] = true;
+        }
+      }
+    }
+  };
+  const int qstep = js * T.n;
+  if (CULL && js == 1) {
+    // whole slots: cull obstacles whose box is at least ab away from the
+    // warp's sample box (the fp32 samples are exact values: no outward rounding)
+    constexpr int UC = NS == 2 ? 2 : (NPAD > 128 ? 8 : 4);
+    float bx0[NS], bx1[NS], by0[NS], by1[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      float lx = INFINITY, hx = -INFINITY, ly = INFINITY, hy = -INFINITY;
+      if (valid) {
+        const bool nan = x[s] != x[s] || y[s] != y[s];
+        lx = nan ? -INFINITY : x[s];
+        hx = nan ? INFINITY : x[s];
+        ly = nan ? -INFINITY : y[s];
+        hy = nan ? INFINITY : y[s];
+      }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        lx = fminf(lx, __shfl_xor_sync(BMPC_FULL, lx, o));
+        hx = fmaxf(hx, __shfl_xor_sync(BMPC_FULL, hx, o));
+        ly = fminf(ly, __shfl_xor_sync(BMPC_FULL, ly, o));
+        hy = fmaxf(hy, __shfl_xor_sync(BMPC_FULL, hy, o));
+      }
+      bx0[s] = lx, bx1[s] = hx, by0[s] = ly, by1[s] = hy;
+    }
+    const int lane = threadIdx.x & 31;
+    for (int c0 = 0; c0 < T.m; c0 += 32) {
+      const int jl = c0 + lane;
+      bool keep = false;
+      if (jl < T.m) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          const float4 bo = __ldg(T.box + (k[s] >> 5) * T.m + jl);
+          const float gx = fmaxf(fmaxf(bo.x - bx1[s], bx0[s] - bo.y), 0.f);
+          const float gy = fmaxf(fmaxf(bo.z - by1[s], by0[s] - bo.w), 0.f);
+          keep |= !(fmaf(gx, gx, gy * gy) >= T.tc);
+        }
+      }
+      unsigned bits = __ballot_sync(BMPC_FULL, keep);
+      while (bits) {
+        int jj[UC];
+        bool on[UC];
+#pragma unroll
+        for (int u = 0; u < UC; ++u) {
+          on[u] = bits != 0u;
+          jj[u] = on[u] ? c0 + __ffs(bits) - 1 : 0;
+          bits &= bits - 1u;
+        }
+        float2 q[NS][UC];
+#pragma unroll
+        for (int u = 0; u < UC; ++u)
+#pragma unroll
+          for (int s = 0; s < NS; ++s)
+            q[s][u] = (on[u] && valid) ? __ldg(T.xf + jj[u] * T.n + k[s]) : make_float2(1e30f, 1e30f);
+        if (valid) {
+#pragma unroll
+          for (int u = 0; u < UC; ++u)
+#pragma unroll
+            for (int s = 0; s < NS; ++s)
+              if (on[u]) term(s, q[s][u], jj[u]);
+        }
+      }
+    }
+  } else if (valid) {
+    const float2* qp[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) qp[s] = T.xf + j0 * T.n + k[s];
+    int j = j0;
+    // software pipeline: the next group's predictions in flight (L2)
+    float2 qn[NS][U];
+    if (j + (U - 1) * js < T.m) {
+#pragma unroll
+      for (int s = 0; s < NS; ++s)
+#pragma unroll
+        for (int u = 0; u < U; ++u) qn[s][u] = __ldg(qp[s] + u * qstep);
+    }
+#pragma unroll 1
+    for (; j + (U - 1) * js < T.m; j += U * js) {
+      float2 q[NS][U];
+#pragma unroll
+      for (int s = 0; s < NS; ++s)
+#pragma unroll
+        for (int u = 0; u < U; ++u) q[s][u] = qn[s][u];
+      if (j + (2 * U - 1) * js < T.m) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+#pragma unroll
+          for (int u = 0; u < U; ++u) qn[s][u] = __ldg(qp[s] + (U + u) * qstep);
+      }
+      bool any = false;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          const float px = x[s] - q[s][u].x, py = y[s] - q[s][u].y;
+          any |= !(fmaf(px, px, py * py) >= T.ab2);
+        }
+      if (any) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int s = 0; s < NS; ++s) term(s, q[s][u], j + u * js);
+      }
+#pragma unroll
+      for (int s = 0; s < NS; ++s) qp[s] += U * qstep;
+    }
+    for (; j < T.m; j += js) {
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        term(s, __ldg(qp[s]), j);
+        qp[s] += qstep;
+      }
+    }
+  }
+  if (NS == 1 && group > 1) {  // split slot: combine the group's partial sums
+    for (int o = 1; o < group; o <<= 1) {
+      srx[0] += __shfl_xor_sync(BMPC_FULL, srx[0], o);
+      sry[0] += __shfl_xor_sync(BMPC_FULL, sry[0], o);
+      sq[0] += __shfl_xor_sync(BMPC_FULL, sq[0], o);
+      hit[0] |= __shfl_xor_sync(BMPC_FULL, (int)hit[0], o) != 0;
+    }
+  }
+  // P^T sum_j g_j = m (P^T P) c - P^T sum_inside r_j (the Gram part in fp64, (6))
+  const bool own = valid && leader;
+  bool any = false;
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    sqo += own ? sq[s] : 0.f;
+    any |= own && hit[s];
+    srx[s] = own ? -srx[s] : 0.f;
+    sry[s] = own ? -sry[s] : 0.f;
+  }
+  if (__any_sync(BMPC_FULL, any)) {
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      float p[NS];
+      basis1<NS, PAIRED, NPAD>(T.P, i, k, p);
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        Gx[i] = fmaf(p[s], srx[s], Gx[i]);
+        Gy[i] = fmaf(p[s], sry[s], Gy[i]);
+      }
+    }
+  }
+}
+
 template <int NB, int NKM, bool F32, bool TEAMS, bool XS, bool CULL>
 #ifndef BMPC_MINB
 #define BMPC_MINB 1
@@ -775,8 +993,11 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
   // (bmpc_basis_index); two-slot chunks are then even slot pairs (one warp per
   // instance)
   constexpr bool PAIRED = !TEAMS && (npad % 64) == 0;
-  double* sPT = sm;                  // P^T, Pdot^T, Pddot^T
-  double* sM = sPT + 3 * NB * npad;  // m P^T P + Pddot^T Pddot (written above)
+  // fp32 mode: the basis sits in shared memory in fp32 (half the bytes); the
+  // few fp64 basis reads (initial targets, fused scoring) go to the global image
+  constexpr int kBasisD = bmpc_basis_doubles(NB, npad, F32);
+  double* sPT = sm;                  // P^T, Pdot^T, Pddot^T (fp64 mode)
+  double* sM = sPT + kBasisD;        // m P^T P + Pddot^T Pddot (+ Pdot^T Pdot in fp32 mode)
   double* sMp = sM + NB * C.kms;     // P^T P
   double* sMdd = sMp + NB * C.kms;   // Pddot^T Pddot
   double* sMd = sMdd + NB * C.kms;   // Pdot^T Pdot
@@ -828,9 +1049,12 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
   const int ipb = W / TW;
   const int first_inst = blockIdx.x * ipb;
   const int scene0 = first_inst / A.l;
-  double* sXi = sm + C.const_doubles + (size_t)ipb * bmpc_team_doubles(npad, TW);
+  const int img_doubles = C.const_doubles - 3 * NB * npad + kBasisD;  // in shared memory
+  double* sXi = sm + img_doubles + (size_t)ipb * bmpc_team_doubles(npad, TW);
   if (threadIdx.x == 0) {
-    const unsigned bytes = (unsigned)C.const_doubles * 8u;
+    // fp32 mode: the fp32 basis, then the image past its fp64 basis
+    const unsigned bbytes = (unsigned)kBasisD * 8u;
+    const unsigned bytes = (unsigned)img_doubles * 8u;
     unsigned xbytes = 0;
     if constexpr (XS) {
       const int last_inst = min(A.L, first_inst + ipb) - 1;
@@ -839,9 +1063,12 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
     mbar_init(&s_cbar, 1);
     mbar_arrive_expect_tx(&s_cbar, bytes + xbytes);
     constexpr unsigned kChunk = 16384;
-    for (unsigned o = 0; o < bytes; o += kChunk)
-      bulk_copy_g2s(reinterpret_cast<char*>(sm) + o, reinterpret_cast<const char*>(C.IMG) + o,
-                    bytes - o < kChunk ? bytes - o : kChunk, &s_cbar);
+    const char* src0 = F32 ? reinterpret_cast<const char*>(C.IMGF) : reinterpret_cast<const char*>(C.IMG);
+    const char* src1 = reinterpret_cast<const char*>(C.IMG + 3 * NB * npad);
+    for (unsigned o = 0; o < bbytes; o += kChunk)
+      bulk_copy_g2s(reinterpret_cast<char*>(sm) + o, src0 + o, min(kChunk, bbytes - o), &s_cbar);
+    for (unsigned o = bbytes; o < bytes; o += kChunk)
+      bulk_copy_g2s(reinterpret_cast<char*>(sm) + o, src1 + (o - bbytes), min(kChunk, bytes - o), &s_cbar);
     if constexpr (XS) {
       const char* src = reinterpret_cast<const char*>(A.xis) + (size_t)scene0 * A.m * n * 16;
       for (unsigned o = 0; o < xbytes; o += kChunk)
@@ -855,18 +1082,35 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
     // the G Gram block of this launch's obstacle count: m P^T P + Pddot^T Pddot
     // (overwrites the image's F_axis^T F_axis block, which the sweep never reads)
     const double md = (double)A.m;
-    double* g = sm + 3 * NB * npad;
+    double* g = sm + kBasisD;
+    // fp32 mode: + Pdot^T Pdot, the whole F_axis^T F_axis (its sweep adds only
+    // the small residual contractions to it, see (6))
     for (int q = threadIdx.x; q < NB * C.kms; q += blockDim.x)
-      g[q] = fma(md, g[NB * C.kms + q], g[2 * NB * C.kms + q]);
+      g[q] = F32 ? fma(md, g[NB * C.kms + q], g[2 * NB * C.kms + q]) + g[3 * NB * C.kms + q]
+                 : fma(md, g[NB * C.kms + q], g[2 * NB * C.kms + q]);
     __syncthreads();
   }
 
   const int inst = blockIdx.x * (W / TW) + team;
   if (inst >= L) return;  // team-uniform; no block-wide barriers below this point
 
-  const double* __restrict__ sP = sPT;
-  const double* __restrict__ sPd = sPT + NB * npad;
-  const double* __restrict__ sPdd = sPT + 2 * NB * npad;
+  // fp64 basis: shared memory, or the global image in the fp32 mode (read only
+  // by the initial targets and the fused scoring there)
+  const double* __restrict__ sP = F32 ? C.IMG : sPT;
+  const double* __restrict__ sPd = sP + NB * npad;
+  const double* __restrict__ sPdd = sP + 2 * NB * npad;
+  // fp32 mode: the shared-memory basis, per-sample arrays and coefficient copies
+  const float* __restrict__ fP = reinterpret_cast<const float*>(sm);
+  const float* __restrict__ fPd = fP + NB * npad;
+  const float* __restrict__ fPdd = fP + 2 * NB * npad;
+  float* const fth = reinterpret_cast<float*>(arr);  // theta
+  float* const fxd = fth + npad;                      // xdot, ydot
+  float* const fyd = fxd + npad;
+  float* const fxs = fyd + npad;                      // ellipse-frame b x, a y
+  float* const fys = fxs + npad;
+  float* const fcxy = fys + npad;                     // 32: (c_x[i], c_y[i]) pairs
+  float* const fcp = fcxy + 32;                       // 16: c_psi
+  using R = std::conditional_t<F32, float, double>;   // sample-pass arithmetic
   // basis value (row i of sP / sPd / sPdd) at sample k
   auto bi = [](int i, int k) { return bmpc_basis_index(i, k, npad); };
   const double2* __restrict__ xi =
@@ -957,7 +1201,6 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
       lamp = cr[2 * NB + li];
       G = cr[(yax ? 4 : 3) * NB + li];
     }
-#pragma unroll
     // the previous sweep's coefficients: the refinement base
     if (owner) cown = cr[5 * NB + (yax ? RX : 0) + li];
     if (owner && !yax) cpown = cr[5 * NB + 2 * RX + li];
@@ -1096,6 +1339,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
       if (refine_xy) c = qp_refine(zr, sHx + lrow * C.kms, rhs, c, hbase, XM0, XM1, xfree);
       cown = c;
       if (owner) ws.cxy[2 * li + (yax ? 1 : 0)] = c;
+      if (F32 && owner) fcxy[2 * li + (yax ? 1 : 0)] = (float)c;
       __syncwarp();
     }
     BMPC_PROF(1);
@@ -1107,14 +1351,14 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
     //     Acceleration block (_speedups.pyx:179-198) in exact form: unclipped
     //     samples give g_acc = (xddot, yddot) and r = 0, so Pddot^T g_acc =
     //     (Pddot^T Pddot) c plus a sparse correction from the clipped samples.
-    double pth;                     // owner lanes: P^T theta
-    double Gx[NB], Gy[NB], pt[NB];  // Gx, Gy: lane partials of F_axis^T g beyond the Gram terms
+    double pth;                // owner lanes: P^T theta
+    R Gx[NB], Gy[NB], pt[NB];  // Gx, Gy: lane partials of F_axis^T g beyond the Gram terms
 #pragma unroll
-    for (int i = 0; i < NB; ++i) Gx[i] = Gy[i] = pt[i] = 0.0;
-    double sqo = 0.0, sqa = 0.0, sqn = 0.0;
+    for (int i = 0; i < NB; ++i) Gx[i] = Gy[i] = pt[i] = 0;
+    R sqo = 0, sqa = 0, sqn = 0;
     {
       bool wrap = false;
-      double prev_last = 0.0;  // theta of sample 32 r - 1: lane 31 of the previous slot
+      R prev_last = 0;  // theta of sample 32 r - 1: lane 31 of the previous slot
       const double amax2 = A.a_max * A.a_max;
       // this warp's slots r = wt, wt + TW, ... in chunks of CH (every slot of a
       // chunk valid at compile time); chunks stay rolled for the instruction cache
@@ -1215,23 +1459,120 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
           }
         }
       };
+      // fp32 mode pass A: the same chunk in single precision (no teams); the
+      // samples for pass B and the obstacle block are stored in fp32, the
+      // positions already in the ellipse frame
+      const float amax2f = (float)(A.a_max * A.a_max), amaxf = (float)A.a_max;
+      const float af = (float)a, bf = (float)b;
+      auto chunk_a32 = [&](auto nsc, const int r0) {
+        constexpr int NSC = decltype(nsc)::value;
+        int k[NSC];
+        bool v[NSC];
+        float xx[NSC], yy[NSC], xd[NSC], yd[NSC], xdd[NSC], ydd[NSC];
+#pragma unroll
+        for (int s = 0; s < NSC; ++s) {
+          k[s] = lane + 32 * (r0 + s);
+          v[s] = k[s] < n;
+          xx[s] = yy[s] = xd[s] = yd[s] = xdd[s] = ydd[s] = 0.f;
+        }
+        const float2* __restrict__ cf = reinterpret_cast<const float2*>(fcxy);
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+          const float2 c = cf[i];
+          float p[NSC], pd[NSC], pdd[NSC];
+          basis3<NSC, PAIRED, npad>(fP, fPd, fPdd, i, k, p, pd, pdd);
+#pragma unroll
+          for (int s = 0; s < NSC; ++s) {
+            xx[s] = fmaf(p[s], c.x, xx[s]);
+            yy[s] = fmaf(p[s], c.y, yy[s]);
+            xd[s] = fmaf(pd[s], c.x, xd[s]);
+            yd[s] = fmaf(pd[s], c.y, yd[s]);
+            xdd[s] = fmaf(pdd[s], c.x, xdd[s]);
+            ydd[s] = fmaf(pdd[s], c.y, ydd[s]);
+          }
+        }
+        float th[NSC];
+        bool clip[NSC], anyclip = false;
+#pragma unroll
+        for (int s = 0; s < NSC; ++s) th[s] = atan2_f32_nb(yd[s], xd[s]);
+#pragma unroll
+        for (int s = 0; s < NSC; ++s) {
+          float prev = __shfl_up_sync(BMPC_FULL, th[s], 1);
+          const float lst = __shfl_sync(BMPC_FULL, th[s], 31);
+          if (lane == 0) prev = prev_last;
+          prev_last = lst;
+          if (v[s] && k[s] > 0 && !(fabsf(th[s] - prev) < 3.14159265f)) wrap = true;
+          if (v[s]) {
+            fth[k[s]] = th[s];
+            fxd[k[s]] = xd[s];
+            fyd[k[s]] = yd[s];
+            fxs[k[s]] = xx[s] * bf;
+            fys[k[s]] = yy[s] * af;
+          } else {
+            th[s] = 0.f;
+          }
+          clip[s] = v[s] && fmaf(xdd[s], xdd[s], ydd[s] * ydd[s]) > amax2f;
+          anyclip |= clip[s];
+        }
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+          float p[NSC];
+          basis1<NSC, PAIRED, npad>(fP, i, k, p);
+#pragma unroll
+          for (int s = 0; s < NSC; ++s) pt[i] = fmaf(p[s], th[s], pt[i]);
+        }
+        if (__any_sync(BMPC_FULL, anyclip)) {  // clipped samples: g = a_max (cos, sin)
+          float ex[NSC], ey[NSC];
+#pragma unroll
+          for (int s = 0; s < NSC; ++s) {
+            const float m2 = fmaf(xdd[s], xdd[s], ydd[s] * ydd[s]);
+            const float mi = rsqrtf(m2);
+            ex[s] = clip[s] ? amaxf * (xdd[s] * mi) - xdd[s] : 0.f;
+            ey[s] = clip[s] ? amaxf * (ydd[s] * mi) - ydd[s] : 0.f;
+            sqa = fmaf(ex[s], ex[s], fmaf(ey[s], ey[s], sqa));
+          }
+#pragma unroll
+          for (int i = 0; i < NB; ++i) {
+            float pdd[NSC];
+            basis1<NSC, PAIRED, npad>(fPdd, i, k, pdd);
+#pragma unroll
+            for (int s = 0; s < NSC; ++s) {
+              Gx[i] = fmaf(pdd[s], ex[s], Gx[i]);
+              Gy[i] = fmaf(pdd[s], ey[s], Gy[i]);
+            }
+          }
+        }
+      };
       int r0 = wt;
+      if constexpr (F32) {
 #pragma unroll kChunkUnrollA
-      for (; r0 + (CH - 1) * TW < NKM; r0 += CH * TW) chunk_a(std::integral_constant<int, CH>{}, r0);
+        for (; r0 + (CH - 1) < NKM; r0 += CH) chunk_a32(std::integral_constant<int, CH>{}, r0);
 #pragma unroll 1
-      for (; CH > 1 && r0 < NKM; r0 += TW) chunk_a(std::integral_constant<int, 1>{}, r0);  // remainder
+        for (; CH > 1 && r0 < NKM; r0 += 1) chunk_a32(std::integral_constant<int, 1>{}, r0);
+      } else {
+#pragma unroll kChunkUnrollA
+        for (; r0 + (CH - 1) * TW < NKM; r0 += CH * TW) chunk_a(std::integral_constant<int, CH>{}, r0);
+#pragma unroll 1
+        for (; CH > 1 && r0 < NKM; r0 += TW) chunk_a(std::integral_constant<int, 1>{}, r0);  // remainder
+      }
       BMPC_PROF(2);
       // P^T theta of this warp's slots (again after an unwrap)
       auto pt_slots = [&]() {
 #pragma unroll
-        for (int i = 0; i < NB; ++i) pt[i] = 0.0;
+        for (int i = 0; i < NB; ++i) pt[i] = 0;
 #pragma unroll 1
         for (int r = wt; r < NKM; r += TW) {
           const int k = lane + 32 * r;
           if (k < n) {
-            const double t = ws.th[k];
+            if constexpr (F32) {
+              const float t = fth[k];
 #pragma unroll
-            for (int i = 0; i < NB; ++i) pt[i] = fma(sP[bi(i, k)], t, pt[i]);
+              for (int i = 0; i < NB; ++i) pt[i] = fmaf(fP[bi(i, k)], t, pt[i]);
+            } else {
+              const double t = ws.th[k];
+#pragma unroll
+              for (int i = 0; i < NB; ++i) pt[i] = fma(sP[bi(i, k)], t, pt[i]);
+            }
           }
         }
       };
@@ -1246,7 +1587,10 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
       if (TW == 1) {
         if (__any_sync(BMPC_FULL, wrap)) {  // rare: exact numpy unwrap, then P^T theta again
           __syncwarp();
-          if (lane == 0) np_unwrap_serial(ws.th, n);
+          if (lane == 0) {
+            if constexpr (F32) np_unwrap_serial_f(fth, n);
+            else np_unwrap_serial(ws.th, n);
+          }
           __syncwarp();
           pt_slots();
         }
@@ -1284,7 +1628,33 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
     // (3) obstacle block (exact form, independent of psi), samples dealt as in
     //     slot(): full slots two at a time, the n % 32 leftover samples split
     //     over lane groups.
-    {
+    if constexpr (F32) {
+      const double abd = a * b;
+      TailArgs32 T{fP, fxs, fys, xf, xis, n, m, (float)a, (float)b, (float)inv_a, (float)inv_b,
+                   (float)(abd * abd), a, b, inv_a, inv_b, abd * abd,
+                   CULL ? reinterpret_cast<const float4*>(A.boxes) + (size_t)(inst / A.l) * ((n + 31) >> 5) * m
+                        : nullptr,
+                   __double2float_ru(abd * abd * (1.0 + 1e-4))};
+      int r = 0;
+      if (kPairSlots<NB>) {
+#pragma unroll 1
+        for (; r + 1 < sl.F; r += 2) {
+          const int ks[2] = {lane + 32 * r, lane + 32 * (r + 1)};
+          obstacle_block_f32<2, NB, npad, BMPC_UPAIR, PAIRED, CULL>(T, ks, 0, 1, 0, true, true, Gx, Gy, sqo);
+        }
+      }
+#pragma unroll 1
+      for (; r < nslots; ++r) {
+        const Slot S = slot(r, lane, sl);
+        const int ks[1] = {S.k};
+        if (r < sl.F)
+          obstacle_block_f32<1, NB, npad, BMPC_USINGLE, false, CULL>(T, ks, S.j0, S.js, 1, S.valid, S.leader,
+                                                                      Gx, Gy, sqo);
+        else
+          obstacle_block_f32<1, NB, npad, (NKM >= 7 ? BMPC_USPLIT_MANY : BMPC_USPLIT), false, false>(
+              T, ks, S.j0, S.js, sl.g, S.valid, S.leader, Gx, Gy, sqo);
+      }
+    } else {
       TailArgs T{sP, cxy, xis, xf, kStoreXY ? ws.x : nullptr, kStoreXY ? ws.y : nullptr, n, m, a, b,
                  inv_a, inv_b, __double2float_ru((a * b) * (a * b) * 1.02),
                  __double2float_rd(prefilter_lim(a, b)),
@@ -1321,6 +1691,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
       if (refine_psi) c = qp_refine(zr, sHp + lrow * C.kms, rhs, c, 0, PM0, PM1, pfree);
       cpown = c;
       if (!yax && owner) ws.cp[li] = c;
+      if (F32 && !yax && owner) fcp[li] = (float)c;
       __syncwarp();
     }
     BMPC_PROF(4);
@@ -1329,9 +1700,9 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
     //     contracted onto Pdot.
     // full chunks of CH slots (every slot valid at compile time), then the
     // NKM % CH remainder; chunks stay rolled for the instruction cache
-    double cps_reg[NB];  // c_psi, held in registers for every chunk
+    R cps_reg[NB];  // c_psi, held in registers for every chunk
 #pragma unroll
-    for (int i = 0; i < NB; ++i) cps_reg[i] = ws.cp[i];
+    for (int i = 0; i < NB; ++i) cps_reg[i] = F32 ? (R)fcp[i] : (R)ws.cp[i];
     auto chunk_b = [&](auto nsc, const int r0) {
       constexpr int NSC = decltype(nsc)::value;
       int k[NSC];
@@ -1395,8 +1766,8 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
         gnx[s] = v[s] ? u * cps[s] : 0.0;
         gny[s] = v[s] ? u * sps[s] : 0.0;
         const double rnx = xd - gnx[s], rny = yd - gny[s];
-        const double q = fma(rnx, rnx, fma(rny, rny, sqn));
-        sqn = v[s] ? q : sqn;
+        const double q = fma(rnx, rnx, fma(rny, rny, (double)sqn));
+        sqn = v[s] ? (R)q : sqn;
       }
       if (last && (A.flags & BMPC_F_V)) {
 #pragma unroll
@@ -1414,12 +1785,79 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
         }
       }
     };
+    // fp32 mode pass B: psi, sin/cos, the clipped speed and the non-holonomic
+    // residual in single precision; contracted as Pdot^T (g_nh - xdot), the
+    // small part of Pdot^T g_nh (the Gram part Pdot^T Pdot c is added in fp64)
+    auto chunk_b32 = [&](auto nsc, const int r0) {
+      constexpr int NSC = decltype(nsc)::value;
+      int k[NSC];
+      bool v[NSC];
+      float ps[NSC], ps1[NSC];
+#pragma unroll
+      for (int s = 0; s < NSC; ++s) {
+        k[s] = lane + 32 * (r0 + s);
+        v[s] = k[s] < n;
+        ps[s] = ps1[s] = 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        float p[NSC];
+        basis1<NSC, PAIRED, npad>(fP, i, k, p);
+#pragma unroll
+        for (int s = 0; s < NSC; ++s) {
+          if (i & 1) ps1[s] = fmaf(p[s], cps_reg[i], ps1[s]);
+          else ps[s] = fmaf(p[s], cps_reg[i], ps[s]);
+        }
+      }
+      float sps[NSC], cps[NSC];
+      bool big = false;
+#pragma unroll
+      for (int s = 0; s < NSC; ++s) {
+        ps[s] += ps1[s];
+        sincos_f32_nb(ps[s], &sps[s], &cps[s]);
+        big |= !(fabsf(ps[s]) < 1.0e4f);
+      }
+      if (big) {
+#pragma unroll
+        for (int s = 0; s < NSC; ++s)
+          if (!(fabsf(ps[s]) < 1.0e4f)) sincosf(ps[s], &sps[s], &cps[s]);
+      }
+      const float vminf = (float)A.v_min, vmaxf = (float)A.v_max;
+      float rnx[NSC], rny[NSC];
+#pragma unroll
+      for (int s = 0; s < NSC; ++s) {
+        const float xd = v[s] ? fxd[k[s]] : 0.f, yd = v[s] ? fyd[k[s]] : 0.f;
+        float u = sqrt_f32_nb(fmaf(xd, xd, yd * yd));
+        u = u < vminf ? vminf : (u > vmaxf ? vmaxf : u);
+        rnx[s] = v[s] ? fmaf(u, cps[s], -xd) : 0.f;  // g_nh - xdot
+        rny[s] = v[s] ? fmaf(u, sps[s], -yd) : 0.f;
+        sqn = fmaf(rnx[s], rnx[s], fmaf(rny[s], rny[s], sqn));
+        if (last && (A.flags & BMPC_F_V) && v[s]) A.v_out[(size_t)k[s] * L + inst] = (double)u;
+      }
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        float pd[NSC];
+        basis1<NSC, PAIRED, npad>(fPd, i, k, pd);
+#pragma unroll
+        for (int s = 0; s < NSC; ++s) {
+          Gx[i] = fmaf(pd[s], rnx[s], Gx[i]);
+          Gy[i] = fmaf(pd[s], rny[s], Gy[i]);
+        }
+      }
+    };
     {
       int r0 = wt;
+      if constexpr (F32) {
 #pragma unroll kChunkUnrollB
-      for (; r0 + (CH - 1) * TW < NKM; r0 += CH * TW) chunk_b(std::integral_constant<int, CH>{}, r0);
+        for (; r0 + (CH - 1) < NKM; r0 += CH) chunk_b32(std::integral_constant<int, CH>{}, r0);
 #pragma unroll 1
-      for (; CH > 1 && r0 < NKM; r0 += TW) chunk_b(std::integral_constant<int, 1>{}, r0);
+        for (; CH > 1 && r0 < NKM; r0 += 1) chunk_b32(std::integral_constant<int, 1>{}, r0);
+      } else {
+#pragma unroll kChunkUnrollB
+        for (; r0 + (CH - 1) * TW < NKM; r0 += CH * TW) chunk_b(std::integral_constant<int, CH>{}, r0);
+#pragma unroll 1
+        for (; CH > 1 && r0 < NKM; r0 += TW) chunk_b(std::integral_constant<int, 1>{}, r0);
+      }
     }
     BMPC_PROF(12);
 
@@ -1502,8 +1940,15 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
         a3[j & 1] = fma(m3[j], cj, a3[j & 1]);
       }
       const double rest = gn;
-      G = (a1[0] + a1[1]) + rest;
-      lam -= rho * ((a3[0] + a3[1]) - rest);
+      if constexpr (F32) {
+        // m1 = F_axis^T F_axis here, gn = F_axis^T (g - F c): G = F_axis^T g and
+        // lambda -= rho F_axis^T (F c - g) from the residual contractions alone
+        G = (a1[0] + a1[1]) + rest;
+        lam += rho * rest;
+      } else {
+        G = (a1[0] + a1[1]) + rest;
+        lam -= rho * ((a3[0] + a3[1]) - rest);
+      }
     }
     // lambda_psi step P^T (psi - theta) = (P^T P) c_psi - P^T theta (solver.py:494),
     // evaluated here where its latency overlaps the residual bookkeeping
@@ -1555,6 +2000,20 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
     // sweep's pass A (the same sequential fma chains as k_score's sampling, so
     // the fused and stand-alone scores agree bit for bit); psi is sampled here
     auto sample = [&](int k, double& x, double& y, double& xd, double& yd, double& ps) {
+      if constexpr (F32) {  // fp64 samples of the final coefficients (global basis)
+        x = y = xd = yd = ps = 0.0;
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+          const double p = sP[bi(i, k)], pd = sPd[bi(i, k)];
+          const double2 c = cxy2[i];
+          x = __fma_rn(p, c.x, x);
+          y = __fma_rn(p, c.y, y);
+          xd = __fma_rn(pd, c.x, xd);
+          yd = __fma_rn(pd, c.y, yd);
+          ps = __fma_rn(p, ws.cp[i], ps);
+        }
+        return;
+      }
       xd = ws.xd[k];
       yd = ws.yd[k];
       ps = 0.0;

@@ -19,7 +19,7 @@
 namespace bmpc {
 cudaError_t launch_am_solve(const bmpc_dev_consts& C, const bmpc_solve_args& A, int warps,
                             cudaStream_t st);
-size_t am_solve_smem_bytes(int nb, int npad, int kxs, int kps, int warps, int team);
+size_t am_solve_smem_bytes(int nb, int npad, int kxs, int kps, int warps, int team, bool f32);
 cudaError_t op_obstacle_update(int n, int l, long long mn, const double* x, const double* y,
                                const double* xi_x, const double* xi_y, double a, double b,
                                double* alpha, double* d, cudaStream_t st);
@@ -296,7 +296,10 @@ int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pd
   // bmpc_ctx_info, the stand-alone kernels), then the image, then the KKT pairs.
   const size_t nimg = bmpc_const_image_doubles(nb, npad);
   const size_t oI = nPT;  // image start (nPT is even: 16-byte aligned)
-  std::vector<double> h(nPT + nimg + 2 * nKx + 2 * nKp, 0.0);
+  // ... and last the fp32 copy of the image's basis part (the fp32 mode's
+  // shared-memory basis; nPT floats = nPT / 2 doubles, nPT even)
+  const size_t oF = nPT + nimg + 2 * nKx + 2 * nKp;
+  std::vector<double> h(oF + nPT / 2, 0.0);
   const double* mats[3] = {P, Pdot, Pddot};
   for (int q = 0; q < 3; ++q)
     for (int i = 0; i < nb; ++i)
@@ -304,6 +307,7 @@ int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pd
         const double v = mats[q][(size_t)k * nb + i];
         h[((size_t)q * nb + i) * npad + k] = v;
         h[oI + bmpc_basis_index(q * nb + i, k, npad)] = v;
+        reinterpret_cast<float*>(h.data() + oF)[bmpc_basis_index(q * nb + i, k, npad)] = (float)v;
       }
   const size_t oM = oI + (size_t)3 * nb * npad;
   for (int i = 0; i < nb; ++i)
@@ -388,6 +392,7 @@ int bmpc_ctx_create(int n, int nb, double rho, const double* P, const double* Pd
   c->C.M = c->dmem + oM;
   c->C.tau = c->dmem + otau;
   c->C.const_doubles = (int)nimg;
+  c->C.IMGF = reinterpret_cast<const float*>(c->dmem + oF);
   c->C.refine = refine;
   c->cond_xy = cond_x;
   c->cond_psi = cond_p;
@@ -447,13 +452,13 @@ static int check_problem(const bmpc_ctx* ctx, const bmpc_problem* p) {
 // Warps (= instances) per CTA: about one CTA per SM for small batches, at most
 // 8 (the register file holds 8 warps of this kernel), and never more than the
 // opt-in shared memory per block allows.
-static int auto_warps(const bmpc_ctx* ctx, int L, int req, int team) {
+static int auto_warps(const bmpc_ctx* ctx, int L, int req, int team, bool f32) {
   // warps per block: a multiple of the team size, about one block per SM
   int ipb = req > 0 ? req / team : (L + ctx->sms - 1) / ctx->sms;
   if (ipb < 1) ipb = 1;
   if (ipb * team > BMPC_MAX_WARPS) ipb = BMPC_MAX_WARPS / team;
   while (ipb > 1 && bmpc::am_solve_smem_bytes(ctx->C.nb, ctx->C.npad, ctx->C.kxs, ctx->C.kps,
-                                              ipb * team, team) > (size_t)ctx->smem_optin)
+                                              ipb * team, team, f32) > (size_t)ctx->smem_optin)
     --ipb;
   return ipb * team;
 }
@@ -536,7 +541,7 @@ static int launch_sweeps(bmpc_ctx* ctx, const bmpc_problem* p, const double* xi2
     A.score = *fsc;
   }
   if (L == 0 || iters <= 0) return BMPC_OK;
-  CK(bmpc::launch_am_solve(ctx->C, A, auto_warps(ctx, L, o->warps_per_block, A.team), st),
+  CK(bmpc::launch_am_solve(ctx->C, A, auto_warps(ctx, L, o->warps_per_block, A.team, o->precision == 1), st),
      "am_solve launch");
   return BMPC_OK;
 }
@@ -649,7 +654,7 @@ static int solve_impl(bmpc_ctx* ctx, const bmpc_problem* p, const bmpc_solve_opt
   int rc = check_problem(ctx, p);
   if (rc) return rc;
   if (!o || !out) return fail(BMPC_EINVAL, "null opts/out");
-  if (o->precision != 0 && o->precision != 1) return fail(BMPC_EINVAL, "precision must be 0 (fp64) or 1 (fp32 obstacle block)");
+  if (o->precision != 0 && o->precision != 1) return fail(BMPC_EINVAL, "precision must be 0 (fp64) or 1 (fp32 sample passes)");
   if (o->max_iter < 1) return fail(BMPC_EINVAL, "max_iter must be >= 1");
   if (o->team_warps != 0 && o->team_warps != 1 && o->team_warps != 2 && o->team_warps != 4)
     return fail(BMPC_EINVAL, "team_warps must be 0, 1, 2 or 4");

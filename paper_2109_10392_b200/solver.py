@@ -226,8 +226,11 @@ def _default_boundary(spec) -> bool:
 
 
 def _precision_code(precision: str) -> int:
-    """"fp64": everything in double; "fp32": the obstacle block in single
-    precision (QP steps, sampling, contractions and multipliers stay fp64)."""
+    """"fp64": everything in double (the reference's arithmetic); "fp32": the
+    per-sample passes in single precision -- sampling, heading atan2 / unwrap,
+    sin/cos, the acceleration, non-holonomic and obstacle blocks and their
+    residual contractions -- while the QP steps, the Gram terms of G and the
+    multipliers stay fp64 (tolerance in DESIGN.md, tests/test_gpu_solver.py)."""
     codes = {"fp64": 0, "fp32": 1}
     if precision not in codes:
         raise ValueError(f"precision must be one of {sorted(codes)}, got {precision!r}")

@@ -88,13 +88,19 @@ def test_solve_and_score_parity(cuda, name):
     del l
 
 
-FP32_TOL = 1e-5  # measured: see DESIGN.md (fp32 mode)
+# fp32 mode (precision="fp32": the per-sample passes in single precision, the
+# QP steps / Gram terms / multipliers in fp64): stated tolerance 5e-5 relative
+# trajectory error; measured on B200 <= 1.2e-5 (c4s), <= 4.4e-6 elsewhere
+# (tools/fp32_report.py).
+FP32_TOL = 5e-5
 
 
-@pytest.mark.parametrize("name", ["c0", "c1", "c2f", "c3s", "c3f", "c4s", "c4f"])
+@pytest.mark.parametrize("name", ["c0", "c1", "c2s", "c2f", "c3s", "c3f", "c4s", "c4f", "reverse"])
 def test_fp32_mode_tolerance(cuda, name):
-    """Mixed-precision mode (fp32 obstacle block) against the reference: the
-    stated tolerance on stable columns; reported, not bit-compatible."""
+    """fp32 mode against the reference: the stated tolerance on stable
+    columns, and the same best / unfiltered / heading+collision argmin indices
+    and feasibility as the reference's fp64 solve (measured identical on every
+    fixture); reported separately, not bit-compatible."""
     from paper_2109_10392_b200.planner import FilterLimits, MetaCostSpec, plan_batch
 
     z = golden(name)
@@ -106,6 +112,11 @@ def test_fp32_mode_tolerance(cuda, name):
     stable = z["screen_div"] <= SCREEN
     print(f"fp32 {name}: max rel traj err {err[stable].max():.3e} median {np.median(err[stable]):.3e}")
     assert err[stable].max() <= FP32_TOL
+    for s in range(int(z["S"])):
+        assert (res.best_index[s] if res.best_index[s] is not None else -1) == int(z["cruise_best_index"][s])
+        assert int(res.argmin_all[s]) == int(z["cruise_argmin_all"][s])
+        assert int(res.argmin_hc[s]) == int(z["cruise_argmin_hc"][s])
+    np.testing.assert_array_equal(res.feasible, z["cruise_feasible"].astype(bool))
 
 
 @pytest.mark.parametrize("name", ["c0", "c2f", "c3s", "c3f", "c4f"])
