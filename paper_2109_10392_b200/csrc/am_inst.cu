@@ -37,9 +37,11 @@ static size_t xs_stage_bytes(const bmpc_dev_consts& C, const bmpc_solve_args& A,
 #ifdef BMPC_NO_XI_STAGE
   return 0;
 #endif
-  if (A.team != 1 || C.npad > 128 || A.m <= 0 || !A.xis || A.l < warps) return 0;
+  if (A.team != 1 || C.npad > 128 || A.m <= 0 || !A.xis || (BMPC_XS32 && !A.xs32) || A.l < warps) return 0;
   const int scenes = (A.S > 1 && A.l % warps != 0) ? 2 : 1;
-  const size_t xs = (size_t)scenes * A.m * C.n * 16;
+  // + the clearance-skipping arrays behind them (BMPC_SKIP: 12 bytes per sample and warp)
+  const size_t xs = (size_t)scenes * A.m * C.n * (BMPC_XS32 ? 8 : 16) +
+                    ((BMPC_SKIP && !BMPC_XS32 && bmpc_stores_xy(C.npad)) ? (size_t)warps * C.npad * 12 : 0);
   static int optin[16] = {0};
   int dev = 0;
   cudaGetDevice(&dev);

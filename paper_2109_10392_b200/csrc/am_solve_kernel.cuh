@@ -271,6 +271,9 @@ struct TailArgs {
   float lim32;    // largest coordinate magnitude the prefilter may decide
   const float4* box;  // [slot][m] obstacle bounding boxes (k_obstacle_boxes) or nullptr
   float tc;           // culling threshold round_up((ab)^2 (1 + 1e-4)) on the squared box gap
+  float2* sk_p0;      // clearance skipping: per sample the recorded frame position
+  float* sk_m0;       //   and squared clearance (-1: never skip), or nullptr
+  float ab_ru;        // a b rounded up to fp32
 };
 
 // fp32 mode inside term (the outside test runs in fp64 in both modes): with
@@ -339,17 +342,62 @@ __device__ __forceinline__ T ldq(const T* p) {
     return __ldg(p);
 }
 
+// BMPC_XS32: staged predictions are the fp32 ellipse-frame copies (half the
+// shared-memory bytes); the obstacle test runs through the exact fp32
+// prefilter on them, undecided terms take the fp64 pair from global memory.
+#ifndef BMPC_XS32
+#define BMPC_XS32 0
+#endif
+// BMPC_SKIP: clearance skipping of whole obstacle slots (staged fp64
+// predictions, one warp per instance, n <= 128).  A pass over a slot records
+// per sample its position P0 (ellipse frame, fp32) and a lower bound M0 of
+// min_j |P0 - Q_j| - ab; while every sample of the slot has moved less than
+// its M0 since then, every term of the slot is outside (triangle inequality)
+// and contributes exactly nothing, so the pass is skipped.  Bit-identical to
+// running it (kSkipSlack covers every fp32 rounding of the test).
+#ifndef BMPC_SKIP
+#define BMPC_SKIP 1
+#endif
+#ifndef BMPC_SKIP_LATE
+#define BMPC_SKIP_LATE 0  // 1: the clearance test in its own loop after pass A's chunks
+#endif
+constexpr float kSkipSlack = 0.02f;    // frame units, >> the test's rounding (2.5e-3 worst case)
+constexpr float kSkipMaxM = 2048.f;    // clearance cap
+constexpr float kSkipMaxP0 = 6000.f;   // |P0| bound: |P| <= 8192 while skipping
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 #ifndef BMPC_PF_SCALE
 #define BMPC_PF_SCALE 1  // obstacles in flight with the prefilter, relative to U (2, 3: slower at c4)
 #endif
-template <int NS, int NB, int NPAD, bool F32, int U, bool XS, bool PAIRED, bool CULL>
+template <int NS, int NB, int NPAD, bool F32, int U, bool XS, bool PAIRED, bool CULL, bool TRACK = false>
 __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)[NS], int j0, int js,
                                                int group, bool valid, bool leader,
                                                double (&Gx)[NB], double (&Gy)[NB], double& sqo) {
+  static_assert(!TRACK || (XS && !F32 && !BMPC_XS32), "clearance tracking: staged fp64 predictions only");
   double x[NS], y[NS], gsx[NS], gsy[NS], sq[NS];  // gsx, gsy: sum of inside residuals
   double cin[NS];                                   // inside terms per sample
+  // TRACK: high word of the smallest r^2 seen per sample (positive doubles order
+  // like their high words; truncation rounds down), and the smallest squared box
+  // gap of the culled obstacles
+  int rmn[NS];
+  float cmn[NS];
 #pragma unroll
-  for (int s = 0; s < NS; ++s) x[s] = y[s] = gsx[s] = gsy[s] = sq[s] = cin[s] = 0.0;
+  for (int s = 0; s < NS; ++s) {
+    x[s] = y[s] = gsx[s] = gsy[s] = sq[s] = cin[s] = 0.0;
+    rmn[s] = 0x7fefffff;
+    cmn[s] = 3.0e38f;
+  }
+  const double abd2 = (T.a * T.b) * (T.a * T.b);
+  // r^2 of one term, its outside test (obstacle_inside_s), and the running minimum
+  auto inside_t = [&](int s, double2 q) {
+    const double px = x[s] - q.x, py = y[s] - q.y;
+    const double r2 = fma(px, px, py * py);
+    if constexpr (TRACK) rmn[s] = min(rmn[s], __double2hiint(r2));
+    return !(r2 >= abd2);
+  };
   if (valid) {
     if (T.xs) {
 #pragma unroll
@@ -392,7 +440,6 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
 #pragma unroll
   for (int s = 0; s < NS; ++s) srx[s] = sry[s] = sqf[s] = 0.f;
   const float af = (float)T.a, bf = (float)T.b, ab2 = (float)(T.a * T.b * T.a * T.b);
-  const double abd2 = (T.a * T.b) * (T.a * T.b);
   // CULL is a separate instantiation: the culling code compiled into the other
   // kernels costs them registers even unused (c1 +13%)
   if (CULL && js == 1) {
@@ -433,16 +480,37 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
     }
     const float tc = T.tc;
     const int lane = threadIdx.x & 31;
+#if defined(BMPC_CULL_PF) || BMPC_XS32
+    float cxf[NS], cyf[NS];  // fp32 samples for the prefilter (NaN: never decides)
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const bool ok = fabs(x[s]) <= (double)T.lim32 && fabs(y[s]) <= (double)T.lim32;
+      cxf[s] = ok ? __double2float_rn(x[s]) : __int_as_float(0x7fc00000);
+      cyf[s] = __double2float_rn(y[s]);
+    }
+#endif
     for (int c0 = 0; c0 < T.m; c0 += 32) {
       const int jl = c0 + lane;
       bool keep = false;
+      float g2[NS];
+#pragma unroll
+      for (int s = 0; s < NS; ++s) g2[s] = 0.f;
       if (jl < T.m) {
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
           const float4 bo = __ldg(T.box + (k[s] >> 5) * T.m + jl);
           const float gx = fmaxf(fmaxf(bo.x - bx1[s], bx0[s] - bo.y), 0.f);
           const float gy = fmaxf(fmaxf(bo.z - by1[s], by0[s] - bo.w), 0.f);
-          keep |= !(fmaf(gx, gx, gy * gy) >= tc);
+          g2[s] = fmaf(gx, gx, gy * gy);
+          keep |= !(g2[s] >= tc);
+        }
+      }
+      if constexpr (TRACK) {
+        // culled obstacles: every sample of the slot is at least the box gap away
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          const int cg = (jl < T.m && !keep) ? __float_as_int(g2[s]) : 0x7f7fffff;
+          cmn[s] = fminf(cmn[s], __int_as_float(__reduce_min_sync(BMPC_FULL, cg)));
         }
       }
       unsigned bits = __ballot_sync(BMPC_FULL, keep);
@@ -455,25 +523,30 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
           jj[u] = on[u] ? c0 + __ffs(bits) - 1 : 0;
           bits &= bits - 1u;
         }
-#if defined(BMPC_CULL_PF)
-        // survivors through the fp32 prefilter (unstaged predictions): the
-        // pairs take half the registers, the fp64 pair only when undecided
-        if constexpr (!XS) {
+#if defined(BMPC_CULL_PF) || BMPC_XS32
+        // survivors through the fp32 prefilter (unstaged predictions, or the
+        // staged fp32 copies): the pairs take half the registers, the fp64
+        // pair only when undecided
+#ifdef BMPC_CULL_PF
+        constexpr bool kCullPf = !XS || BMPC_XS32;
+#else
+        constexpr bool kCullPf = XS;
+#endif
+        if constexpr (kCullPf) {
           float2 qf[NS][UC];
 #pragma unroll
           for (int u = 0; u < UC; ++u)
 #pragma unroll
             for (int s = 0; s < NS; ++s)
-              qf[s][u] = (on[u] && valid) ? __ldg(T.xf + jj[u] * T.n + k[s]) : make_float2(0.f, 0.f);
+              qf[s][u] = (on[u] && valid) ? ldq<XS>(T.xf + jj[u] * T.n + k[s]) : make_float2(0.f, 0.f);
           if (valid) {
-            const float lim = T.lim32;
 #pragma unroll
             for (int u = 0; u < UC; ++u)
 #pragma unroll
               for (int s = 0; s < NS; ++s) {
-                const bool ok = fabs(x[s]) <= (double)lim && fabs(y[s]) <= (double)lim;
-                const float dx = __double2float_rn(x[s]) - qf[s][u].x, dy = __double2float_rn(y[s]) - qf[s][u].y;
-                if (on[u] && !(ok && fmaf(dx, dx, dy * dy) >= T.t32)) {
+                // cxf is NaN past the prefilter bound: such samples never decide
+                const float dx = cxf[s] - qf[s][u].x, dy = cyf[s] - qf[s][u].y;
+                if (on[u] && !(fmaf(dx, dx, dy * dy) >= T.t32)) {
                   const double2 q = __ldg(T.xi + jj[u] * T.n + k[s]);
                   if (obstacle_inside_s(x[s], y[s], q, abd2)) {
                     if constexpr (F32)
@@ -498,7 +571,7 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
           for (int u = 0; u < UC; ++u)
 #pragma unroll
             for (int s = 0; s < NS; ++s)
-              if (on[u] && obstacle_inside_s(x[s], y[s], q[s][u], abd2)) {
+              if (on[u] && inside_t(s, q[s][u])) {
                 if constexpr (F32)
                   obstacle_term_f32(x[s], y[s], q[s][u], af, bf, ab2, ia, ib, srx[s], sry[s], sqf[s],
                                     cin[s]);
@@ -514,7 +587,7 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
 #ifdef BMPC_NO_PREFILTER
     constexpr bool kFp64Loop = true;
 #else
-    constexpr bool kFp64Loop = XS;
+    constexpr bool kFp64Loop = XS && !BMPC_XS32;
 #endif
     if constexpr (kFp64Loop) {
     // predictions staged in shared memory: the fp64 test straight away (LDS
@@ -551,7 +624,7 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
         for (int u = 0; u < U; ++u)
 #pragma unroll
           for (int s = 0; s < NS; ++s) {
-            in[s][u] = obstacle_inside_s(x[s], y[s], q[s][u], abd2);
+            in[s][u] = inside_t(s, q[s][u]);
             any |= in[s][u];
           }
         if (any) {
@@ -576,7 +649,7 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
         const double2 q = ldq<XS>(qp[s]);
-        if (obstacle_inside_s(x[s], y[s], q, abd2)) {
+        if (inside_t(s, q)) {
           if constexpr (F32)
             obstacle_term_f32(x[s], y[s], q, af, bf, ab2, ia, ib, srx[s], sry[s], sqf[s], cin[s]);
           else
@@ -706,6 +779,25 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
       gsy[0] += __shfl_xor_sync(BMPC_FULL, gsy[0], o);
       sq[0] += __shfl_xor_sync(BMPC_FULL, sq[0], o);
       cin[0] += __shfl_xor_sync(BMPC_FULL, cin[0], o);
+      if constexpr (TRACK) rmn[0] = min(rmn[0], __shfl_xor_sync(BMPC_FULL, rmn[0], o));
+    }
+  }
+  if constexpr (TRACK) {
+    // record the slot's clearances: M0 <= min_j |P0 - Q_j| - ab - slack, every
+    // step rounded down; a sample with an inside (or NaN) term, out of the
+    // coordinate bound, or without clearance never skips (M0^2 stored as -1)
+    if (valid && leader) {
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const float r2f = fminf(__double2float_rd(__hiloint2double(rmn[s], 0)), cmn[s]);
+        // MUFU sqrt (2 ulp) scaled below the true root
+        const float r0 = fminf(__fmul_rd(sqrt_approx(r2f), 1.f - 1e-6f), kSkipMaxM);
+        const float M = __fsub_rd(__fsub_rd(r0, T.ab_ru), kSkipSlack);
+        const float X0 = __double2float_rn(x[s]), Y0 = __double2float_rn(y[s]);
+        const bool ok = M > 0.f && !(cin[s] > 0.0) && fabsf(X0) <= kSkipMaxP0 && fabsf(Y0) <= kSkipMaxP0;
+        T.sk_p0[k[s]] = make_float2(X0, Y0);
+        T.sk_m0[k[s]] = ok ? __fmul_rd(M, M) : -1.f;
+      }
     }
   }
   // P^T sum_j g_j = m (P^T P) c - P^T sum_inside r_j: only samples with an inside
@@ -982,7 +1074,10 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
 #endif
   constexpr int CH = NKM < BMPC_CH ? NKM : BMPC_CH;  // sample slots per pass A / B chunk
 #ifndef BMPC_CHUNK_UNROLL_A
-#define BMPC_CHUNK_UNROLL_A 2  // two pass-A chunks in flight (overlaps one chunk's atan2 with the next one's sampling)
+// chunks stay rolled: the sweep loop must fit the 32 KB instruction cache
+// (two chunks in flight overlapped one chunk's atan2 with the next one's
+// sampling, -1%, but the larger loop cost 2-8% in instruction fetch stalls)
+#define BMPC_CHUNK_UNROLL_A 1
 #endif
 #ifndef BMPC_CHUNK_UNROLL_B
 #define BMPC_CHUNK_UNROLL_B 1
@@ -1051,6 +1146,19 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
   const int scene0 = first_inst / A.l;
   const int img_doubles = C.const_doubles - 3 * NB * npad + kBasisD;  // in shared memory
   double* sXi = sm + img_doubles + (size_t)ipb * bmpc_team_doubles(npad, TW);
+  // clearance skipping (BMPC_SKIP): per warp, behind the staged predictions,
+  // npad (P0.x, P0.y) fp32 pairs and npad squared clearances (am_inst.cu
+  // xs_stage_bytes sizes both)
+  constexpr bool SKIP = BMPC_SKIP && XS && !TEAMS && !F32 && kStoreXY && !BMPC_XS32;
+  float2* sk_p0 = nullptr;
+  float* sk_m0 = nullptr;
+  if constexpr (SKIP) {
+    const int last_inst = min(A.L, first_inst + ipb) - 1;
+    const size_t xb = (size_t)(last_inst / A.l - scene0 + 1) * A.m * n * 16;
+    char* base = reinterpret_cast<char*>(sXi) + xb + (size_t)warp * npad * 12;
+    sk_p0 = reinterpret_cast<float2*>(base);
+    sk_m0 = reinterpret_cast<float*>(base + (size_t)npad * 8);
+  }
   if (threadIdx.x == 0) {
     // fp32 mode: the fp32 basis, then the image past its fp64 basis
     const unsigned bbytes = (unsigned)kBasisD * 8u;
@@ -1058,7 +1166,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
     unsigned xbytes = 0;
     if constexpr (XS) {
       const int last_inst = min(A.L, first_inst + ipb) - 1;
-      xbytes = (unsigned)((last_inst / A.l - scene0 + 1) * A.m * n * 16);
+      xbytes = (unsigned)((last_inst / A.l - scene0 + 1) * A.m * n * (BMPC_XS32 ? 8 : 16));
     }
     mbar_init(&s_cbar, 1);
     mbar_arrive_expect_tx(&s_cbar, bytes + xbytes);
@@ -1070,7 +1178,8 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
     for (unsigned o = bbytes; o < bytes; o += kChunk)
       bulk_copy_g2s(reinterpret_cast<char*>(sm) + o, src1 + (o - bbytes), min(kChunk, bytes - o), &s_cbar);
     if constexpr (XS) {
-      const char* src = reinterpret_cast<const char*>(A.xis) + (size_t)scene0 * A.m * n * 16;
+      const char* src = BMPC_XS32 ? reinterpret_cast<const char*>(A.xs32) + (size_t)scene0 * A.m * n * 8
+                                  : reinterpret_cast<const char*>(A.xis) + (size_t)scene0 * A.m * n * 16;
       for (unsigned o = 0; o < xbytes; o += kChunk)
         bulk_copy_g2s(reinterpret_cast<char*>(sXi) + o, src + o, xbytes - o < kChunk ? xbytes - o : kChunk,
                       &s_cbar);
@@ -1116,9 +1225,11 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
   const double2* __restrict__ xi =
       reinterpret_cast<const double2*>(A.xi) + (size_t)(inst / A.l) * A.m * n;
   const double2* __restrict__ xis =
-      XS ? reinterpret_cast<const double2*>(sXi) + (size_t)(inst / A.l - scene0) * A.m * n
-         : reinterpret_cast<const double2*>(A.xis) + (size_t)(inst / A.l) * A.m * n;
-  const float2* __restrict__ xf = reinterpret_cast<const float2*>(A.xs32) + (size_t)(inst / A.l) * A.m * n;
+      (XS && !BMPC_XS32) ? reinterpret_cast<const double2*>(sXi) + (size_t)(inst / A.l - scene0) * A.m * n
+                         : reinterpret_cast<const double2*>(A.xis) + (size_t)(inst / A.l) * A.m * n;
+  const float2* __restrict__ xf =
+      (XS && BMPC_XS32) ? reinterpret_cast<const float2*>(sXi) + (size_t)(inst / A.l - scene0) * A.m * n
+                        : reinterpret_cast<const float2*>(A.xs32) + (size_t)(inst / A.l) * A.m * n;
   const int m = A.m;
   const double a = A.a, b = A.b, rho = C.rho;
   const double inv_a = 1.0 / a, inv_b = 1.0 / b;
@@ -1321,8 +1432,17 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
   __shared__ int s_poll_next[BMPC_MAX_WARPS];
 #define BMPC_POLL (TEAMS && (A.flags & BMPC_F_POLL) != 0)  // the host sets it only with notconv
   if (BMPC_POLL && lane == 0) s_poll_next[warp] = 0;
+  if constexpr (SKIP) {
+    for (int k = lane; k < npad; k += 32) {  // nothing recorded yet
+      sk_m0[k] = -1.f;
+      sk_p0[k] = make_float2(0.f, 0.f);
+    }
+    __syncwarp();
+  }
   for (int t = 0; t < iters; ++t) {
     const bool last = t == iters - 1;
+    unsigned skipmask = 0;   // slots whose obstacle pass is provably all outside (warp-uniform)
+    unsigned clearbits = 0;  // this lane's samples that passed the clearance test, per slot
     if (BMPC_POLL && wt == 0 && lane == 0 && t > 0) {
       const unsigned sa = (unsigned)__cvta_generic_to_shared(&s_poll[warp][0]);
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n\tcp.async.commit_group;"
@@ -1386,6 +1506,20 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
             yd[s] = fma(pd[s], c.y, yd[s]);
             xdd[s] = fma(pdd[s], c.x, xdd[s]);
             ydd[s] = fma(pdd[s], c.y, ydd[s]);
+          }
+        }
+        if constexpr (SKIP && !BMPC_SKIP_LATE) {
+          // clearance test: moved less than the recorded clearance since the
+          // slot's last obstacle pass (fp32; the slack covers every rounding)
+          const float bf = (float)b, af = (float)a;
+#pragma unroll
+          for (int s = 0; s < NSC; ++s) {
+            // padding samples hold P0 = 0, clearance -1 and never pass; their
+            // lanes are masked after the vote (one vote for all slots, below)
+            const float2 p0 = sk_p0[k[s]];
+            const float dx = fmaf(bf, __double2float_rn(xx[s]), -p0.x);
+            const float dy = fmaf(af, __double2float_rn(yy[s]), -p0.y);
+            if (fmaf(dx, dx, dy * dy) < sk_m0[k[s]] || !v[s]) clearbits |= 1u << (r0 + s);
           }
         }
         double th[NSC];
@@ -1555,6 +1689,28 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
 #pragma unroll 1
         for (; CH > 1 && r0 < NKM; r0 += TW) chunk_a(std::integral_constant<int, 1>{}, r0);  // remainder
       }
+      if constexpr (SKIP && BMPC_SKIP_LATE) {
+        // clearance test after the chunks, on the stored samples (keeps the
+        // chunks' register footprint)
+        const float bf = (float)b, af = (float)a;
+#pragma unroll
+        for (int r = 0; r < NKM; ++r) {
+          const int k = lane + 32 * r;
+          const float2 p0 = sk_p0[k];
+          const float dx = fmaf(bf, __double2float_rn(ws.x[k]), -p0.x);
+          const float dy = fmaf(af, __double2float_rn(ws.y[k]), -p0.y);
+          if (fmaf(dx, dx, dy * dy) < sk_m0[k] || k >= n) clearbits |= 1u << r;
+        }
+      }
+      if constexpr (SKIP) {
+        skipmask = __reduce_and_sync(BMPC_FULL, clearbits);
+#ifdef BMPC_PHASE_PROF
+        if (lane == 0) {  // slots tested / skipped
+          s_prof[warp][14] += nslots;
+          s_prof[warp][15] += __popc(skipmask & ((1u << nslots) - 1u));
+        }
+#endif
+      }
       BMPC_PROF(2);
       // P^T theta of this warp's slots (again after an unwrap)
       auto pt_slots = [&]() {
@@ -1660,7 +1816,44 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
                  __double2float_rd(prefilter_lim(a, b)),
                  CULL ? reinterpret_cast<const float4*>(A.boxes) + (size_t)(inst / A.l) * ((n + 31) >> 5) * m
                       : nullptr,
-                 __double2float_ru((a * b) * (a * b) * (1.0 + 1e-4))};
+                 __double2float_ru((a * b) * (a * b) * (1.0 + 1e-4)), sk_p0, sk_m0, __double2float_ru(a * b)};
+      if constexpr (SKIP) {
+        // only the slots that failed the clearance test (pass A): full slots in
+        // pairs as they come, a leftover one alone; each pass records the
+        // slot's new clearances
+        const unsigned todo = ~skipmask & ((1u << nslots) - 1u);
+        unsigned full = todo & ((1u << sl.F) - 1u);
+#ifndef BMPC_SKIP_NOPAIR
+#define BMPC_SKIP_NOPAIR 1  // no two-slot passes: most slots are skipped, and the sweep code stays small
+#endif
+        if (kPairSlots<NB> && !BMPC_SKIP_NOPAIR) {
+#pragma unroll 1
+          while (full & (full - 1u)) {  // at least two
+            const int ra = __ffs(full) - 1;
+            full &= full - 1u;
+            const int rb = __ffs(full) - 1;
+            full &= full - 1u;
+            const int ks[2] = {lane + 32 * ra, lane + 32 * rb};
+            obstacle_block<2, NB, npad, F32, BMPC_UPAIR, XS, false, CULL, true>(T, ks, 0, 1, 0, true, true, Gx, Gy,
+                                                                                  sqo);
+          }
+        }
+#pragma unroll 1
+        while (full) {
+          const int r = __ffs(full) - 1;
+          full &= full - 1u;
+          const int ks[1] = {lane + 32 * r};
+          obstacle_block<1, NB, npad, F32, BMPC_USINGLE, XS, false, CULL, true>(T, ks, 0, 1, 1, true, true, Gx, Gy,
+                                                                                  sqo);
+        }
+        if (todo >> sl.F) {  // the leftover samples, obstacles split over lane groups (js = g)
+          const Slot S = slot(sl.F, lane, sl);
+          const int ks[1] = {S.k};
+          obstacle_block<1, NB, npad, F32, (NKM >= 7 ? BMPC_USPLIT_MANY : BMPC_USPLIT), XS, false, false, true>(
+              T, ks, S.j0, S.js, sl.g, S.valid, S.leader, Gx, Gy, sqo);
+        }
+        __syncwarp();  // the recorded clearances are read by other lanes in the next sweep's pass A
+      } else {
       int r = wt;  // this warp's slots r = wt, wt + TW, ...
       if (kPairSlots<NB>) {
 #pragma unroll 1
@@ -1679,6 +1872,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
         else  // the leftover samples, obstacles split over lane groups (js = g)
           obstacle_block<1, NB, npad, F32, (NKM >= 7 ? BMPC_USPLIT_MANY : BMPC_USPLIT), XS, false, false>(
               T, ks, S.j0, S.js, sl.g, S.valid, S.leader, Gx, Gy, sqo);
+      }
       }
     }
     BMPC_PROF(5);

@@ -10,7 +10,7 @@ from collections import defaultdict
 from pathlib import Path
 
 rep, obj, func = sys.argv[1:4]
-src = Path("paper_2109_10392_b200/csrc/am_solve_kernel.cuh").read_text().splitlines()
+src = Path(__import__("os").environ.get("KSRC","paper_2109_10392_b200/csrc/am_solve_kernel.cuh")).read_text().splitlines()
 marks = []  # (line, phase) from BMPC_PROF markers: a marker closes the phase above it
 for i, l in enumerate(src, 1):
     m = re.search(r"BMPC_PROF(?:_NS)?\((\d+)\);", l)

@@ -68,3 +68,5 @@ print(f"{args.config} L={W.L} iters={iters} launch {ms:.3f} ms (profiling build)
 for i, name in enumerate(PHASES):
     print(f"  {name:12s} {buf[i] / per:10.1f} cycles/warp/sweep  {100.0 * buf[i] / tot:5.1f}%")
 print(f"  {'total':12s} {tot / per:10.1f}")
+if buf[14]:
+    print(f"  obstacle slots tested {buf[14] / per:.2f} per warp-sweep, skipped {100.0 * buf[15] / buf[14]:.1f}%")
