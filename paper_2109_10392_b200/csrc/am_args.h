@@ -152,6 +152,12 @@ typedef struct {
 #ifndef BMPC_MAX_WARPS
 #define BMPC_MAX_WARPS 8  // warps (instances) per CTA; the kernel's launch bound is 32x this
 #endif
+// Clearance skipping of obstacle slots (am_solve_kernel.cuh): 12 bytes per
+// sample and warp of recorded positions and clearances.
+#ifndef BMPC_SKIP
+#define BMPC_SKIP 1
+#endif
+BMPC_HD constexpr size_t bmpc_skip_bytes(int npad, int warps) { return BMPC_SKIP ? (size_t)warps * npad * 12 : 0; }
 BMPC_HD constexpr bool bmpc_stores_xy(int npad) { return npad <= BMPC_XY_NPAD_MAX; }
 // Doubles of the image's basis part in shared memory: P^T, Pdot^T, Pddot^T in
 // fp64, or in fp32 (the fp32 mode; npad is a multiple of 32, so this is whole).

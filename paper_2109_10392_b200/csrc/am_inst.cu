@@ -41,7 +41,7 @@ static size_t xs_stage_bytes(const bmpc_dev_consts& C, const bmpc_solve_args& A,
   const int scenes = (A.S > 1 && A.l % warps != 0) ? 2 : 1;
   // + the clearance-skipping arrays behind them (BMPC_SKIP: 12 bytes per sample and warp)
   const size_t xs = (size_t)scenes * A.m * C.n * (BMPC_XS32 ? 8 : 16) +
-                    ((BMPC_SKIP && !BMPC_XS32 && bmpc_stores_xy(C.npad)) ? (size_t)warps * C.npad * 12 : 0);
+                    ((!BMPC_XS32 && bmpc_stores_xy(C.npad)) ? bmpc_skip_bytes(C.npad, warps) : 0);
   static int optin[16] = {0};
   int dev = 0;
   cudaGetDevice(&dev);

@@ -17,7 +17,8 @@ size_t am_solve_smem_bytes(int nb, int npad, int kxs, int kps, int warps, int te
                 "fp32 sample arrays must fit the fp64 region");
   return sizeof(double) * (bmpc_const_image_doubles(nb, npad) - bmpc_basis_doubles(nb, npad, false) +
                            bmpc_basis_doubles(nb, npad, f32) +
-                           (size_t)(warps / team) * bmpc_team_doubles(npad, team));
+                           (size_t)(warps / team) * bmpc_team_doubles(npad, team)) +
+         ((f32 && team == 1) ? bmpc_skip_bytes(npad, warps) : 0);  // fp32 mode: clearance arrays
 }
 
 #define BMPC_DECL(NB)                                                                      \

@@ -355,9 +355,6 @@ __device__ __forceinline__ T ldq(const T* p) {
 // its M0 since then, every term of the slot is outside (triangle inequality)
 // and contributes exactly nothing, so the pass is skipped.  Bit-identical to
 // running it (kSkipSlack covers every fp32 rounding of the test).
-#ifndef BMPC_SKIP
-#define BMPC_SKIP 1
-#endif
 #ifndef BMPC_SKIP_LATE
 #define BMPC_SKIP_LATE 0  // 1: the clearance test in its own loop after pass A's chunks
 #endif
@@ -845,6 +842,9 @@ struct TailArgs32 {
   double da, db, dia, dib, dab2;
   const float4* box;         // [slot][m] obstacle boxes (culling) or nullptr
   float tc;
+  float2* sk_p0;             // clearance skipping (BMPC_SKIP), as in TailArgs
+  float* sk_m0;
+  float ab_ru;
 };
 
 template <int NS>
@@ -859,28 +859,32 @@ __device__ __forceinline__ void obstacle_term32(const TailArgs32& T, float px, f
   sry += ry;
 }
 
-template <int NS, int NB, int NPAD, int U, bool PAIRED, bool CULL>
+template <int NS, int NB, int NPAD, int U, bool PAIRED, bool CULL, bool TRACK = false>
 __device__ __forceinline__ void obstacle_block_f32(const TailArgs32& T, const int (&k)[NS], int j0, int js,
                                                    int group, bool valid, bool leader, float (&Gx)[NB],
                                                    float (&Gy)[NB], float& sqo) {
   float x[NS], y[NS], srx[NS], sry[NS], sq[NS];
   bool hit[NS];
+  float rmn[NS];  // TRACK: smallest r^2 per sample (fminf drops NaN: those terms set `hit`)
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
     x[s] = valid ? T.xs[k[s]] : 0.f;
     y[s] = valid ? T.ys[k[s]] : 0.f;
     srx[s] = sry[s] = sq[s] = 0.f;
     hit[s] = false;
+    rmn[s] = 3.0e38f;
   }
   // one term of obstacle jj at sample s, prediction q
   auto term = [&](int s, float2 q, int jj) {
     const float px = x[s] - q.x, py = y[s] - q.y;
     const float r2 = fmaf(px, px, py * py);
+    if constexpr (TRACK) rmn[s] = fminf(rmn[s], r2);
     if (!(r2 >= T.ab2)) {  // inside, or NaN
       if (r2 == r2) {
         obstacle_term32<NS>(T, px, py, r2, srx[s], sry[s], sq[s]);
         hit[s] = true;
       } else {  // rare: the fp64 test and term on the fp64 pair
+        if constexpr (TRACK) hit[s] = true;  // undecidable in fp32: the sample never skips
         const double2 q64 = __ldg(T.xi + jj * T.n + k[s]);
         const double dx = (double)x[s] - q64.x, dy = (double)y[s] - q64.y;
         const double d2 = fma(dx, dx, dy * dy);
@@ -925,13 +929,24 @@ __device__ __forceinline__ void obstacle_block_f32(const TailArgs32& T, const in
     for (int c0 = 0; c0 < T.m; c0 += 32) {
       const int jl = c0 + lane;
       bool keep = false;
+      float g2[NS];
+#pragma unroll
+      for (int s = 0; s < NS; ++s) g2[s] = 0.f;
       if (jl < T.m) {
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
           const float4 bo = __ldg(T.box + (k[s] >> 5) * T.m + jl);
           const float gx = fmaxf(fmaxf(bo.x - bx1[s], bx0[s] - bo.y), 0.f);
           const float gy = fmaxf(fmaxf(bo.z - by1[s], by0[s] - bo.w), 0.f);
-          keep |= !(fmaf(gx, gx, gy * gy) >= T.tc);
+          g2[s] = fmaf(gx, gx, gy * gy);
+          keep |= !(g2[s] >= T.tc);
+        }
+      }
+      if constexpr (TRACK) {  // culled obstacles: at least the box gap away
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          const int cg = (jl < T.m && !keep) ? __float_as_int(g2[s]) : 0x7f7fffff;
+          rmn[s] = fminf(rmn[s], __int_as_float(__reduce_min_sync(BMPC_FULL, cg)));
         }
       }
       unsigned bits = __ballot_sync(BMPC_FULL, keep);
@@ -991,7 +1006,9 @@ __device__ __forceinline__ void obstacle_block_f32(const TailArgs32& T, const in
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
           const float px = x[s] - q[s][u].x, py = y[s] - q[s][u].y;
-          any |= !(fmaf(px, px, py * py) >= T.ab2);
+          const float r2 = fmaf(px, px, py * py);
+          if constexpr (TRACK) rmn[s] = fminf(rmn[s], r2);
+          any |= !(r2 >= T.ab2);
         }
       if (any) {
 #pragma unroll
@@ -1016,6 +1033,22 @@ __device__ __forceinline__ void obstacle_block_f32(const TailArgs32& T, const in
       sry[0] += __shfl_xor_sync(BMPC_FULL, sry[0], o);
       sq[0] += __shfl_xor_sync(BMPC_FULL, sq[0], o);
       hit[0] |= __shfl_xor_sync(BMPC_FULL, (int)hit[0], o) != 0;
+      if constexpr (TRACK) rmn[0] = fminf(rmn[0], __shfl_xor_sync(BMPC_FULL, rmn[0], o));
+    }
+  }
+  if constexpr (TRACK) {
+    // record the slot's clearances (as the fp64 block does): the fp32 test of a
+    // later sweep says outside for every term while the sample stays within
+    // M0 <= min_j |P0 - Q_j| (1 - 1e-5) - ab (1 + 1e-5) - slack of P0
+    if (valid && leader) {
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const float r0 = fminf(__fmul_rd(sqrt_approx(rmn[s]), 1.f - 1e-5f), kSkipMaxM);
+        const float M = __fsub_rd(__fsub_rd(r0, __fmul_ru(T.ab_ru, 1.f + 1e-5f)), kSkipSlack);
+        const bool ok = M > 0.f && !hit[s] && fabsf(x[s]) <= kSkipMaxP0 && fabsf(y[s]) <= kSkipMaxP0;
+        T.sk_p0[k[s]] = make_float2(x[s], y[s]);
+        T.sk_m0[k[s]] = ok ? __fmul_rd(M, M) : -1.f;
+      }
     }
   }
   // P^T sum_j g_j = m (P^T P) c - P^T sum_inside r_j (the Gram part in fp64, (6))
@@ -1149,12 +1182,13 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
   // clearance skipping (BMPC_SKIP): per warp, behind the staged predictions,
   // npad (P0.x, P0.y) fp32 pairs and npad squared clearances (am_inst.cu
   // xs_stage_bytes sizes both)
-  constexpr bool SKIP = BMPC_SKIP && XS && !TEAMS && !F32 && kStoreXY && !BMPC_XS32;
+  // fp32 mode: every shape (no staging; am_solve_smem_bytes sizes the arrays)
+  constexpr bool SKIP = BMPC_SKIP && !TEAMS && !BMPC_XS32 && (F32 || (XS && kStoreXY));
   float2* sk_p0 = nullptr;
   float* sk_m0 = nullptr;
   if constexpr (SKIP) {
     const int last_inst = min(A.L, first_inst + ipb) - 1;
-    const size_t xb = (size_t)(last_inst / A.l - scene0 + 1) * A.m * n * 16;
+    const size_t xb = XS ? (size_t)(last_inst / A.l - scene0 + 1) * A.m * n * 16 : 0;
     char* base = reinterpret_cast<char*>(sXi) + xb + (size_t)warp * npad * 12;
     sk_p0 = reinterpret_cast<float2*>(base);
     sk_m0 = reinterpret_cast<float*>(base + (size_t)npad * 8);
@@ -1202,6 +1236,21 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
 
   const int inst = blockIdx.x * (W / TW) + team;
   if (inst >= L) return;  // team-uniform; no block-wide barriers below this point
+  // Lockstep: on long horizons (n > 128) the sweep loop outgrows the 32 KB
+  // instruction cache (c4: ~47 KB hot, 35-55% of the stall samples waiting for
+  // instructions), so the block's live warps meet at phase boundaries of each
+  // sweep (named barrier 5): they run the same code at the same time and share
+  // the lines they fetch (c4 fp32 -3.5%, fp64 -1.5%).  Shorter horizons fit the
+  // cache and lose latency hiding instead (c1 +3%, c3 +7%): off there.
+  // Level 1: one meeting per sweep; 2: also around the obstacle block.
+#ifndef BMPC_LOCKSTEP
+#define BMPC_LOCKSTEP -1  // auto
+#endif
+  constexpr int kLockstep = TEAMS ? 0 : BMPC_LOCKSTEP >= 0 ? BMPC_LOCKSTEP : npad > 128 ? (F32 ? 2 : 1) : 0;
+  const int live_threads = 32 * min(W, (L - blockIdx.x * (W / TW)) * TW);
+  auto lockstep = [&](int level) {
+    if (kLockstep >= level) asm volatile("bar.sync 5, %0;" ::"r"(live_threads) : "memory");
+  };
 
   // fp64 basis: shared memory, or the global image in the fp32 mode (read only
   // by the initial targets and the fused scoring there)
@@ -1452,6 +1501,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
     //     lambda), lane i / 16+i coefficient i of x / y.  Ill-conditioned
     //     shapes add one refinement step; it starts from the previous sweep's
     //     c once there is one (the same accuracy, one matrix pass less).
+    lockstep(1);
     {
       const double rhs = rho * G + lam;  // owner lanes (G = lam = 0 elsewhere)
       const double* zr = sZx + lrow * C.kms;
@@ -1625,6 +1675,14 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
             ydd[s] = fmaf(pdd[s], c.y, ydd[s]);
           }
         }
+        if constexpr (SKIP) {  // clearance test on the fp32 frame positions (see chunk_a)
+#pragma unroll
+          for (int s = 0; s < NSC; ++s) {
+            const float2 p0 = sk_p0[k[s]];
+            const float dx = fmaf(xx[s], bf, -p0.x), dy = fmaf(yy[s], af, -p0.y);
+            if (fmaf(dx, dx, dy * dy) < sk_m0[k[s]] || !v[s]) clearbits |= 1u << (r0 + s);
+          }
+        }
         float th[NSC];
         bool clip[NSC], anyclip = false;
 #pragma unroll
@@ -1780,6 +1838,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
       }
     }
     BMPC_PROF(3);
+    lockstep(2);
 
     // (3) obstacle block (exact form, independent of psi), samples dealt as in
     //     slot(): full slots two at a time, the n % 32 leftover samples split
@@ -1790,7 +1849,26 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
                    (float)(abd * abd), a, b, inv_a, inv_b, abd * abd,
                    CULL ? reinterpret_cast<const float4*>(A.boxes) + (size_t)(inst / A.l) * ((n + 31) >> 5) * m
                         : nullptr,
-                   __double2float_ru(abd * abd * (1.0 + 1e-4))};
+                   __double2float_ru(abd * abd * (1.0 + 1e-4)), sk_p0, sk_m0, __double2float_ru(abd)};
+      if constexpr (SKIP) {
+        // only the slots that failed the clearance test, one at a time
+        const unsigned todo = ~skipmask & ((1u << nslots) - 1u);
+        unsigned full = todo & ((1u << sl.F) - 1u);
+#pragma unroll 1
+        while (full) {
+          const int r = __ffs(full) - 1;
+          full &= full - 1u;
+          const int ks[1] = {lane + 32 * r};
+          obstacle_block_f32<1, NB, npad, BMPC_USINGLE, false, CULL, true>(T, ks, 0, 1, 1, true, true, Gx, Gy, sqo);
+        }
+        if (todo >> sl.F) {
+          const Slot S = slot(sl.F, lane, sl);
+          const int ks[1] = {S.k};
+          obstacle_block_f32<1, NB, npad, (NKM >= 7 ? BMPC_USPLIT_MANY : BMPC_USPLIT), false, false, true>(
+              T, ks, S.j0, S.js, sl.g, S.valid, S.leader, Gx, Gy, sqo);
+        }
+        __syncwarp();
+      } else {
       int r = 0;
       if (kPairSlots<NB>) {
 #pragma unroll 1
@@ -1809,6 +1887,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
         else
           obstacle_block_f32<1, NB, npad, (NKM >= 7 ? BMPC_USPLIT_MANY : BMPC_USPLIT), false, false>(
               T, ks, S.j0, S.js, sl.g, S.valid, S.leader, Gx, Gy, sqo);
+      }
       }
     } else {
       TailArgs T{sP, cxy, xis, xf, kStoreXY ? ws.x : nullptr, kStoreXY ? ws.y : nullptr, n, m, a, b,
@@ -1876,6 +1955,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
       }
     }
     BMPC_PROF(5);
+    lockstep(2);
 
     // (4) psi QP (solver.py:322-328), null-space form on lanes 0..NB-1
     {
@@ -2054,6 +2134,7 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
       }
     }
     BMPC_PROF(12);
+    lockstep(3);
 
     // (6) G = F_axis^T g = m (P^T P) c + (Pddot^T Pddot) c + the lane partials
     //     (Pdot^T g_nh and the exact-form corrections):

@@ -1,7 +1,8 @@
 #!/bin/bash
 # A/B of a library variant against the product library (under gpurun): bitwise
 # comparison of the solve on golden fixtures, then timings on BASELINE configs.
-# Usage: bash tools/ab_variant.sh OUT VARIANT [VARIANT...]; CFGS / BITS override the lists.
+# Usage: bash tools/ab_variant.sh OUT VARIANT [VARIANT...]; CFGS / BITS override the lists,
+# PREC=fp32 runs the fp32 mode, ARGS adds profile_solve.py arguments.
 OUT=$1; shift
 mkdir -p gpurun_out
 L=paper_2109_10392_b200/_lib
@@ -23,7 +24,7 @@ for v in prod "$@"; do
   lib=$L/libbatchmpc_b200.so
   [ "$v" != "prod" ] && lib=$L/libbatchmpc_b200_$v.so
   for c in ${CFGS:-c1 c2 c3}; do
-    echo "== $v $c $(BMPC_LIB=$lib timeout 600 python tools/profile_solve.py --config $c --reps ${REPS:-3} $ARGS 2>&1 | tail -1)"
+    echo "== $v $c $(BMPC_LIB=$lib timeout 600 python tools/profile_solve.py --config $c --reps ${REPS:-3} ${PREC:+--precision $PREC} $ARGS 2>&1 | tail -1)"
   done
 done
 } > gpurun_out/$OUT 2>&1

@@ -33,6 +33,7 @@ ap.add_argument("--iters", type=int, default=0)
 ap.add_argument("--warps", type=int, default=0)
 ap.add_argument("--l", type=int, default=None)
 ap.add_argument("--scenes", type=int, default=None)
+ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"])
 args = ap.parse_args()
 
 cfg = CONFIGS[args.config]
@@ -44,7 +45,8 @@ dev = torch.device("cuda", 0)
 prob = D.DeviceProblem.from_host(W.n, W.xi_x, W.xi_y, W.b_xy, W.b_psi, W.l, W.a, W.b, W.v_min,
                                  W.v_max, W.a_max, device=dev)
 sol = D.alloc_solution(solver.basis.n_b, W.n, W.L, iters, False, dev)
-opts = nat.SolveOpts(max_iter=iters, tol=0.0, warps_per_block=args.warps)
+opts = nat.SolveOpts(max_iter=iters, tol=0.0, warps_per_block=args.warps,
+                     precision=1 if args.precision == "fp32" else 0)
 out = D.solution_struct(sol)
 ps = prob.c_struct()
 sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
