@@ -524,7 +524,8 @@ def roofline_entry(args, achieved, peak, k_ms, step_ms, n, m, nb):
          "peak_source": "measured live: DFMA microbenchmark (csrc/peak.cu)",
          "note": "frac = canonical algorithmic work per second over the FP64 peak; the kernel "
                  "executes less than W (exact-form obstacle/acceleration blocks: an outside test "
-                 "per obstacle term; obstacles culled by bounding boxes when m >= 24), so frac "
+                 "per obstacle term; obstacles culled by bounding boxes when m >= 24; whole obstacle slots "
+                 "skipped while every sample stays within its recorded clearance), so frac "
                  "can exceed 1 on obstacle-heavy configs; frac_executed is the executed fp64 "
                  "flops over the peak (ncu capture of the same config, profiles/ncu_<config>_"
                  "<precision>.json)"}

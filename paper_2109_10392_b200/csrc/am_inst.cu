@@ -103,7 +103,7 @@ cudaError_t BMPC_CAT(launch_am_nb_, BMPC_INST_NB)(const bmpc_dev_consts& C,
 extern "C" int BMPC_CAT(bmpc_phase_prof_nb, BMPC_INST_NB)(unsigned long long* out, int reset) {
   if (cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(g_phase_cycles)) != cudaSuccess) return 2;
   if (reset) {
-    static const unsigned long long z[16] = {};
+    static const unsigned long long z[20] = {};
     if (cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z)) != cudaSuccess) return 2;
   }
   return 0;

@@ -42,12 +42,12 @@ namespace bmpc {
 // every warp adds the clock64 cycles of each kernel phase to a per-unit
 // device counter.  Compiled out of the product library.
 #ifdef BMPC_PHASE_PROF
-static __device__ unsigned long long g_phase_cycles[16];
-__shared__ unsigned long long s_prof[BMPC_MAX_WARPS][16];
+static __device__ unsigned long long g_phase_cycles[20];
+__shared__ unsigned long long s_prof[BMPC_MAX_WARPS][20];
 __shared__ long long s_prof_t[BMPC_MAX_WARPS];
 #define BMPC_PROF_DECL                                               \
   if ((threadIdx.x & 31) == 0) {                                     \
-    for (int _i = 0; _i < 16; ++_i) s_prof[threadIdx.x >> 5][_i] = 0; \
+    for (int _i = 0; _i < 20; ++_i) s_prof[threadIdx.x >> 5][_i] = 0; \
     s_prof_t[threadIdx.x >> 5] = clock64();                          \
   }
 #define BMPC_PROF(ph)                                                \
@@ -70,7 +70,7 @@ __shared__ long long s_prof_t[BMPC_MAX_WARPS];
   } while (0)
 #define BMPC_PROF_FLUSH                                               \
   if ((threadIdx.x & 31) == 0)                                        \
-    for (int _i = 0; _i < 16; ++_i)                                   \
+    for (int _i = 0; _i < 20; ++_i)                                   \
       atomicAdd(&g_phase_cycles[_i], s_prof[threadIdx.x >> 5][_i]);
 #else
 #define BMPC_PROF_DECL
@@ -1763,9 +1763,24 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
       if constexpr (SKIP) {
         skipmask = __reduce_and_sync(BMPC_FULL, clearbits);
 #ifdef BMPC_PHASE_PROF
-        if (lane == 0) {  // slots tested / skipped
-          s_prof[warp][14] += nslots;
-          s_prof[warp][15] += __popc(skipmask & ((1u << nslots) - 1u));
+        {
+          // slots tested / skipped; failed slots holding a sample that never
+          // skips (inside or touching an obstacle); failing samples
+          unsigned never = 0;
+          int nfail = 0;
+          for (int r = 0; r < nslots; ++r) {
+            const int k = lane + 32 * r;
+            if (k < n && sk_m0[k] < 0.f) never |= 1u << r;
+            if (k < n && !((clearbits >> r) & 1u)) ++nfail;
+          }
+          never = __reduce_or_sync(BMPC_FULL, never);
+          nfail = __reduce_add_sync(BMPC_FULL, nfail);
+          if (lane == 0) {
+            s_prof[warp][14] += nslots;
+            s_prof[warp][15] += __popc(skipmask & ((1u << nslots) - 1u));
+            s_prof[warp][16] += __popc(never & ~skipmask & ((1u << nslots) - 1u));
+            s_prof[warp][17] += nfail;
+          }
         }
 #endif
       }

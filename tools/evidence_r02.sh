@@ -8,7 +8,8 @@ mkdir -p gpurun_out profiles
 timeout 1500 python -m pytest tests -m gpu -q -rf > gpurun_out/pytest_${TAG}.log 2>&1
 tail -2 gpurun_out/pytest_${TAG}.log
 for spec in "c1::" "c2::" "c3::" "c4:--scenes 128:subset: 128 of the 1024 c4 scenes (a full-c4 capture does not finish under ncu replay)" \
-            "c4f32:--scenes 128 --precision fp32:subset: 128 of the 1024 c4 scenes, fp32 mode"; do
+            "c4f32:--scenes 128 --precision fp32:subset: 128 of the 1024 c4 scenes, fp32 mode" \
+            "c1f32:--precision fp32:fp32 mode" "c3f32:--precision fp32:fp32 mode"; do
   cfg=${spec%%:*}; rest=${spec#*:}; args=${rest%%:*}; note=${rest#*:}
   base=${cfg%f32}; prec=fp64; [ "$base" != "$cfg" ] && prec=fp32
   timeout 600 python tools/profile_solve.py --config $base $args > gpurun_out/p_${TAG}_${cfg}.log 2>&1 || { echo "$cfg plain failed"; continue; }
@@ -27,6 +28,8 @@ for cfg in c2 c3 c4; do
   timeout 1200 python bench.py --config $cfg --steps 3 --warmup 3 > gpurun_out/bench_${TAG}_${cfg}.log 2>&1
 done
 timeout 1200 python bench.py --config c4 --precision fp32 --steps 3 --warmup 3 > gpurun_out/bench_${TAG}_c4f32.log 2>&1
+timeout 600 python bench.py --precision fp32 --steps 20 --warmup 3 > gpurun_out/bench_${TAG}_c1f32.log 2>&1
+timeout 900 python bench.py --config c3 --precision fp32 --steps 3 --warmup 3 > gpurun_out/bench_${TAG}_c3f32.log 2>&1
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_${TAG}_ref.log 2>&1
 bash tools/launch_list.sh ${TAG}
 for f in gpurun_out/bench_${TAG}_*.log; do tail -1 $f | cut -c1-160; done

@@ -53,7 +53,7 @@ sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 lib = nat.load()
 rd = getattr(lib, f"bmpc_phase_prof_nb{solver.basis.n_b}")
 rd.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
-buf = (ctypes.c_ulonglong * 16)()
+buf = (ctypes.c_ulonglong * 20)()
 for rep in range(2):  # warm-up, then measured
     assert rd(buf, 1) == 0
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -71,4 +71,5 @@ for i, name in enumerate(PHASES):
     print(f"  {name:12s} {buf[i] / per:10.1f} cycles/warp/sweep  {100.0 * buf[i] / tot:5.1f}%")
 print(f"  {'total':12s} {tot / per:10.1f}")
 if buf[14]:
-    print(f"  obstacle slots tested {buf[14] / per:.2f} per warp-sweep, skipped {100.0 * buf[15] / buf[14]:.1f}%")
+    print(f"  obstacle slots tested {buf[14] / per:.2f} per warp-sweep, skipped {100.0 * buf[15] / buf[14]:.1f}%, "
+          f"failed with a never-skip sample {100.0 * buf[16] / buf[14]:.1f}%, failing samples per warp-sweep {buf[17] / per:.2f}")
