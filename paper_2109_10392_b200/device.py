@@ -83,6 +83,24 @@ class DeviceProblem:
 
         if mn % n:
             raise ValueError(f"obstacle predictions of length {mn} are not a multiple of n={n}")
+        b_xy = np.asarray(b_xy, dtype=np.float64)
+        b_psi = np.asarray(b_psi, dtype=np.float64)
+        parts = (xi_x, xi_y, b_xy, b_psi)
+        if not non_blocking and sum(p.size for p in parts) <= (1 << 19):
+            # small problems (planner-sized batches): one packed copy instead of
+            # four, each part a 16-byte aligned view of the device block
+            offs, tot = [], 0
+            for p in parts:
+                offs.append(tot)
+                tot += (p.size + 1) & ~1
+            host = np.empty(tot)
+            for p, o in zip(parts, offs):
+                host[o:o + p.size] = p.reshape(-1)
+            blk = torch.from_numpy(host).to(dev)
+            v = [blk[o:o + p.size].view(p.shape) for p, o in zip(parts, offs)]
+            return DeviceProblem(m=mn // n, l=int(l), S=S, xi_x=v[0], xi_y=v[1], b_xy=v[2], b_psi=v[3],
+                                 a=float(a), b=float(b), v_min=float(v_min), v_max=float(v_max),
+                                 a_max=float(a_max))
         return DeviceProblem(m=mn // n, l=int(l), S=S, xi_x=up(xi_x), xi_y=up(xi_y),
                              b_xy=up(b_xy), b_psi=up(b_psi), a=float(a), b=float(b),
                              v_min=float(v_min), v_max=float(v_max), a_max=float(a_max))
@@ -102,6 +120,7 @@ class DeviceSolution:
     iterations: int
     converged: bool
     coef: "object" = None  # (6, nb, L): c_x, c_y, c_psi, l_x, l_y, l_psi are its rows
+    block: "object" = None  # (6 nb + 3, L): coef then res_final, one allocation (one copy back)
 
 
 @dataclass
@@ -119,9 +138,11 @@ class DeviceScore:
 def alloc_solution(nb: int, n: int, L: int, max_iter: int, want_v: bool, device) -> DeviceSolution:
     torch = _torch()
     z = lambda *s: torch.empty(*s, dtype=torch.float64, device=device)  # noqa: E731
-    coef = z(6, nb, L)
+    block = z(6 * nb + 3, L)
+    coef = block[: 6 * nb].view(6, nb, L)
     return DeviceSolution(coef[0], coef[1], coef[2], coef[3], coef[4], coef[5],
-                          z(max_iter, 3, L), z(3, L), z(n, L) if want_v else None, 0, False, coef)
+                          z(max_iter, 3, L), block[6 * nb:], z(n, L) if want_v else None, 0, False, coef,
+                          block)
 
 
 def solution_struct(sol: DeviceSolution) -> nat.SolveOut:

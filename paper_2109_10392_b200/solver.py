@@ -120,8 +120,10 @@ class _History(Sequence):
     device history on first access (the list the reference builds eagerly,
     solver.py:432-436)."""
 
-    def __init__(self, dev_hist, iterations):
-        self._dev, self._n, self._rows = dev_hist, iterations, None
+    def __init__(self, dev_hist, iterations, final=None):
+        # final: host copy of the last sweep's residuals (3, L), so reading
+        # history[-1] -- the common case -- does not bring the whole table back
+        self._dev, self._n, self._rows, self._final = dev_hist, iterations, None, final
 
     def _load(self):
         if self._rows is None:
@@ -134,6 +136,10 @@ class _History(Sequence):
         return self._n
 
     def __getitem__(self, i):
+        if (self._rows is None and self._final is not None and isinstance(i, (int, np.integer))
+                and self._n > 0 and i in (-1, self._n - 1)):
+            r = self._final
+            return Residuals(r_obs=r[0].copy(), r_acc=r[1].copy(), r_nonhol=r[2].copy())
         return self._load()[i]
 
     def __repr__(self):
@@ -552,13 +558,18 @@ class BatchSolver:
             sol = self.solve_device(prob, max_iter, tol, wd, keep_multipliers)
         aux = _LazyAux(self, sol, prob)
         n, L, mn = self.basis.grid.n, prob.L, prob.m * self.basis.grid.n
-        coef = sol.coef.cpu().numpy()  # c_x, c_y, c_psi, l_x, l_y, l_psi in one copy
+        nb = self.basis.n_b
+        # c_x, c_y, c_psi, l_x, l_y, l_psi and the final residuals in one copy into
+        # page-locked memory (torch caches the block; pageable copies run at a
+        # tenth of the link rate); the arrays returned are views of it
+        blk = torch.empty(sol.block.shape, dtype=torch.float64, pin_memory=True).copy_(sol.block).numpy()
+        coef, final = blk[: 6 * nb].reshape(6, nb, L), blk[6 * nb:]
         state = AmState(c_x=coef[0], c_y=coef[1], c_psi=coef[2],
                         alpha=_Deferred(aux, "alpha", (mn, L)), d=_Deferred(aux, "d", (mn, L)),
                         alpha_a=_Deferred(aux, "alpha_a", (n, L)), d_a=_Deferred(aux, "d_a", (n, L)),
                         v=_Deferred(aux, "v", (n, L)), lambda_x=coef[3], lambda_y=coef[4],
                         lambda_psi=coef[5], iteration=sol.iterations)
-        return state, SolveInfo(residual_history=_History(sol.history, sol.iterations),
+        return state, SolveInfo(residual_history=_History(sol.history, sol.iterations, final),
                                 iterations=sol.iterations, converged=sol.converged, iterates=iterates)
 
     def check_scenes(self, batch):

@@ -251,6 +251,33 @@ def test_tol_early_stop_semantics(cuda):
     assert info2.iterations == 5 and not info2.converged
 
 
+@pytest.mark.parametrize("mode", ["fixed", "early", "iterates"])
+def test_history_last_row_without_the_table(cuda, mode):
+    """residual_history[-1] comes from the final residuals that travel with the
+    coefficients; it must equal the last row of the device history table."""
+    z = golden("demo")
+    solver = _solver(z)
+    b = _batch(z)
+    tol = 0.0
+    if mode == "early":  # a tolerance the 21st sweep meets
+        _, full = solver.solve(b, max_iter=30, tol=0.0)
+        tol = full.residual_history[20].overall_max() * (1 + 1e-6)
+    kw = dict(fixed=dict(max_iter=30, tol=0.0), early=dict(max_iter=60, tol=tol),
+              iterates=dict(max_iter=6, tol=0.0, record_iterates=True))[mode]
+    _, info = solver.solve(b, **kw)
+    hist = info.residual_history
+    quick = hist[-1]
+    assert hist._rows is None  # the table stayed on the device
+    quick2 = hist[info.iterations - 1]
+    table = hist[0:len(hist)]  # loads every row
+    assert len(table) == info.iterations
+    for q in (quick, quick2):
+        for f in ("r_obs", "r_acc", "r_nonhol"):
+            np.testing.assert_array_equal(getattr(q, f), getattr(table[-1], f))
+    if mode == "early":
+        assert info.converged and info.iterations <= 21 and quick.overall_max() <= tol
+
+
 def test_warm_start_keep_multipliers(cuda):
     import am_oracle as O
 
