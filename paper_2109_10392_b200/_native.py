@@ -113,6 +113,8 @@ EXPORTS = {
     "bmpc_op_d_obs": ([c_int, c_int, c_int] + [c_void_p] * 5 + [c_double, c_double, c_void_p,
                                                                  c_void_p], c_int),
     "bmpc_block_norms": ([c_int, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p], c_int),
+    "bmpc_op_collision_ratios": ([c_int, c_int, c_int] + [c_void_p] * 4 + [c_double, c_double, c_void_p,
+                                                                            c_void_p], c_int),
 }
 
 _lock = threading.Lock()

@@ -78,6 +78,9 @@ cudaError_t op_heading(const bmpc_dev_consts& C, long long L, const double* c_x,
 cudaError_t op_d_obs(int n, long long l, long long mn, const double* x, const double* y,
                      const double* xi_x, const double* xi_y, const double* alpha, double a,
                      double b, double* d, cudaStream_t st);
+cudaError_t op_collision_ratios(int n, long long l, long long mn, const double* x, const double* y,
+                                const double* xi_x, const double* xi_y, double a, double b,
+                                double* out, cudaStream_t st);
 cudaError_t op_block_norms(int n, long long l, long long mn, const double* r_x, const double* r_y,
                            double* out, cudaStream_t st);
 }  // namespace bmpc
@@ -1186,6 +1189,15 @@ int bmpc_op_d_obs(int n, int l, int mn, const double* x, const double* y, const 
                   const double* xi_y, const double* alpha, double a, double b, double* d, void* s) {
   if (n < 1 || l < 0 || mn < 0 || mn % n) return fail(BMPC_EINVAL, "d_obs: bad shape");
   CK(bmpc::op_d_obs(n, l, mn, x, y, xi_x, xi_y, alpha, a, b, d, S_(s)), "d_obs");
+  return BMPC_OK;
+}
+int bmpc_op_collision_ratios(int n, int l, int mn, const double* x, const double* y,
+                             const double* xi_x, const double* xi_y, double a, double b, double* out,
+                             void* s) {
+  if (n < 1 || l < 0 || mn < 0 || mn % n) return fail(BMPC_EINVAL, "collision_ratios: bad shape");
+  if ((long long)mn * l > 0 && (!x || !y || !xi_x || !xi_y || !out))
+    return fail(BMPC_EINVAL, "collision_ratios: null pointer");
+  CK(bmpc::op_collision_ratios(n, l, mn, x, y, xi_x, xi_y, a, b, out, S_(s)), "collision_ratios");
   return BMPC_OK;
 }
 int bmpc_block_norms(int n, int l, int mn, const double* r_x, const double* r_y, double* out,

@@ -144,6 +144,22 @@ __global__ void k_block_norms(int n, long long l, long long mn, const double* __
   }
 }
 
+// Ellipse separation ratios recomputed from positions (planner.py:219-230):
+// out (m*n, l), row j*n + k = sqrt(((x_k - xi_x)/a)^2 + ((y_k - xi_y)/b)^2), every
+// operation rounded on its own as numpy does (no contraction).
+__global__ void k_collision_ratios(int n, long long l, long long mn, const double* __restrict__ x,
+                                   const double* __restrict__ y, const double* __restrict__ xi_x,
+                                   const double* __restrict__ xi_y, double a, double b,
+                                   double* __restrict__ out) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= mn * l) return;
+  const long long row = e / l, c = e - row * l;
+  const long long k = row % n;
+  const double wx = __ddiv_rn(__dsub_rn(x[k * l + c], xi_x[row]), a);
+  const double wy = __ddiv_rn(__dsub_rn(y[k * l + c], xi_y[row]), b);
+  out[e] = __dsqrt_rn(__dadd_rn(__dmul_rn(wx, wx), __dmul_rn(wy, wy)));
+}
+
 static inline int blocks_for(long long n, int tb) { return (int)((n + tb - 1) / tb); }
 
 cudaError_t op_project(const bmpc_dev_consts& C, int mode, int m, long long L, const double* g,
@@ -173,6 +189,13 @@ cudaError_t op_d_obs(int n, long long l, long long mn, const double* x, const do
                      double b, double* d, cudaStream_t st) {
   if (mn * l > 0)
     k_d_obs<<<blocks_for(mn * l, 256), 256, 0, st>>>(n, l, mn, x, y, xi_x, xi_y, alpha, a, b, d);
+  return cudaGetLastError();
+}
+cudaError_t op_collision_ratios(int n, long long l, long long mn, const double* x, const double* y,
+                                const double* xi_x, const double* xi_y, double a, double b,
+                                double* out, cudaStream_t st) {
+  if (mn * l > 0)
+    k_collision_ratios<<<blocks_for(mn * l, 256), 256, 0, st>>>(n, l, mn, x, y, xi_x, xi_y, a, b, out);
   return cudaGetLastError();
 }
 cudaError_t op_block_norms(int n, long long l, long long mn, const double* r_x, const double* r_y,

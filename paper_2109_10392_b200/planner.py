@@ -143,16 +143,21 @@ def collision_ratios(x, y, xi_x, xi_y, a, b):
     """(m*n, l) ellipse separation ratios recomputed from positions (planner.py:219-230)."""
     import torch
 
+    from .device import stream_ptr
+
     A = [torch.as_tensor(np.asarray(t, dtype=np.float64) if not isinstance(t, torch.Tensor) else t)
          for t in (x, y, xi_x, xi_y)]
     host = not A[0].is_cuda
     dev = torch.device("cuda", torch.cuda.current_device())
-    x, y, xi_x, xi_y = (t.to(dev) for t in A)
-    n = x.shape[0]
+    x, y, xi_x, xi_y = (t.to(dev, dtype=torch.float64).contiguous() for t in A)
+    n, l = x.shape
     m = xi_x.shape[0] // n if n else 0
-    wx = (x.repeat(m, 1) - xi_x[:, None]) / a
-    wy = (y.repeat(m, 1) - xi_y[:, None]) / b
-    r = torch.sqrt(wx * wx + wy * wy)
+    r = torch.empty(m * n, l, dtype=torch.float64, device=dev)
+    if n:
+        nat.check(nat.load().bmpc_op_collision_ratios(n, l, m * n, x.data_ptr(), y.data_ptr(),
+                                                      xi_x.data_ptr(), xi_y.data_ptr(), float(a), float(b),
+                                                      r.data_ptr(), ctypes.c_void_p(stream_ptr())),
+                  "collision_ratios")
     return r.cpu().numpy() if host else r
 
 

@@ -147,3 +147,35 @@ def test_device_math(cuda):
     ns, nc = run(3, t(tq))
     np.testing.assert_array_equal(fs.view(np.int64), ns.view(np.int64))
     np.testing.assert_array_equal(fc.view(np.int64), nc.view(np.int64))
+
+
+def test_collision_ratios_bitwise(cuda, rng):
+    """planner.collision_ratios (its own kernel, bmpc_op_collision_ratios) equals
+    the reference's numpy expression (planner.py:219-230) bit for bit, on host
+    arrays and device tensors, with non-finite entries and an empty batch."""
+    import torch
+
+    from paper_2109_10392_b200.planner import collision_ratios
+
+    n, m, l = 37, 5, 19
+    x, y = rng.normal(50, 40, (n, l)), rng.normal(0, 4, (n, l))
+    xi_x, xi_y = rng.normal(50, 40, m * n), rng.normal(0, 4, m * n)
+    x[3, 2], y[5, 7], xi_x[11] = np.nan, np.inf, 1e4
+    xi_x[40:40 + l] = x[40 % n, :l][: min(l, m * n - 40)]  # some exact zeros in wx
+    a, b = 5.6, 2.4
+
+    def ref(x, y):
+        wx = (np.tile(x, (m, 1)) - xi_x[:, None]) / a
+        wy = (np.tile(y, (m, 1)) - xi_y[:, None]) / b
+        return np.sqrt(wx * wx + wy * wy)
+
+    with np.errstate(all="ignore"):
+        want = ref(x, y)
+    got = collision_ratios(x, y, xi_x, xi_y, a, b)
+    assert isinstance(got, np.ndarray) and got.shape == (m * n, l)
+    np.testing.assert_array_equal(got, want)  # exact on every finite entry, NaN where numpy has NaN
+    assert np.isnan(want).any() and np.isinf(want).any()
+    dev = collision_ratios(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), xi_x, xi_y, a, b)
+    assert dev.is_cuda
+    np.testing.assert_array_equal(dev.cpu().numpy(), want)
+    assert collision_ratios(x[:, :0], y[:, :0], xi_x, xi_y, a, b).shape == (m * n, 0)
