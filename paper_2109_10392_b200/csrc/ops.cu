@@ -130,8 +130,12 @@ __global__ void k_residual_vectors(int n, int l, long long mn, const double* __r
 }
 
 // _speedups.pyx:114-218 (with_angles=false) and :221-318 (tail_update, with_angles=true).
-// One thread per instance column walks the rows in the reference's order, so
-// the per-instance squared block sums accumulate in the same sequence.
+// One thread per (row, instance) element: rows [0, mn) are the obstacle terms,
+// rows [mn, mn + n) sample k of the acceleration and the non-holonomic block.
+// Every element's arithmetic is the reference's statement order (compiled with
+// -fmad=false); the per-instance squared block sums are taken afterwards by
+// k_tail_sums from the stored residuals, walking the rows in the reference's
+// order, so they accumulate in the same sequence.
 template <bool WITH_ANGLES>
 __global__ void k_tail(int n, int l, long long mn, const double* __restrict__ x,
                        const double* __restrict__ y, const double* __restrict__ xd,
@@ -143,12 +147,12 @@ __global__ void k_tail(int n, int l, long long mn, const double* __restrict__ x,
                        double* __restrict__ alpha_a, double* __restrict__ d_a,
                        double* __restrict__ v, double* __restrict__ r_x,
                        double* __restrict__ r_y, double* __restrict__ g_x,
-                       double* __restrict__ g_y, double* __restrict__ sq_obs,
-                       double* __restrict__ sq_acc, double* __restrict__ sq_nonhol) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= l) return;
-  double so = 0.0, sa_ = 0.0, sn = 0.0;
-  for (long long row = 0; row < mn; ++row) {
+                       double* __restrict__ g_y) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (mn + n) * l) return;
+  const long long row = t / l;
+  const long long c = t - row * l;
+  if (row < mn) {
     const long long k = row % n;
     const long long e = row * l + c;
     const double wx = x[k * l + c] - xi_x[row];
@@ -168,56 +172,64 @@ __global__ void k_tail(int n, int l, long long mn, const double* __restrict__ x,
     if (dd < 1.0) dd = 1.0;
     d[e] = dd;
     const double adca = a * dd * ca, bdsa = b * dd * sa;
-    const double rx = wx - adca, ry = wy - bdsa;
-    r_x[e] = rx;
-    r_y[e] = ry;
-    so += rx * rx + ry * ry;
+    r_x[e] = wx - adca;
+    r_y[e] = wy - bdsa;
     g_x[e] = xi_x[row] + adca;
     g_y[e] = xi_y[row] + bdsa;
+    return;
   }
-  for (int k = 0; k < n; ++k) {
-    const long long i = (long long)k * l + c;
-    const double ax = xdd[i], ay = ydd[i];
-    const double mag = sqrt(ax * ax + ay * ay);
-    if (WITH_ANGLES) alpha_a[i] = atan2(ay, ax);
-    double caa, saa;
-    if (mag > 0.0) {
-      caa = ax / mag;
-      saa = ay / mag;
-    } else {
-      caa = 1.0;
-      saa = 0.0;
-    }
-    const double dd = mag < a_max ? mag : a_max;
-    d_a[i] = dd;
-    const double daca = dd * caa, dasa = dd * saa;
-    double rx = ax - daca, ry = ay - dasa;
-    const long long ea = (mn + k) * l + c;
-    r_x[ea] = rx;
-    r_y[ea] = ry;
-    sa_ += rx * rx + ry * ry;
-    g_x[ea] = daca;
-    g_y[ea] = dasa;
-    double s = sqrt(xd[i] * xd[i] + yd[i] * yd[i]);
-    if (s < v_min) s = v_min;
-    else if (s > v_max) s = v_max;
-    v[i] = s;
-    const double cp = cos(psi[i]), sp = sin(psi[i]);
-    const double vcp = s * cp, vsp = s * sp;
-    rx = xd[i] - vcp;
-    ry = yd[i] - vsp;
-    const long long en = (mn + n + k) * l + c;
-    r_x[en] = rx;
-    r_y[en] = ry;
-    sn += rx * rx + ry * ry;
-    g_x[en] = vcp;
-    g_y[en] = vsp;
+  const long long k = row - mn;
+  const long long i = k * l + c;
+  const double ax = xdd[i], ay = ydd[i];
+  const double mag = sqrt(ax * ax + ay * ay);
+  if (WITH_ANGLES) alpha_a[i] = atan2(ay, ax);
+  double caa, saa;
+  if (mag > 0.0) {
+    caa = ax / mag;
+    saa = ay / mag;
+  } else {
+    caa = 1.0;
+    saa = 0.0;
   }
-  if (!WITH_ANGLES) {
-    sq_obs[c] = so;
-    sq_acc[c] = sa_;
-    sq_nonhol[c] = sn;
+  const double dd = mag < a_max ? mag : a_max;
+  d_a[i] = dd;
+  const double daca = dd * caa, dasa = dd * saa;
+  const long long ea = (mn + k) * l + c;
+  r_x[ea] = ax - daca;
+  r_y[ea] = ay - dasa;
+  g_x[ea] = daca;
+  g_y[ea] = dasa;
+  double s = sqrt(xd[i] * xd[i] + yd[i] * yd[i]);
+  if (s < v_min) s = v_min;
+  else if (s > v_max) s = v_max;
+  v[i] = s;
+  const double cp = cos(psi[i]), sp = sin(psi[i]);
+  const double vcp = s * cp, vsp = s * sp;
+  const long long en = (mn + n + k) * l + c;
+  r_x[en] = xd[i] - vcp;
+  r_y[en] = yd[i] - vsp;
+  g_x[en] = vcp;
+  g_y[en] = vsp;
+}
+
+// Per-instance squared block sums of tail_core (_speedups.pyx:176, :198, :216):
+// s += rx rx + ry ry over the block's rows in increasing order, one thread per
+// instance column (coalesced across columns).
+__global__ void k_tail_sums(int n, int l, long long mn, const double* __restrict__ r_x,
+                            const double* __restrict__ r_y, double* __restrict__ sq_obs,
+                            double* __restrict__ sq_acc, double* __restrict__ sq_nonhol) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= l) return;
+  const int blk = blockIdx.y;  // 0 obstacle, 1 acceleration, 2 non-holonomic rows
+  const long long r0 = blk == 0 ? 0 : (blk == 1 ? mn : mn + n);
+  const long long r1 = blk == 0 ? mn : (blk == 1 ? mn + n : mn + 2LL * n);
+  double s = 0.0;
+#pragma unroll 8
+  for (long long row = r0; row < r1; ++row) {
+    const double rx = r_x[row * l + c], ry = r_y[row * l + c];
+    s += rx * rx + ry * ry;
   }
+  (blk == 0 ? sq_obs : (blk == 1 ? sq_acc : sq_nonhol))[c] = s;
 }
 
 // ------------------------------------------------------------------ sampling --
@@ -507,16 +519,17 @@ cudaError_t op_tail(bool with_angles, int n, int l, long long mn, const double* 
                     double* g_x, double* g_y, double* sq_obs, double* sq_acc, double* sq_nonhol,
                     cudaStream_t st) {
   if (l <= 0) return cudaSuccess;
-  const int tb = 64;
-  const int grid = (l + tb - 1) / tb;
-  if (with_angles)
-    k_tail<true><<<grid, tb, 0, st>>>(n, l, mn, x, y, xd, yd, xdd, ydd, psi, xi_x, xi_y, v_min, v_max,
-                                      a_max, a, b, alpha, d, alpha_a, d_a, v, r_x, r_y, g_x, g_y,
-                                      sq_obs, sq_acc, sq_nonhol);
-  else
-    k_tail<false><<<grid, tb, 0, st>>>(n, l, mn, x, y, xd, yd, xdd, ydd, psi, xi_x, xi_y, v_min, v_max,
-                                       a_max, a, b, alpha, d, alpha_a, d_a, v, r_x, r_y, g_x, g_y,
-                                       sq_obs, sq_acc, sq_nonhol);
+  const long long tot = (mn + n) * (long long)l;
+  if (with_angles) {
+    k_tail<true><<<nblk(tot), kTB, 0, st>>>(n, l, mn, x, y, xd, yd, xdd, ydd, psi, xi_x, xi_y, v_min,
+                                            v_max, a_max, a, b, alpha, d, alpha_a, d_a, v, r_x, r_y, g_x,
+                                            g_y);
+  } else {
+    k_tail<false><<<nblk(tot), kTB, 0, st>>>(n, l, mn, x, y, xd, yd, xdd, ydd, psi, xi_x, xi_y, v_min,
+                                             v_max, a_max, a, b, alpha, d, alpha_a, d_a, v, r_x, r_y, g_x,
+                                             g_y);
+    k_tail_sums<<<dim3((l + 31) / 32, 3), 32, 0, st>>>(n, l, mn, r_x, r_y, sq_obs, sq_acc, sq_nonhol);
+  }
   return cudaGetLastError();
 }
 cudaError_t op_sample(int n, int npad, int nb, int L, const double* PT, const double* c_x,
