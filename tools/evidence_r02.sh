@@ -7,7 +7,8 @@ TAG=${1:-r02}
 mkdir -p gpurun_out profiles
 timeout 1500 python -m pytest tests -m gpu -q -rf > gpurun_out/pytest_${TAG}.log 2>&1
 tail -2 gpurun_out/pytest_${TAG}.log
-for spec in "c1::" "c2::" "c3::" "c4:--scenes 128:subset: 128 of the 1024 c4 scenes (a full-c4 capture does not finish under ncu replay)" \
+# NONCU=1: skip the ncu captures (the persistent kernel unchanged since the last ones)
+[ -n "$NONCU" ] || for spec in "c1::" "c2::" "c3::" "c4:--scenes 128:subset: 128 of the 1024 c4 scenes (a full-c4 capture does not finish under ncu replay)" \
             "c4f32:--scenes 128 --precision fp32:subset: 128 of the 1024 c4 scenes, fp32 mode" \
             "c1f32:--precision fp32:fp32 mode" "c3f32:--precision fp32:fp32 mode"; do
   cfg=${spec%%:*}; rest=${spec#*:}; args=${rest%%:*}; note=${rest#*:}
