@@ -564,6 +564,13 @@ class BatchSolver:
         # tenth of the link rate); the arrays returned are views of it
         blk = torch.empty(sol.block.shape, dtype=torch.float64, pin_memory=True).copy_(sol.block).numpy()
         coef, final = blk[: 6 * nb].reshape(6, nb, L), blk[6 * nb:]
+        # The reference's QP solves run through scipy's lu_solve (solver.py:166),
+        # whose finite check raises on the first non-finite right-hand side.  A
+        # non-finite right-hand side poisons its instance for good (NaN
+        # coefficients, samples and residuals), so the final residuals tell: the
+        # same error, raised after the solve (3 L values to look at, not the inputs).
+        if not np.isfinite(final).all():
+            raise ValueError("array must not contain infs or NaNs")
         state = AmState(c_x=coef[0], c_y=coef[1], c_psi=coef[2],
                         alpha=_Deferred(aux, "alpha", (mn, L)), d=_Deferred(aux, "d", (mn, L)),
                         alpha_a=_Deferred(aux, "alpha_a", (n, L)), d_a=_Deferred(aux, "d_a", (n, L)),

@@ -644,3 +644,60 @@ def test_repeat_runs_bitwise_deterministic(cuda, name, team):
             assert cuda.equal(getattr(again, k), getattr(ref, k)), k
     again = solver.solve_device(prob, max_iter=30, tol=1e-9, team_warps=team)
     assert again.iterations == tol_ref.iterations and cuda.equal(again.c_x, tol_ref.c_x)
+
+
+@pytest.mark.parametrize("name,where", [("c0", "b_xy"), ("c3f", "b_xy"), ("c0", "xi")])
+def test_nan_stays_in_its_column(cuda, name, where):
+    """Non-finite inputs behave as in the reference's numpy arithmetic: a NaN
+    boundary value poisons exactly its own instance (coefficients NaN, never
+    feasible, numpy's argmin rule picks it as the unfiltered argmin) and every
+    other column keeps its bits; a NaN obstacle sample poisons its scene."""
+    from paper_2109_10392_b200.planner import FilterLimits, MetaCostSpec, plan_batch
+
+    z = golden(name)
+    solver = _solver(z)
+    spec, limits = MetaCostSpec("cruise", v_cruise=20.0), FilterLimits()
+    clean = plan_batch(solver, _Scenes(z), max_iter=20, tol=0.0, spec=spec, limits=limits)
+    sc = _Scenes(z)
+    L = sc.l * sc.S
+    if where == "b_xy":
+        bad = min(5, sc.l - 1)  # an instance of scene 0
+        sc.b_xy = np.array(sc.b_xy, copy=True)
+        sc.b_xy[3, bad] = np.nan
+        res = plan_batch(solver, sc, max_iter=20, tol=0.0, spec=spec, limits=limits)
+        keep = np.arange(L) != bad
+        for k in ("c_x", "c_y", "c_psi"):
+            np.testing.assert_array_equal(getattr(res, k)[:, keep], getattr(clean, k)[:, keep])
+        for k in ("meta_cost", "min_ratio", "heading_max", "flags"):
+            np.testing.assert_array_equal(getattr(res, k)[keep], getattr(clean, k)[keep])
+        # (the coefficients the boundary pins come straight from b; the free ones are NaN)
+        assert np.isnan(res.c_x[:, bad]).any() and np.isnan(res.meta_cost[bad])
+        assert not res.feasible[bad]
+        assert int(res.argmin_all[0]) == bad  # np.argmin returns the first NaN
+        # the filtered winner ignores the poisoned column
+        want = clean.best_index[0]
+        if want == bad:
+            cost = np.where(clean.feasible[:sc.l] & (np.arange(sc.l) != bad), clean.meta_cost[:sc.l], np.inf)
+            want = int(np.argmin(cost)) if np.isfinite(cost).any() else None
+        assert res.best_index[0] == want
+        assert res.best_index[1:] == clean.best_index[1:]
+    else:
+        sc.xi_x = np.array(sc.xi_x, copy=True)
+        sc.xi_x[0, 17] = np.nan  # obstacle 0, sample 17 of scene 0
+        res = plan_batch(solver, sc, max_iter=20, tol=0.0, spec=spec, limits=limits)
+        # every instance of the scene sees the NaN term at sample 17: the reference's
+        # closed forms propagate it into g and the whole column
+        assert np.isnan(res.c_x[:, :sc.l]).any(axis=0).all() and not res.feasible[:sc.l].any()
+        assert res.best_index[0] is None
+    # The reference-shaped BatchSolver.solve keeps the reference's error: its QP
+    # solves go through scipy's lu_solve (solver.py:166), whose finite check
+    # raises ValueError on the first non-finite right-hand side.
+    if sc.S == 1:
+        from paper_2109_10392_b200 import ProblemBatch
+
+        pb = ProblemBatch(l=sc.l, xi_x=sc.xi_x[0], xi_y=sc.xi_y[0], a=sc.a, b=sc.b, v_min=sc.v_min,
+                          v_max=sc.v_max, a_max=sc.a_max, b_xy=sc.b_xy, b_psi=sc.b_psi)
+        with pytest.raises(ValueError, match="infs or NaNs"):
+            solver.solve(pb, max_iter=8, tol=0.0)
+        with pytest.raises(ValueError, match="infs or NaNs"):
+            solver.solve(pb, max_iter=8, tol=1e-3)
