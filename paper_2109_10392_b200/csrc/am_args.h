@@ -90,6 +90,8 @@ typedef struct {
   const double* xis;    // the same pairs in the ellipse frame: (b xi_x, a xi_y)
   const float* xs32;    // those pairs rounded to fp32 (NaN beyond the prefilter bound)
   const float* boxes;   // [S][ceil(n/32)][m] float4 obstacle boxes per sample slot, or NULL
+  float* skipg;         // clearance-skipping scratch in global memory (long horizons, fp64):
+                        // [BMPC_SKIPG_SMS][BMPC_MAX_WARPS][npad] (float2 P0, then float M0^2), or NULL
   const double* b_xy;   // [12][L]
   const double* b_psi;  // [4][L]
   // warm start (BMPC_INIT_WARM), reference AmState layouts (rows, L)
@@ -152,6 +154,7 @@ typedef struct {
 #ifndef BMPC_MAX_WARPS
 #define BMPC_MAX_WARPS 8  // warps (instances) per CTA; the kernel's launch bound is 32x this
 #endif
+#define BMPC_SKIPG_SMS 256  // SM ids covered by the global clearance scratch (a block on a higher id never skips)
 // Clearance skipping of obstacle slots (am_solve_kernel.cuh): 12 bytes per
 // sample and warp of recorded positions and clearances.
 #ifndef BMPC_SKIP

@@ -28,6 +28,19 @@ static cudaError_t launch_t(const bmpc_dev_consts& C, const bmpc_solve_args& A, 
   }
   const int ipb = warps / A.team;  // instances per block
   const int grid = (A.L + ipb - 1) / ipb;
+  if (A.skipg) {
+    // The global clearance scratch is indexed by SM id and warp: valid only
+    // while an SM holds one block of this launch.  Two blocks fit when their
+    // shared memory (+1 KB reserved each) does: then no scratch, no skipping.
+    int per_sm = 0;
+    cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    if (2 * (smem + 1024) <= (size_t)per_sm) {
+      bmpc_solve_args A2 = A;
+      A2.skipg = nullptr;
+      kfn<<<grid, warps * 32, smem, st>>>(C, A2);
+      return cudaGetLastError();
+    }
+  }
   kfn<<<grid, warps * 32, smem, st>>>(C, A);
   return cudaGetLastError();
 }

@@ -369,11 +369,28 @@ __device__ __forceinline__ float sqrt_approx(float x) {
 #ifndef BMPC_PF_SCALE
 #define BMPC_PF_SCALE 1  // obstacles in flight with the prefilter, relative to U (2, 3: slower at c4)
 #endif
-template <int NS, int NB, int NPAD, bool F32, int U, bool XS, bool PAIRED, bool CULL, bool TRACK = false>
+// TESTIN (with TRACK, whole slots): the clearance test runs here, on the
+// positions this pass has just evaluated, against the records in T.sk_p0 /
+// T.sk_m0 (global scratch of the long-horizon kernels, which do not sample
+// x, y in pass A); a slot whose samples are all clear returns before the loop.
+template <int NS, int NB, int NPAD, bool F32, int U, bool XS, bool PAIRED, bool CULL, bool TRACK = false,
+          bool TESTIN = false>
 __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)[NS], int j0, int js,
                                                int group, bool valid, bool leader,
                                                double (&Gx)[NB], double (&Gy)[NB], double& sqo) {
-  static_assert(!TRACK || (XS && !F32 && !BMPC_XS32), "clearance tracking: staged fp64 predictions only");
+  static_assert(!TRACK || (!F32 && !BMPC_XS32 && (XS || CULL)),
+                "clearance tracking: the fp64 loops (staged, or the culling survivors)");
+  static_assert(!TESTIN || (TRACK && NS == 1), "in-pass clearance test: tracked single-slot passes");
+  float2 tp0[NS];
+  float tm0[NS];
+  if constexpr (TESTIN) {  // issued first: the loads fly while x, y are evaluated
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      // (no scratch, e.g. an SM id past its range: nothing recorded, never clear)
+      tp0[s] = T.sk_m0 ? T.sk_p0[k[s]] : make_float2(0.f, 0.f);
+      tm0[s] = T.sk_m0 ? T.sk_m0[k[s]] : -1.f;
+    }
+  }
   double x[NS], y[NS], gsx[NS], gsy[NS], sq[NS];  // gsx, gsy: sum of inside residuals
   double cin[NS];                                   // inside terms per sample
   // TRACK: high word of the smallest r^2 seen per sample (positive doubles order
@@ -428,6 +445,17 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
       y[s] = __dmul_rn(y[s], T.a);
 #endif
     }
+  }
+  if constexpr (TESTIN) {
+    // moved less than the recorded clearance since the slot's last pass (fp32;
+    // kSkipSlack covers every rounding): every term is outside, nothing to add
+    bool clear = true;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const float dx = __double2float_rn(x[s]) - tp0[s].x, dy = __double2float_rn(y[s]) - tp0[s].y;
+      clear &= !valid || fmaf(dx, dx, dy * dy) < tm0[s];
+    }
+    if (__all_sync(BMPC_FULL, clear)) return;
   }
   const double ia = T.ia, ib = T.ib;
   constexpr int UF = U * BMPC_PF_SCALE;
@@ -783,7 +811,7 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
     // record the slot's clearances: M0 <= min_j |P0 - Q_j| - ab - slack, every
     // step rounded down; a sample with an inside (or NaN) term, out of the
     // coordinate bound, or without clearance never skips (M0^2 stored as -1)
-    if (valid && leader) {
+    if (valid && leader && (!TESTIN || T.sk_m0)) {
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
         const float r2f = fminf(__double2float_rd(__hiloint2double(rmn[s], 0)), cmn[s]);
@@ -1184,8 +1212,24 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
   // xs_stage_bytes sizes both)
   // fp32 mode: every shape (no staging; am_solve_smem_bytes sizes the arrays)
   constexpr bool SKIP = BMPC_SKIP && !TEAMS && !BMPC_XS32 && (F32 || (XS && kStoreXY));
+  // Long horizons in fp64 (unstaged predictions, culling; shared memory is
+  // full): the same records in a global scratch indexed by SM and warp (one
+  // block per SM), the test inside the obstacle pass (x, y are evaluated there).
+#ifndef BMPC_SKIPG
+#define BMPC_SKIPG 1
+#endif
+  constexpr bool SKIPG = BMPC_SKIP && BMPC_SKIPG && !SKIP && !TEAMS && !BMPC_XS32 && !F32 && !XS && CULL && !kStoreXY;
   float2* sk_p0 = nullptr;
   float* sk_m0 = nullptr;
+  if constexpr (SKIPG) {
+    unsigned smid;
+    asm("mov.u32 %0, %%smid;" : "=r"(smid));
+    if (A.skipg && smid < BMPC_SKIPG_SMS) {
+      char* base = reinterpret_cast<char*>(A.skipg) + ((size_t)smid * BMPC_MAX_WARPS + warp) * npad * 12;
+      sk_p0 = reinterpret_cast<float2*>(base);
+      sk_m0 = reinterpret_cast<float*>(base + (size_t)npad * 8);
+    }
+  }
   if constexpr (SKIP) {
     const int last_inst = min(A.L, first_inst + ipb) - 1;
     const size_t xb = XS ? (size_t)(last_inst / A.l - scene0 + 1) * A.m * n * 16 : 0;
@@ -1485,6 +1529,15 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
     for (int k = lane; k < npad; k += 32) {  // nothing recorded yet
       sk_m0[k] = -1.f;
       sk_p0[k] = make_float2(0.f, 0.f);
+    }
+    __syncwarp();
+  }
+  if constexpr (SKIPG) {
+    if (sk_m0) {
+      for (int k = lane; k < npad; k += 32) {
+        sk_m0[k] = -1.f;
+        sk_p0[k] = make_float2(0.f, 0.f);
+      }
     }
     __syncwarp();
   }
@@ -1947,6 +2000,21 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
               T, ks, S.j0, S.js, sl.g, S.valid, S.leader, Gx, Gy, sqo);
         }
         __syncwarp();  // the recorded clearances are read by other lanes in the next sweep's pass A
+      } else if constexpr (SKIPG) {
+        // every whole slot takes its pass; the pass tests the slot's recorded
+        // clearances itself and returns early when they all hold
+#pragma unroll 1
+        for (int r = 0; r < sl.F; ++r) {
+          const int ks[1] = {lane + 32 * r};
+          obstacle_block<1, NB, npad, F32, BMPC_USINGLE, XS, false, CULL, SKIPG, SKIPG>(T, ks, 0, 1, 1, true, true,
+                                                                                          Gx, Gy, sqo);
+        }
+        if (sl.R > 0) {  // the leftover samples: split over lane groups, untracked, every sweep
+          const Slot S = slot(sl.F, lane, sl);
+          const int ks[1] = {S.k};
+          obstacle_block<1, NB, npad, F32, (NKM >= 7 ? BMPC_USPLIT_MANY : BMPC_USPLIT), XS, false, false>(
+              T, ks, S.j0, S.js, sl.g, S.valid, S.leader, Gx, Gy, sqo);
+        }
       } else {
       int r = wt;  // this warp's slots r = wt, wt + TW, ...
       if (kPairSlots<NB>) {

@@ -470,9 +470,20 @@ static int auto_warps(const bmpc_ctx* ctx, int L, int req, int team, bool f32) {
 static inline size_t box_offset(size_t tot) { return (5 * tot + 1) & ~(size_t)1; }
 // Bytes of the packed predictions: raw pairs (2 tot doubles), ellipse-frame
 // pairs (2 tot), their fp32 copy (tot), the per-slot obstacle boxes.
+// ... and, for long horizons (n > 128), the clearance-skipping scratch of the
+// unstaged fp64 culling kernels: 12 bytes per sample for every resident warp,
+// indexed by SM and warp (one block per SM there: shared memory is full).
+static inline size_t skip_scratch_offset(const bmpc_problem* p, int n) {  // doubles
+  const size_t tot = (size_t)p->S * p->m * n;
+  return (box_offset(tot) + 2 * (size_t)p->S * ((n + 31) / 32) * p->m + 1) & ~(size_t)1;
+}
+static inline size_t skip_scratch_doubles(int n) {
+  const size_t npad = n <= 224 ? 224 : 256;
+  return n > 128 ? (size_t)BMPC_SKIPG_SMS * BMPC_MAX_WARPS * npad * 12 / 8 : 0;
+}
 static size_t xi_work_bytes(const bmpc_problem* p, int n) {
   const size_t tot = (size_t)p->S * p->m * n;
-  return tot == 0 ? 0 : (box_offset(tot) + 2 * (size_t)p->S * ((n + 31) / 32) * p->m) * sizeof(double);
+  return tot == 0 ? 0 : (skip_scratch_offset(p, n) + skip_scratch_doubles(n)) * sizeof(double);
 }
 
 // Obstacle culling by bounding boxes pays from about two dozen obstacles (c2
@@ -511,6 +522,10 @@ static int launch_sweeps(bmpc_ctx* ctx, const bmpc_problem* p, const double* xi2
   A.xs32 = xi2 ? reinterpret_cast<const float*>(xi2 + 4 * (size_t)p->S * p->m * ctx->C.n) : nullptr;
   A.boxes = (xi2 && use_cull(p, o, extra_flags))
                 ? reinterpret_cast<const float*>(xi2 + box_offset((size_t)p->S * p->m * ctx->C.n))
+                : nullptr;
+  // (only the fp64 culling kernels of long horizons use it)
+  A.skipg = (A.boxes && ctx->C.n > 128 && o->precision == 0)
+                ? reinterpret_cast<float*>(const_cast<double*>(xi2) + skip_scratch_offset(p, ctx->C.n))
                 : nullptr;
   A.b_xy = p->b_xy;
   A.b_psi = p->b_psi;

@@ -22,6 +22,9 @@ SHAPES = [  # (n, t_f, degree, m, l, sweeps)
     (256, 8.0, 9, 6, 12, 25),    # npad 256, no leftover
     (100, 5.0, 10, 0, 20, 30),   # no obstacles (m = 0: no staged predictions)
     (64, 4.0, 7, 3, 3, 30),      # fewer goals than a block's warps
+    # long horizons with culling (m >= 24): clearance records in the global scratch
+    (200, 10.0, 15, 30, 1300, 20),  # full blocks of 8 warps, one block per SM: scratch in use
+    (200, 10.0, 5, 30, 700, 20),    # small basis: several blocks fit an SM, so the launch drops the scratch
 ]
 
 
