@@ -2003,13 +2003,19 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
       } else if constexpr (SKIPG) {
         // every whole slot takes its pass; the pass tests the slot's recorded
         // clearances itself and returns early when they all hold
+#ifndef BMPC_SKIPG_LEFTOVER_CULL
+// 1: the leftover samples through the culling path too (tracked, unsplit): c4
+// 208.2 vs 212.1 ms per 128 scenes, but the unsplit pass sums a sample's
+// inside terms in another order (coefficients move by 1e-7 absolute): off
+#define BMPC_SKIPG_LEFTOVER_CULL 0
+#endif
 #pragma unroll 1
-        for (int r = 0; r < sl.F; ++r) {
+        for (int r = 0; r < (BMPC_SKIPG_LEFTOVER_CULL ? nslots : sl.F); ++r) {
           const int ks[1] = {lane + 32 * r};
-          obstacle_block<1, NB, npad, F32, BMPC_USINGLE, XS, false, CULL, SKIPG, SKIPG>(T, ks, 0, 1, 1, true, true,
-                                                                                          Gx, Gy, sqo);
+          obstacle_block<1, NB, npad, F32, BMPC_USINGLE, XS, false, CULL, SKIPG, SKIPG>(
+              T, ks, 0, 1, 1, BMPC_SKIPG_LEFTOVER_CULL ? ks[0] < n : true, true, Gx, Gy, sqo);
         }
-        if (sl.R > 0) {  // the leftover samples: split over lane groups, untracked, every sweep
+        if (!BMPC_SKIPG_LEFTOVER_CULL && sl.R > 0) {  // the leftover samples: split over lane groups, untracked, every sweep
           const Slot S = slot(sl.F, lane, sl);
           const int ks[1] = {S.k};
           obstacle_block<1, NB, npad, F32, (NKM >= 7 ? BMPC_USPLIT_MANY : BMPC_USPLIT), XS, false, false>(
