@@ -2352,6 +2352,12 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
     if (stop) return;  // an earlier sweep converged everywhere: the re-run takes over
   }
 
+  // The global clearance scratch slot of this warp is reused by the next block
+  // scheduled on this SM, which starts by clearing it: make this warp's last
+  // records land first (they are thousands of cycles old by the time the block
+  // exits; the fence makes it certain).
+  if constexpr (SKIPG) __threadfence();
+
   // ------------------------------------------------- fused planner scoring ----
   // sample_plan + filter_candidates + meta_cost of this instance straight from
   // the on-chip coefficients (planner.py:210-245, :412-423; csrc/score.cuh).
