@@ -366,6 +366,35 @@ __device__ __forceinline__ float sqrt_approx(float x) {
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
+// Warp-wide min / max of a float (no NaN among the inputs) in one REDUX each:
+// floats order like the signed integers key(f) = bits >= 0 ? bits : bits ^
+// 0x7fffffff, and the map is its own inverse.  (-0 sorts below +0; the boxes it
+// feeds only take differences, where the sign of a zero is immaterial.)
+#ifndef BMPC_BOX_REDUX
+#define BMPC_BOX_REDUX 1  // 0: xor-shuffle butterflies
+#endif
+__device__ __forceinline__ int f2key(float f) {
+  const int b = __float_as_int(f);
+  return b >= 0 ? b : b ^ 0x7fffffff;
+}
+__device__ __forceinline__ float warp_fmin(float v) {
+#if BMPC_BOX_REDUX
+  return __int_as_float(f2key(__int_as_float(__reduce_min_sync(BMPC_FULL, f2key(v)))));
+#else
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v = fminf(v, __shfl_xor_sync(BMPC_FULL, v, o));
+  return v;
+#endif
+}
+__device__ __forceinline__ float warp_fmax(float v) {
+#if BMPC_BOX_REDUX
+  return __int_as_float(f2key(__int_as_float(__reduce_max_sync(BMPC_FULL, f2key(v)))));
+#else
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v = fmaxf(v, __shfl_xor_sync(BMPC_FULL, v, o));
+  return v;
+#endif
+}
 #ifndef BMPC_PF_SCALE
 #define BMPC_PF_SCALE 1  // obstacles in flight with the prefilter, relative to U (2, 3: slower at c4)
 #endif
@@ -494,14 +523,7 @@ __device__ __forceinline__ void obstacle_block(const TailArgs& T, const int (&k)
         ly = nan ? -INFINITY : __double2float_rd(y[s]);
         hy = nan ? INFINITY : __double2float_ru(y[s]);
       }
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) {
-        lx = fminf(lx, __shfl_xor_sync(BMPC_FULL, lx, o));
-        hx = fmaxf(hx, __shfl_xor_sync(BMPC_FULL, hx, o));
-        ly = fminf(ly, __shfl_xor_sync(BMPC_FULL, ly, o));
-        hy = fmaxf(hy, __shfl_xor_sync(BMPC_FULL, hy, o));
-      }
-      bx0[s] = lx, bx1[s] = hx, by0[s] = ly, by1[s] = hy;
+      bx0[s] = warp_fmin(lx), bx1[s] = warp_fmax(hx), by0[s] = warp_fmin(ly), by1[s] = warp_fmax(hy);
     }
     const float tc = T.tc;
     const int lane = threadIdx.x & 31;
@@ -944,14 +966,7 @@ __device__ __forceinline__ void obstacle_block_f32(const TailArgs32& T, const in
         ly = nan ? -INFINITY : y[s];
         hy = nan ? INFINITY : y[s];
       }
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) {
-        lx = fminf(lx, __shfl_xor_sync(BMPC_FULL, lx, o));
-        hx = fmaxf(hx, __shfl_xor_sync(BMPC_FULL, hx, o));
-        ly = fminf(ly, __shfl_xor_sync(BMPC_FULL, ly, o));
-        hy = fmaxf(hy, __shfl_xor_sync(BMPC_FULL, hy, o));
-      }
-      bx0[s] = lx, bx1[s] = hx, by0[s] = ly, by1[s] = hy;
+      bx0[s] = warp_fmin(lx), bx1[s] = warp_fmax(hx), by0[s] = warp_fmin(ly), by1[s] = warp_fmax(hy);
     }
     const int lane = threadIdx.x & 31;
     for (int c0 = 0; c0 < T.m; c0 += 32) {
