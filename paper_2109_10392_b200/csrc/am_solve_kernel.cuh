@@ -1569,7 +1569,10 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
     //     lambda), lane i / 16+i coefficient i of x / y.  Ill-conditioned
     //     shapes add one refinement step; it starts from the previous sweep's
     //     c once there is one (the same accuracy, one matrix pass less).
-    lockstep(1);
+#ifndef BMPC_LOCKSTEP_EVERY
+#define BMPC_LOCKSTEP_EVERY 1  // meet every k-th sweep
+#endif
+    if (BMPC_LOCKSTEP_EVERY == 1 || t % BMPC_LOCKSTEP_EVERY == 0) lockstep(1);
     {
       const double rhs = rho * G + lam;  // owner lanes (G = lam = 0 elsewhere)
       const double* zr = sZx + lrow * C.kms;
@@ -2059,7 +2062,10 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
       }
     }
     BMPC_PROF(5);
-    lockstep(2);
+#ifndef BMPC_LS_AFTER_OBST
+#define BMPC_LS_AFTER_OBST 0  // 1: fp64 long horizons also meet after the obstacle block
+#endif
+    lockstep(BMPC_LS_AFTER_OBST && !F32 ? 1 : 2);
 
     // (4) psi QP (solver.py:322-328), null-space form on lanes 0..NB-1
     {
