@@ -81,3 +81,27 @@ def test_shape_parity(cuda, shape):
     assert err[stable].max() <= 1e-8
     hist = np.stack([[h.r_obs, h.r_acc, h.r_nonhol] for h in info.residual_history])
     np.testing.assert_allclose(hist[-1][:, stable], ref["history"][-1][:, stable], rtol=1e-6, atol=1e-9)
+
+
+def test_long_horizon_skipping_equals_no_skipping_bitwise(cuda):
+    """The long-horizon fp64 kernel skips obstacle slots through a global scratch
+    that the launch only hands out when one block fits an SM.  With one warp per
+    block several blocks fit, the scratch is dropped and nothing is skipped: both
+    launches must agree bit for bit (coefficients, multipliers, residuals)."""
+    from paper_2109_10392_b200 import ProblemBatch, make_solver
+
+    # n_b = 10 on 224 padded samples: the constants take ~66 KB and a warp's
+    # scratch 15 KB, so 8 warps per block (185 KB) leave room for one block per
+    # SM, one warp per block (81 KB) for two
+    n, t_f, degree, m, l, sweeps = 200, 10.0, 9, 30, 1300, 40
+    xi_x, xi_y, b_xy, b_psi = _scene(n, t_f, m, l, seed=7, crowd=True)
+    solver = make_solver(n, t_f, degree, m)
+    batch = ProblemBatch(l=l, xi_x=xi_x, xi_y=xi_y, a=5.6, b=2.4, v_min=0.1, v_max=35.0, a_max=8.0,
+                         b_xy=b_xy, b_psi=b_psi)
+    prob = solver.device_problem(batch)
+    full = solver.solve_device(prob, sweeps, 0.0)                      # 8 warps per block: scratch in use
+    single = solver.solve_device(prob, sweeps, 0.0, warps_per_block=1)  # scratch dropped
+    for k in ("c_x", "c_y", "c_psi", "l_x", "l_y", "l_psi", "res_final", "v"):
+        a, b = getattr(full, k).cpu().numpy(), getattr(single, k).cpu().numpy()
+        assert np.array_equal(a, b, equal_nan=True), k
+    np.testing.assert_array_equal(full.history[:sweeps].cpu().numpy(), single.history[:sweeps].cpu().numpy())
