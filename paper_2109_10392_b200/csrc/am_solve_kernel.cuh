@@ -1159,6 +1159,12 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
 #define BMPC_CHUNK_UNROLL_B 1
 #endif
   constexpr int kChunkUnrollA = BMPC_CHUNK_UNROLL_A, kChunkUnrollB = BMPC_CHUNK_UNROLL_B;
+  // Odd slot counts (n_b = 16 at c4: seven slots): the last chunk repeats the
+  // last slot, masked, instead of a separate one-slot body in the hot loop.
+#ifndef BMPC_ODD_DUP
+#define BMPC_ODD_DUP 0
+#endif
+  constexpr bool kOddDup = BMPC_ODD_DUP && !TEAMS && !F32 && CH == 2 && (NKM & 1) && NKM > 2;
   // constant image (am_args.h, capi.cu bmpc_ctx_create)
   // basis rows in paired-slot order when npad is a whole number of slot pairs
   // (bmpc_basis_index); two-slot chunks are then even slot pairs (one warp per
@@ -1610,8 +1616,14 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
         double xx[NSC], yy[NSC], xd[NSC], yd[NSC], xdd[NSC], ydd[NSC];
 #pragma unroll
         for (int s = 0; s < NSC; ++s) {
-          k[s] = lane + 32 * (r0 + s * TW);
-          v[s] = k[s] < n;
+          if constexpr (kOddDup) {  // a slot past the last one repeats it, masked
+            const int r = min(r0 + s * TW, NKM - 1);
+            k[s] = lane + 32 * r;
+            v[s] = k[s] < n && r0 + s * TW < NKM;
+          } else {
+            k[s] = lane + 32 * (r0 + s * TW);
+            v[s] = k[s] < n;
+          }
           xx[s] = yy[s] = xd[s] = yd[s] = xdd[s] = ydd[s] = 0.0;
         }
 #pragma unroll
@@ -1813,10 +1825,15 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
 #pragma unroll 1
         for (; CH > 1 && r0 < NKM; r0 += 1) chunk_a32(std::integral_constant<int, 1>{}, r0);
       } else {
+        if constexpr (kOddDup) {
+#pragma unroll 1
+          for (; r0 < NKM; r0 += CH * TW) chunk_a(std::integral_constant<int, CH>{}, r0);
+        } else {
 #pragma unroll kChunkUnrollA
         for (; r0 + (CH - 1) * TW < NKM; r0 += CH * TW) chunk_a(std::integral_constant<int, CH>{}, r0);
 #pragma unroll 1
         for (; CH > 1 && r0 < NKM; r0 += TW) chunk_a(std::integral_constant<int, 1>{}, r0);  // remainder
+        }
       }
       if constexpr (SKIP && BMPC_SKIP_LATE) {
         // clearance test after the chunks, on the stored samples (keeps the
@@ -2094,8 +2111,14 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
       double ps[NSC];
 #pragma unroll
       for (int s = 0; s < NSC; ++s) {
-        k[s] = lane + 32 * (r0 + s * TW);
-        v[s] = k[s] < n;
+        if constexpr (kOddDup) {
+          const int r = min(r0 + s * TW, NKM - 1);
+          k[s] = lane + 32 * r;
+          v[s] = k[s] < n && r0 + s * TW < NKM;
+        } else {
+          k[s] = lane + 32 * (r0 + s * TW);
+          v[s] = k[s] < n;
+        }
         ps[s] = 0.0;
       }
       // two partial sums per slot: half the dependent chain
@@ -2237,10 +2260,15 @@ __global__ void __launch_bounds__(BMPC_MAXT, TEAMS ? BMPC_TEAM_MINB : BMPC_MINB)
 #pragma unroll 1
         for (; CH > 1 && r0 < NKM; r0 += 1) chunk_b32(std::integral_constant<int, 1>{}, r0);
       } else {
+        if constexpr (kOddDup) {
+#pragma unroll 1
+          for (; r0 < NKM; r0 += CH * TW) chunk_b(std::integral_constant<int, CH>{}, r0);
+        } else {
 #pragma unroll kChunkUnrollB
         for (; r0 + (CH - 1) * TW < NKM; r0 += CH * TW) chunk_b(std::integral_constant<int, CH>{}, r0);
 #pragma unroll 1
         for (; CH > 1 && r0 < NKM; r0 += TW) chunk_b(std::integral_constant<int, 1>{}, r0);
+        }
       }
     }
     BMPC_PROF(12);
